@@ -1,0 +1,111 @@
+"""ctypes binding of the C ABI (include/fkde_gpu.h) in libfkde_b200.so.
+
+The shared library is built in-tree (``python -m paper_2602_10378_b200.build``
+or ``__graft_entry__.build()``).  There is no fallback: if the library is
+missing or cannot load, importing the engine raises ImportError.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libfkde_b200.so")
+
+# fkde_status
+OK = 0
+INVALID_ARGUMENT = 1
+DIMENSION_MISMATCH = 2
+SCORE_UNDERFLOW = 3
+NON_FINITE = 4
+CUDA_ERROR = 5
+NCCL_ERROR = 6
+UNSUPPORTED_D = 7
+NO_DEVICE = 8
+
+KERNEL_GAUSSIAN = 0
+KERNEL_LAPLACE_CORRECTED = 1
+METHOD_KDE, METHOD_SDKDE, METHOD_LAPLACE = 0, 1, 2
+
+OPT_ENGINE, OPT_SPLITS, OPT_TIMING, OPT_MAX_CTAS = 1, 2, 3, 4
+ENGINE_TC, ENGINE_SIMT = 0, 1
+
+T_PREP, T_SCORE, T_FINALIZE, T_GATHER, T_QUERY, T_REDUCE, T_TOTAL, T_COUNT = range(8)
+
+EXPORTED_SYMBOLS = (
+    "fkde_gpu_device_count", "fkde_gpu_create", "fkde_gpu_nccl_unique_id",
+    "fkde_gpu_create_rank", "fkde_gpu_destroy", "fkde_gpu_last_error", "fkde_gpu_set_option",
+    "fkde_gpu_world", "fkde_gpu_stream", "fkde_gpu_last_timing", "fkde_gpu_last_launch_count",
+    "fkde_gpu_score", "fkde_gpu_score_accumulate", "fkde_gpu_kde", "fkde_gpu_sdkde",
+    "fkde_gpu_estimate", "fkde_gpu_pairwise_sq_dists", "fkde_gpu_sdkde_device",
+    "fkde_gpu_kde_device", "fkde_gpu_shard_range",
+)
+
+_lib = None
+
+_dp = ctypes.POINTER(ctypes.c_double)
+_sz = ctypes.c_size_t
+_szp = ctypes.POINTER(ctypes.c_size_t)
+_vp = ctypes.c_void_p
+
+
+def _declare(lib):
+    lib.fkde_gpu_device_count.argtypes = [ctypes.POINTER(ctypes.c_int)]
+    lib.fkde_gpu_create.argtypes = [ctypes.POINTER(ctypes.c_int), ctypes.c_int,
+                                    ctypes.POINTER(_vp)]
+    lib.fkde_gpu_nccl_unique_id.argtypes = [ctypes.c_char_p]
+    lib.fkde_gpu_create_rank.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                         ctypes.c_char_p, ctypes.POINTER(_vp)]
+    lib.fkde_gpu_destroy.argtypes = [_vp]
+    lib.fkde_gpu_destroy.restype = None
+    lib.fkde_gpu_last_error.argtypes = [_vp]
+    lib.fkde_gpu_last_error.restype = ctypes.c_char_p
+    lib.fkde_gpu_set_option.argtypes = [_vp, ctypes.c_int, ctypes.c_int64]
+    lib.fkde_gpu_world.argtypes = [_vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
+    lib.fkde_gpu_stream.argtypes = [_vp]
+    lib.fkde_gpu_stream.restype = _vp
+    lib.fkde_gpu_last_timing.argtypes = [_vp, ctypes.POINTER(ctypes.c_float), ctypes.c_int]
+    lib.fkde_gpu_last_launch_count.argtypes = [_vp]
+    lib.fkde_gpu_last_launch_count.restype = ctypes.c_int64
+    lib.fkde_gpu_score.argtypes = [_vp, _dp, _sz, _sz, ctypes.c_double, _dp, _szp]
+    lib.fkde_gpu_score_accumulate.argtypes = [_vp, _dp, _sz, _sz, ctypes.c_double, _dp, _dp]
+    lib.fkde_gpu_kde.argtypes = [_vp, _dp, _sz, _dp, _sz, _sz, ctypes.c_double, ctypes.c_int,
+                                 ctypes.c_int, _dp]
+    lib.fkde_gpu_sdkde.argtypes = [_vp, _dp, _sz, _dp, _sz, _sz, ctypes.c_double, ctypes.c_double,
+                                   _dp, _dp, _szp]
+    lib.fkde_gpu_estimate.argtypes = [_vp, _dp, _sz, _dp, _sz, _sz, ctypes.c_int, ctypes.c_double,
+                                      ctypes.c_double, _sz, _sz, ctypes.c_int, _dp, _dp, _dp, _szp]
+    lib.fkde_gpu_pairwise_sq_dists.argtypes = [_vp, _dp, _sz, _dp, _sz, _sz, _dp]
+    lib.fkde_gpu_sdkde_device.argtypes = [_vp, _vp, _sz, _vp, _sz, _sz, ctypes.c_double,
+                                          ctypes.c_double, _vp]
+    lib.fkde_gpu_kde_device.argtypes = [_vp, _vp, _sz, _vp, _sz, _sz, ctypes.c_double,
+                                        ctypes.c_int, ctypes.c_int, _vp]
+    lib.fkde_gpu_shard_range.argtypes = [_sz, ctypes.c_int, ctypes.c_int, _sz, _szp, _szp, _szp]
+    return lib
+
+
+def shard_range(n: int, world: int, rank: int, align: int = 1):
+    """(begin, rows, chunk) of rank's slice -- the engine's own partition."""
+    lib = load()
+    b, r, c = ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_size_t()
+    rc = lib.fkde_gpu_shard_range(n, world, rank, align, ctypes.byref(b), ctypes.byref(r),
+                                  ctypes.byref(c))
+    if rc != OK:
+        raise ValueError(f"fkde_gpu_shard_range({n}, {world}, {rank}, {align}) -> {rc}")
+    return b.value, r.value, c.value
+
+
+def load():
+    """Load libfkde_b200.so (raises ImportError loudly if absent)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} not found: build the CUDA extension first "
+                "(python -c 'import __graft_entry__ as g; g.build()')")
+        _lib = _declare(ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL))
+    return _lib
+
+
+def loaded_path() -> str:
+    return LIB_PATH

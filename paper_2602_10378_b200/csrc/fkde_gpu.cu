@@ -1,0 +1,1114 @@
+// fkde_gpu.cu -- runtime + C ABI of the B200-native Flash-SD-KDE engine.
+//
+// Implements include/fkde_gpu.h.  The estimator pipeline of the reference
+// (fkde::engine::sdkde_flash, engine.cpp:389-405) runs per device as:
+//
+//   H2D -> column mean (centring) -> operand scale -> pack A/B tiles
+//   -> pairwise_tc_kernel<Score>     (rows sharded across ranks)
+//   -> finalize_score (s, x + h^2/2 s)
+//   -> ncclAllGather(x_sd)           (only when world > 1)
+//   -> pack -> pairwise_tc_kernel<Gauss|Laplace> (queries sharded)
+//   -> reduce_density -> ncclAllGather(densities) -> D2H
+//
+// Single process: one host thread per device (ncclCommInitAll).  One process
+// per GPU: fkde_gpu_create_rank (ncclCommInitRank with a caller-broadcast id).
+// NCCL is loaded lazily with dlopen so that single-GPU use has no NCCL
+// dependency and a process that already loaded torch's NCCL reuses it.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/fkde_gpu.h"
+#include "layout.cuh"
+#include "pairwise_simt.cuh"
+#include "pairwise_tc.cuh"
+#include "prep_kernels.cuh"
+
+using namespace fkde_b200;
+
+namespace {
+
+// --------------------------------------------------------------------------
+// NCCL (dlopen)
+// --------------------------------------------------------------------------
+struct NcclApi {
+    bool loaded = false;
+    std::string err;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        const char* names[] = {"libnccl.so.2", "libnccl.so"};
+        void* h = nullptr;
+        for (const char* nm : names) {
+            h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+            if (h) break;
+        }
+        if (!h) {
+            api.err = std::string("cannot dlopen libnccl.so.2: ") + dlerror();
+            return;
+        }
+        api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+        api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+        api.CommInitAll = (decltype(api.CommInitAll))dlsym(h, "ncclCommInitAll");
+        api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+        api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
+        api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+        api.loaded = api.GetUniqueId && api.CommInitRank && api.CommInitAll && api.CommDestroy &&
+                     api.AllGather && api.GetErrorString;
+        if (!api.loaded) api.err = "libnccl.so.2 lacks required symbols";
+    });
+    return api;
+}
+
+// --------------------------------------------------------------------------
+// errors
+// --------------------------------------------------------------------------
+struct Status {
+    int code = FKDE_OK;
+    std::string msg;
+    size_t index = 0;
+    bool ok() const { return code == FKDE_OK; }
+};
+
+Status make_status(int code, const char* fmt, ...) {
+    Status s;
+    s.code = code;
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    s.msg = buf;
+    return s;
+}
+
+#define CUDA_TRY(expr)                                                                         \
+    do {                                                                                       \
+        cudaError_t e__ = (expr);                                                              \
+        if (e__ != cudaSuccess)                                                                \
+            return make_status(FKDE_CUDA_ERROR, "%s failed: %s (%s:%d)", #expr,                \
+                               cudaGetErrorString(e__), __FILE__, __LINE__);                   \
+    } while (0)
+
+#define NCCL_TRY(expr)                                                                         \
+    do {                                                                                       \
+        ncclResult_t r__ = (expr);                                                             \
+        if (r__ != ncclSuccess)                                                                \
+            return make_status(FKDE_NCCL_ERROR, "%s failed: %s", #expr,                        \
+                               nccl().GetErrorString(r__));                                    \
+    } while (0)
+
+#define STATUS_TRY(expr)            \
+    do {                            \
+        Status s__ = (expr);        \
+        if (!s__.ok()) return s__;  \
+    } while (0)
+
+// --------------------------------------------------------------------------
+// device state
+// --------------------------------------------------------------------------
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    template <typename T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+Status ensure(DevBuf& b, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    if (b.bytes >= bytes) return {};
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+    const size_t want = round_up(bytes + bytes / 8, 1 << 20);  // grow with headroom
+    CUDA_TRY(cudaMalloc(&b.p, want));
+    b.bytes = want;
+    return {};
+}
+
+struct Options {
+    int engine = FKDE_ENGINE_TC;
+    int splits = 0;
+    int timing = 0;
+    int max_ctas = 0;
+};
+
+struct Device {
+    int dev = 0;
+    int rank = 0;
+    int world = 1;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    ncclComm_t comm = nullptr;
+    bool attrs_set = false;
+    DevBuf X, Y, opA, opB, part0, part1, xsd, out, aux0, aux1, colpart, scal, err, flags;
+    cudaEvent_t ev[FKDE_T_COUNT + 1] = {};
+    int64_t launches = 0;
+    float timing[FKDE_T_COUNT] = {};
+    Status last;
+};
+
+}  // namespace
+
+struct fkde_gpu_ctx {
+    std::vector<Device> devs;
+    int world = 1;
+    bool per_rank = false;  // one process per GPU
+    Options opt;
+    std::string err;
+    std::mutex mu;
+};
+
+namespace {
+
+Status set_error(fkde_gpu_ctx* ctx, Status s) {
+    if (ctx) ctx->err = s.msg;
+    return s;
+}
+
+// shard [r*chunk, min(n,(r+1)*chunk)) with chunk = ceil(n/world): equal-size
+// allgather slices (the tail slice is padding).
+struct Shard {
+    size_t chunk, begin, rows;
+};
+Shard shard_of(size_t n, int world, int rank, size_t align = 1) {
+    Shard s;
+    s.chunk = round_up((n + world - 1) / world, align);
+    s.begin = std::min(n, s.chunk * rank);
+    s.rows = std::min(n, s.begin + s.chunk) - s.begin;
+    return s;
+}
+
+int choose_splits(const Options& o, size_t row_tiles, size_t col_tiles, int ctas) {
+    if (o.splits > 0) return static_cast<int>(std::min<size_t>(o.splits, col_tiles));
+    // minimise rounds * (tiles per unit + pipeline fill) over S in [1, min(col_tiles, 64)]
+    double best = 1e300;
+    int best_s = 1;
+    const size_t smax = std::min<size_t>(col_tiles, 64);
+    for (size_t s = 1; s <= smax; ++s) {
+        const size_t units = row_tiles * s;
+        const size_t rounds = (units + ctas - 1) / ctas;
+        const double per_unit = static_cast<double>((col_tiles + s - 1) / s) + 2.0;
+        const double t = static_cast<double>(rounds) * per_unit;
+        if (t < best * 0.999) {
+            best = t;
+            best_s = static_cast<int>(s);
+        }
+    }
+    return best_s;
+}
+
+template <int MODE>
+Status launch_pairwise(Device& D, const Options& o, const PairArgs& a, size_t n_cols) {
+    if (o.engine == FKDE_ENGINE_SIMT) {
+        pairwise_simt_kernel<MODE><<<a.n_row_tiles, 128, 0, D.stream>>>(a, n_cols);
+    } else {
+        using Cfg = TcConfig<MODE>;
+        static thread_local int attr_done_dev[64] = {};
+        if (!(attr_done_dev[D.dev & 63] & (1 << MODE))) {
+            CUDA_TRY(cudaFuncSetAttribute(pairwise_tc_kernel<MODE>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          Cfg::kSmemBytes));
+            attr_done_dev[D.dev & 63] |= 1 << MODE;
+        }
+        const int units = a.n_row_tiles * a.splits;
+        int grid = std::min(units, D.num_sms);
+        if (o.max_ctas > 0) grid = std::min(grid, o.max_ctas);
+        pairwise_tc_kernel<MODE><<<grid, Cfg::kThreads, Cfg::kSmemBytes, D.stream>>>(a);
+    }
+    ++D.launches;
+    CUDA_TRY(cudaGetLastError());
+    return {};
+}
+
+inline unsigned grid1(size_t n, unsigned bs) { return static_cast<unsigned>((n + bs - 1) / bs); }
+
+void record(Device& D, const Options& o, int idx) {
+    if (o.timing) cudaEventRecord(D.ev[idx], D.stream);
+}
+
+// ---- building blocks ------------------------------------------------------------
+// mean of X (n x d) into sc->mu; also zero-initialises sc.
+Status compute_mean(Device& D, const double* dX, size_t n, int d, PassScalars* sc) {
+    CUDA_TRY(cudaMemsetAsync(sc, 0, sizeof(PassScalars), D.stream));
+    const int nparts = static_cast<int>(std::min<size_t>(256, std::max<size_t>(1, n / 64)));
+    STATUS_TRY(ensure(D.colpart, nparts * 16 * sizeof(double)));
+    colsum_stage1<<<nparts, 256, 0, D.stream>>>(dX, n, d, D.colpart.as<double>(), sc);
+    colsum_stage2<<<1, 16, 0, D.stream>>>(D.colpart.as<double>(), nparts, n, d, sc);
+    D.launches += 2;
+    CUDA_TRY(cudaGetLastError());
+    return {};
+}
+
+Status pack(Device& D, const double* x, size_t rows, int d, int format, bool center, double k,
+            const PassScalars* sc, DevBuf& out, size_t* rows_padded) {
+    const size_t rp = round_up(std::max<size_t>(rows, 1), kTileRows);
+    STATUS_TRY(ensure(out, rp * kRowBytes));
+    PackArgs a;
+    a.x = x;
+    a.rows = rows;
+    a.rows_padded = rp;
+    a.d = d;
+    a.format = format;
+    a.center = center ? 1 : 0;
+    a.k = k;
+    a.sc = sc;
+    a.out = out.as<uint4>();
+    pack_operands<<<grid1(rp, 128), 128, 0, D.stream>>>(a);
+    ++D.launches;
+    CUDA_TRY(cudaGetLastError());
+    *rows_padded = rp;
+    return {};
+}
+
+// one pairwise pass over (row operand x column operand) with density partials
+Status density_pass(Device& D, const Options& o, int mode, size_t rows_pad, size_t n_cols,
+                    const PassScalars* sc, int* nparts_out) {
+    const size_t rt = rows_pad / kTileRows;
+    const size_t ct = round_up(n_cols, kTileRows) / kTileRows;
+    int splits = o.engine == FKDE_ENGINE_SIMT ? 1
+                                              : choose_splits(o, rt, ct, o.max_ctas > 0
+                                                                             ? std::min(o.max_ctas, D.num_sms)
+                                                                             : D.num_sms);
+    const size_t nparts = static_cast<size_t>(splits) * 2;
+    STATUS_TRY(ensure(D.part0, nparts * rows_pad * sizeof(float)));
+    if (mode == kModeLaplace) STATUS_TRY(ensure(D.part1, nparts * rows_pad * sizeof(float)));
+    PairArgs a;
+    a.opA = D.opA.as<uint8_t>();
+    a.opB = D.opB.as<uint8_t>();
+    a.n_row_tiles = static_cast<int>(rt);
+    a.n_col_tiles = static_cast<int>(ct);
+    a.splits = splits;
+    a.sc = sc;
+    a.part0 = D.part0.as<float>();
+    a.part1 = mode == kModeLaplace ? D.part1.as<float>() : nullptr;
+    a.rows_pad = rows_pad;
+    a.diag_tile0 = -1;
+    if (mode == kModeGauss)
+        STATUS_TRY(launch_pairwise<kModeGauss>(D, o, a, n_cols));
+    else
+        STATUS_TRY(launch_pairwise<kModeLaplace>(D, o, a, n_cols));
+    *nparts_out = static_cast<int>(nparts);
+    return {};
+}
+
+// flag list for exact_rows_fp64: [0] = count, [1..] = local row indices
+Status prepare_flags(Device& D, size_t rows) {
+    STATUS_TRY(ensure(D.flags, (rows + 1) * sizeof(unsigned int)));
+    CUDA_TRY(cudaMemsetAsync(D.flags.p, 0, sizeof(unsigned int), D.stream));
+    return {};
+}
+
+Status launch_exact(Device& D, const ExactArgs& e) {
+    exact_rows_fp64<<<2 * D.num_sms, 256, 0, D.stream>>>(e);
+    ++D.launches;
+    CUDA_TRY(cudaGetLastError());
+    return {};
+}
+
+Status allgather(Device& D, void* buf, size_t count_per_rank, ncclDataType_t t) {
+    if (D.world <= 1) return {};
+    const size_t elt = t == ncclFloat64 ? 8 : 4;
+    char* base = static_cast<char*>(buf);
+    NCCL_TRY(nccl().AllGather(base + D.rank * count_per_rank * elt, buf, count_per_rank, t, D.comm,
+                              D.stream));
+    return {};
+}
+
+// ---- per-device programs ---------------------------------------------------------------
+struct Job {
+    enum Kind { kScore, kScoreAcc, kKde, kSdkde, kDist } kind;
+    // host (h*) or device (d*) inputs
+    const double* hX = nullptr;
+    const double* hY = nullptr;
+    const double* dX = nullptr;
+    const double* dY = nullptr;
+    size_t n = 0, m = 0;
+    int d = 0;
+    double h = 1.0, h_score = 1.0;
+    int kernel = FKDE_KERNEL_GAUSSIAN;
+    int fused = 1;
+    // host outputs (only device 0 / every rank writes them)
+    double* out = nullptr;       // densities [m] | scores [n*d] | phi_sum [n]
+    double* out2 = nullptr;      // debiased [n*d] | weighted [n*d]
+    double* d_out = nullptr;     // device output (device-resident API)
+    bool sync = true;
+};
+
+// Score pass on this rank's row shard; leaves the requested per-row outputs in
+// D.aux0 / D.aux1 / D.xsd in global row layout (gathered when world > 1).
+Status score_program(Device& D, const Options& o, const Job& J, const double* dX,
+                     PassScalars* sc, bool want_xsd) {
+    const int d = J.d;
+    const size_t n = J.n;
+    const double ks = std::sqrt(kLog2e) / J.h_score;
+    STATUS_TRY(compute_mean(D, dX, n, d, sc));
+    max_half_norm<<<grid1(n, 256), 256, 0, D.stream>>>(dX, n, d, ks, sc, sc);
+    set_scale_exponent<<<1, 1, 0, D.stream>>>(sc);
+    D.launches += 2;
+    // row shards start on a tile boundary so the diagonal is tile aligned
+    const Shard sh = shard_of(n, D.world, D.rank, kTileRows);
+    size_t rows_pad = 0, cols_pad = 0;
+    STATUS_TRY(pack(D, dX + sh.begin * d, sh.rows, d, 0, true, ks, sc, D.opA, &rows_pad));
+    STATUS_TRY(pack(D, dX, n, d, 1, true, ks, sc, D.opB, &cols_pad));
+    record(D, o, FKDE_T_SCORE);
+
+    const size_t rt = rows_pad / kTileRows, ct = cols_pad / kTileRows;
+    const int ctas = o.max_ctas > 0 ? std::min(o.max_ctas, D.num_sms) : D.num_sms;
+    const int splits = o.engine == FKDE_ENGINE_SIMT ? 1 : choose_splits(o, rt, ct, ctas);
+    STATUS_TRY(ensure(D.part0, static_cast<size_t>(splits) * rows_pad * sizeof(float)));
+    STATUS_TRY(ensure(D.part1, static_cast<size_t>(splits) * rows_pad * kMaxDim * sizeof(float)));
+    PairArgs a;
+    a.opA = D.opA.as<uint8_t>();
+    a.opB = D.opB.as<uint8_t>();
+    a.n_row_tiles = static_cast<int>(rt);
+    a.n_col_tiles = static_cast<int>(ct);
+    a.splits = splits;
+    a.sc = sc;
+    a.part0 = D.part0.as<float>();
+    a.part1 = D.part1.as<float>();
+    a.rows_pad = rows_pad;
+    a.diag_tile0 = static_cast<int>(sh.begin / kTileRows);
+    STATUS_TRY(launch_pairwise<kModeScore>(D, o, a, n));
+    record(D, o, FKDE_T_FINALIZE);
+
+    const size_t nrows_g = sh.chunk * D.world;  // gather layout
+    FinalizeArgs f{};
+    f.part_s = D.part0.as<float>();
+    f.part_t = D.part1.as<float>();
+    f.splits = splits;
+    f.rows_pad = rows_pad;
+    f.rows = sh.rows;
+    f.row0 = sh.begin;
+    f.d = d;
+    f.x = dX;
+    f.sc = sc;
+    f.k = ks;
+    f.h_score = J.h_score;
+    f.shift = 0.5 * J.h * J.h;
+    STATUS_TRY(ensure(D.err, sizeof(unsigned long long)));
+    CUDA_TRY(cudaMemsetAsync(D.err.p, 0xFF, sizeof(unsigned long long), D.stream));
+    f.underflow_row = D.err.as<unsigned long long>();
+    if (J.kind == Job::kScore) {
+        STATUS_TRY(ensure(D.aux0, nrows_g * d * sizeof(double)));
+        f.score = D.aux0.as<double>();
+    } else if (J.kind == Job::kScoreAcc) {
+        STATUS_TRY(ensure(D.aux0, nrows_g * sizeof(double)));
+        STATUS_TRY(ensure(D.aux1, nrows_g * d * sizeof(double)));
+        f.phi_sum = D.aux0.as<double>();
+        f.weighted = D.aux1.as<double>();
+    }
+    if (want_xsd) {
+        STATUS_TRY(ensure(D.xsd, nrows_g * d * sizeof(double)));
+        f.xsd_c = D.xsd.as<double>();
+    }
+    STATUS_TRY(prepare_flags(D, sh.rows));
+    f.flag_count = D.flags.as<unsigned int>();
+    f.flag_rows = f.flag_count + 1;
+    finalize_score<<<grid1(std::max<size_t>(sh.rows, 1), 128), 128, 0, D.stream>>>(f);
+    ++D.launches;
+    CUDA_TRY(cudaGetLastError());
+    {
+        ExactArgs e{};
+        e.mode = kExactScore;
+        e.count = f.flag_count;
+        e.rows = f.flag_rows;
+        e.rowpts = dX + sh.begin * d;
+        e.row0 = sh.begin;
+        e.center_rows = 0;
+        e.cols = dX;
+        e.n = n;
+        e.d = d;
+        e.sc = sc;
+        e.h = J.h_score;
+        e.shift = f.shift;
+        e.score = f.score;
+        e.xsd_c = f.xsd_c;
+        e.phi_sum = f.phi_sum;
+        e.weighted = f.weighted;
+        STATUS_TRY(launch_exact(D, e));
+    }
+    record(D, o, FKDE_T_GATHER);
+    if (J.kind == Job::kScore) STATUS_TRY(allgather(D, D.aux0.p, sh.chunk * d, ncclFloat64));
+    if (J.kind == Job::kScoreAcc) {
+        STATUS_TRY(allgather(D, D.aux0.p, sh.chunk, ncclFloat64));
+        STATUS_TRY(allgather(D, D.aux1.p, sh.chunk * d, ncclFloat64));
+    }
+    if (want_xsd) STATUS_TRY(allgather(D, D.xsd.p, sh.chunk * d, ncclFloat64));
+    return {};
+}
+
+// Density of the rank's query shard against `dCols` (n x d; centred iff
+// !center_cols), gathered into D.out (m doubles, gather layout).
+Status query_program(Device& D, const Options& o, const Job& J, const double* dCols,
+                     bool cols_centred, const double* dQ, PassScalars* sc_q, int kernel,
+                     int fused) {
+    const int d = J.d;
+    const size_t n = J.n, m = J.m;
+    const double kh = std::sqrt(kLog2e) / J.h;
+    // scale exponent over both point sets (identical on every rank)
+    max_half_norm<<<grid1(n, 256), 256, 0, D.stream>>>(dCols, n, d, kh,
+                                                       cols_centred ? nullptr : sc_q, sc_q);
+    max_half_norm<<<grid1(m, 256), 256, 0, D.stream>>>(dQ, m, d, kh, sc_q, sc_q);
+    set_scale_exponent<<<1, 1, 0, D.stream>>>(sc_q);
+    D.launches += 3;
+    const Shard sh = shard_of(m, D.world, D.rank);
+    size_t rows_pad = 0, cols_pad = 0;
+    STATUS_TRY(pack(D, dCols, n, d, 1, !cols_centred, kh, sc_q, D.opB, &cols_pad));
+    STATUS_TRY(pack(D, dQ + sh.begin * d, sh.rows, d, 0, true, kh, sc_q, D.opA, &rows_pad));
+    record(D, o, FKDE_T_QUERY);
+
+    const double norm = std::pow(2.0 * M_PI, -0.5 * d) * std::pow(J.h, -static_cast<double>(d)) /
+                        static_cast<double>(n);  // gaussian_norm_const(h,d)/n, kernels.cpp:26-29
+    STATUS_TRY(ensure(D.out, sh.chunk * D.world * sizeof(double)));
+    double* outp = D.out.as<double>() + sh.begin;
+    ReduceArgs r{};
+    r.rows_pad = rows_pad;
+    r.rows = sh.rows;
+    r.scale = norm;
+    r.out = outp;
+    STATUS_TRY(prepare_flags(D, sh.rows));
+    unsigned int* flag_count = D.flags.as<unsigned int>();
+    int nparts = 0;
+    if (kernel == FKDE_KERNEL_GAUSSIAN) {
+        STATUS_TRY(density_pass(D, o, kModeGauss, rows_pad, n, sc_q, &nparts));
+        record(D, o, FKDE_T_REDUCE);
+        r.part0 = D.part0.as<float>();
+        r.nparts = nparts;
+        r.ca = 1.0;
+        r.cb = 0.0;
+        r.accumulate = 0;
+        r.flag_count = flag_count;
+        r.flag_rows = flag_count + 1;
+        if (sh.rows) reduce_density<<<grid1(sh.rows, 256), 256, 0, D.stream>>>(r);
+        ++D.launches;
+    } else if (fused) {
+        // LaplaceFused: phi (1 + d/2 - u) = (1 + d/2) phi + ln2 * phi * log2(phi)
+        STATUS_TRY(density_pass(D, o, kModeLaplace, rows_pad, n, sc_q, &nparts));
+        record(D, o, FKDE_T_REDUCE);
+        r.part0 = D.part0.as<float>();
+        r.part1 = D.part1.as<float>();
+        r.nparts = nparts;
+        r.ca = 1.0 + 0.5 * d;
+        r.cb = kLn2;
+        r.accumulate = 0;
+        r.flag_count = flag_count;
+        r.flag_rows = flag_count + 1;
+        if (sh.rows) reduce_density<<<grid1(sh.rows, 256), 256, 0, D.stream>>>(r);
+        ++D.launches;
+    } else {
+        // engine.cpp:372-379: Gaussian pass, then the correction pass
+        // phi (d/2 - u), accumulated into the same values.
+        STATUS_TRY(density_pass(D, o, kModeGauss, rows_pad, n, sc_q, &nparts));
+        r.part0 = D.part0.as<float>();
+        r.nparts = nparts;
+        r.ca = 1.0;
+        r.cb = 0.0;
+        r.accumulate = 0;
+        if (sh.rows) reduce_density<<<grid1(sh.rows, 256), 256, 0, D.stream>>>(r);
+        ++D.launches;
+        STATUS_TRY(density_pass(D, o, kModeLaplace, rows_pad, n, sc_q, &nparts));
+        record(D, o, FKDE_T_REDUCE);
+        r.part0 = D.part0.as<float>();
+        r.part1 = D.part1.as<float>();
+        r.nparts = nparts;
+        r.ca = 0.5 * d;
+        r.cb = kLn2;
+        r.accumulate = 1;
+        r.flag_count = flag_count;
+        r.flag_rows = flag_count + 1;
+        if (sh.rows) reduce_density<<<grid1(sh.rows, 256), 256, 0, D.stream>>>(r);
+        ++D.launches;
+    }
+    CUDA_TRY(cudaGetLastError());
+    {
+        ExactArgs e{};
+        e.mode = kernel == FKDE_KERNEL_GAUSSIAN ? kExactGauss : kExactLaplace;
+        e.count = flag_count;
+        e.rows = flag_count + 1;
+        e.rowpts = dQ + sh.begin * d;
+        e.row0 = sh.begin;
+        e.center_rows = cols_centred ? 1 : 0;
+        e.cols = dCols;
+        e.n = n;
+        e.d = d;
+        e.sc = sc_q;
+        e.h = J.h;
+        e.norm = norm;
+        e.out = outp;
+        STATUS_TRY(launch_exact(D, e));
+    }
+    STATUS_TRY(allgather(D, D.out.p, sh.chunk, ncclFloat64));
+    return {};
+}
+
+Status run_job(Device& D, const Options& o, const Job& J) {
+    CUDA_TRY(cudaSetDevice(D.dev));
+    D.launches = 0;
+    if (o.timing && !D.ev[0])
+        for (auto& e : D.ev) CUDA_TRY(cudaEventCreate(&e));
+    record(D, o, FKDE_T_PREP);
+    const int d = J.d;
+    const double* dX = J.dX;
+    const double* dY = J.dY;
+    if (J.kind == Job::kDist) {
+        STATUS_TRY(ensure(D.X, J.n * d * sizeof(double)));
+        STATUS_TRY(ensure(D.Y, J.m * d * sizeof(double)));
+        STATUS_TRY(ensure(D.aux0, (J.n + J.m) * sizeof(double)));
+        STATUS_TRY(ensure(D.out, J.n * J.m * sizeof(double)));
+        CUDA_TRY(cudaMemcpyAsync(D.X.p, J.hX, J.n * d * 8, cudaMemcpyHostToDevice, D.stream));
+        CUDA_TRY(cudaMemcpyAsync(D.Y.p, J.hY, J.m * d * 8, cudaMemcpyHostToDevice, D.stream));
+        double* an = D.aux0.as<double>();
+        sq_norms_fp64<<<grid1(J.n, 256), 256, 0, D.stream>>>(D.X.as<double>(), J.n, d, an);
+        sq_norms_fp64<<<grid1(J.m, 256), 256, 0, D.stream>>>(D.Y.as<double>(), J.m, d, an + J.n);
+        dim3 g(grid1(J.m, 128), static_cast<unsigned>(std::min<size_t>(J.n, 65535)));
+        block_sq_dists_fp64<<<g, 128, 0, D.stream>>>(D.X.as<double>(), an, J.n, D.Y.as<double>(),
+                                                     an + J.n, J.m, d, D.out.as<double>());
+        D.launches += 3;
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaMemcpyAsync(J.out, D.out.p, J.n * J.m * 8, cudaMemcpyDeviceToHost, D.stream));
+        CUDA_TRY(cudaStreamSynchronize(D.stream));
+        return {};
+    }
+    if (!dX) {
+        STATUS_TRY(ensure(D.X, J.n * d * sizeof(double)));
+        CUDA_TRY(cudaMemcpyAsync(D.X.p, J.hX, J.n * d * sizeof(double), cudaMemcpyHostToDevice,
+                                 D.stream));
+        dX = D.X.as<double>();
+    }
+    if (J.m && !dY) {
+        STATUS_TRY(ensure(D.Y, J.m * d * sizeof(double)));
+        CUDA_TRY(cudaMemcpyAsync(D.Y.p, J.hY, J.m * d * sizeof(double), cudaMemcpyHostToDevice,
+                                 D.stream));
+        dY = D.Y.as<double>();
+    }
+    STATUS_TRY(ensure(D.scal, 2 * sizeof(PassScalars)));
+    PassScalars* sc_s = D.scal.as<PassScalars>();
+    PassScalars* sc_q = sc_s + 1;
+
+    switch (J.kind) {
+        case Job::kScore:
+        case Job::kScoreAcc:
+            STATUS_TRY(score_program(D, o, J, dX, sc_s, false));
+            record(D, o, FKDE_T_QUERY);
+            record(D, o, FKDE_T_REDUCE);
+            break;
+        case Job::kSdkde: {
+            STATUS_TRY(score_program(D, o, J, dX, sc_s, true));
+            // sc_q: same centring mean, fresh scale (x_sd is already centred)
+            CUDA_TRY(cudaMemcpyAsync(sc_q, sc_s, sizeof(PassScalars), cudaMemcpyDeviceToDevice,
+                                     D.stream));
+            CUDA_TRY(cudaMemsetAsync(&sc_q->max_half_norm_bits, 0, sizeof(unsigned int), D.stream));
+            STATUS_TRY(query_program(D, o, J, D.xsd.as<double>(), true, dY, sc_q,
+                                     FKDE_KERNEL_GAUSSIAN, 1));
+            break;
+        }
+        case Job::kKde: {
+            STATUS_TRY(compute_mean(D, dX, J.n, d, sc_q));
+            record(D, o, FKDE_T_SCORE);
+            record(D, o, FKDE_T_FINALIZE);
+            record(D, o, FKDE_T_GATHER);
+            STATUS_TRY(query_program(D, o, J, dX, false, dY, sc_q, J.kernel, J.fused));
+            break;
+        }
+        default:
+            break;
+    }
+
+    // outputs
+    const size_t nd = J.n * d;
+    if (J.kind == Job::kSdkde || J.kind == Job::kKde) {
+        if (J.d_out) {
+            CUDA_TRY(cudaMemcpyAsync(J.d_out, D.out.p, J.m * sizeof(double),
+                                     cudaMemcpyDeviceToDevice, D.stream));
+        }
+        if (J.out) {
+            CUDA_TRY(cudaMemcpyAsync(J.out, D.out.p, J.m * sizeof(double), cudaMemcpyDeviceToHost,
+                                     D.stream));
+        }
+        if (J.kind == Job::kSdkde && J.out2) {
+            STATUS_TRY(ensure(D.aux1, nd * sizeof(double)));
+            add_mean<<<grid1(nd, 256), 256, 0, D.stream>>>(D.xsd.as<double>(), J.n, d, sc_s,
+                                                          D.aux1.as<double>());
+            ++D.launches;
+            CUDA_TRY(cudaMemcpyAsync(J.out2, D.aux1.p, nd * sizeof(double),
+                                     cudaMemcpyDeviceToHost, D.stream));
+        }
+    } else if (J.kind == Job::kScore) {
+        CUDA_TRY(cudaMemcpyAsync(J.out, D.aux0.p, nd * sizeof(double), cudaMemcpyDeviceToHost,
+                                 D.stream));
+    } else if (J.kind == Job::kScoreAcc) {
+        CUDA_TRY(cudaMemcpyAsync(J.out, D.aux0.p, J.n * sizeof(double), cudaMemcpyDeviceToHost,
+                                 D.stream));
+        CUDA_TRY(cudaMemcpyAsync(J.out2, D.aux1.p, nd * sizeof(double), cudaMemcpyDeviceToHost,
+                                 D.stream));
+    }
+    record(D, o, FKDE_T_TOTAL);
+    if (!J.sync) return {};
+
+    CUDA_TRY(cudaStreamSynchronize(D.stream));
+    // input validity (SampleSet::validate) and score underflow (engine.cpp:326-330)
+    PassScalars hs[2];
+    CUDA_TRY(cudaMemcpy(hs, D.scal.p, sizeof(hs), cudaMemcpyDeviceToHost));
+    if (hs[0].nonfinite || hs[1].nonfinite)
+        return make_status(FKDE_NON_FINITE, "SampleSet: non-finite entry");
+    if (J.kind == Job::kScore || J.kind == Job::kScoreAcc || J.kind == Job::kSdkde) {
+        unsigned long long row = ~0ull;
+        CUDA_TRY(cudaMemcpy(&row, D.err.p, sizeof(row), cudaMemcpyDeviceToHost));
+        if (row != ~0ull && J.kind != Job::kScoreAcc) {
+            Status s = make_status(FKDE_SCORE_UNDERFLOW,
+                                   "score denominator underflowed to zero at train point %llu",
+                                   row);
+            s.index = static_cast<size_t>(row);
+            return s;
+        }
+    }
+    return {};
+}
+
+// Runs the job on every device of the context (one host thread per device in
+// the single-process multi-device case).  Host outputs are written by device 0.
+Status run_all(fkde_gpu_ctx* ctx, const Job& J) {
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    if (ctx->devs.size() == 1) return set_error(ctx, run_job(ctx->devs[0], ctx->opt, J));
+    std::vector<Status> st(ctx->devs.size());
+    std::vector<std::thread> th;
+    for (size_t i = 0; i < ctx->devs.size(); ++i) {
+        Job Ji = J;
+        if (i > 0) {
+            Ji.out = nullptr;
+            Ji.out2 = nullptr;
+        }
+        th.emplace_back([&, i, Ji] { st[i] = run_job(ctx->devs[i], ctx->opt, Ji); });
+    }
+    for (auto& t : th) t.join();
+    for (auto& s : st)
+        if (!s.ok()) return set_error(ctx, s);
+    return set_error(ctx, {});
+}
+
+bool finite_h(double h) { return h > 0.0 && std::isfinite(h); }
+
+Status validate_set(const void* p, size_t n, size_t d, const char* what) {
+    if (!p) return make_status(FKDE_INVALID_ARGUMENT, "%s: null pointer", what);
+    if (n == 0 || d == 0) return make_status(FKDE_INVALID_ARGUMENT, "SampleSet: n and d must be >= 1");
+    if (d > static_cast<size_t>(kMaxDim))
+        return make_status(FKDE_UNSUPPORTED_D, "d=%zu exceeds the tensor-core path's limit of %d",
+                           d, kMaxDim);
+    return {};
+}
+
+int finish(fkde_gpu_ctx* ctx, const Status& s, size_t* err_index = nullptr) {
+    if (ctx) ctx->err = s.msg;
+    if (err_index && s.code == FKDE_SCORE_UNDERFLOW) *err_index = s.index;
+    return s.code;
+}
+
+Status init_device(Device& D, int dev, int rank, int world) {
+    D.dev = dev;
+    D.rank = rank;
+    D.world = world;
+    CUDA_TRY(cudaSetDevice(dev));
+    cudaDeviceProp prop;
+    CUDA_TRY(cudaGetDeviceProperties(&prop, dev));
+    if (prop.major != 10)
+        return make_status(FKDE_NO_DEVICE, "device %d is sm_%d%d; this build targets sm_100a", dev,
+                           prop.major, prop.minor);
+    D.num_sms = prop.multiProcessorCount;
+    CUDA_TRY(cudaStreamCreateWithFlags(&D.stream, cudaStreamNonBlocking));
+    return {};
+}
+
+}  // namespace
+
+// =============================================================================
+// C ABI
+// =============================================================================
+extern "C" {
+
+int fkde_gpu_shard_range(size_t n, int world, int rank, size_t align, size_t* begin,
+                         size_t* rows, size_t* chunk) {
+    if (world < 1 || rank < 0 || rank >= world || align == 0) return FKDE_INVALID_ARGUMENT;
+    const Shard s = shard_of(n, world, rank, align);
+    if (begin) *begin = s.begin;
+    if (rows) *rows = s.rows;
+    if (chunk) *chunk = s.chunk;
+    return FKDE_OK;
+}
+
+int fkde_gpu_device_count(int* count) {
+    int c = 0;
+    cudaError_t e = cudaGetDeviceCount(&c);
+    if (count) *count = e == cudaSuccess ? c : 0;
+    return e == cudaSuccess ? FKDE_OK : FKDE_NO_DEVICE;
+}
+
+int fkde_gpu_create(const int* devices, int n_devices, fkde_gpu_ctx** out) {
+    if (!out || n_devices < 1) return FKDE_INVALID_ARGUMENT;
+    *out = nullptr;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) return FKDE_NO_DEVICE;
+    auto* ctx = new fkde_gpu_ctx();
+    ctx->devs.resize(n_devices);
+    ctx->world = n_devices;
+    std::vector<int> ids(n_devices);
+    for (int i = 0; i < n_devices; ++i) {
+        ids[i] = devices ? devices[i] : i;
+        Status s = init_device(ctx->devs[i], ids[i], i, n_devices);
+        if (!s.ok()) {
+            fkde_gpu_destroy(ctx);
+            return s.code;
+        }
+    }
+    if (n_devices > 1) {
+        if (!nccl().loaded) {
+            fkde_gpu_destroy(ctx);
+            return FKDE_NCCL_ERROR;
+        }
+        std::vector<ncclComm_t> comms(n_devices);
+        if (nccl().CommInitAll(comms.data(), n_devices, ids.data()) != ncclSuccess) {
+            fkde_gpu_destroy(ctx);
+            return FKDE_NCCL_ERROR;
+        }
+        for (int i = 0; i < n_devices; ++i) ctx->devs[i].comm = comms[i];
+    }
+    *out = ctx;
+    return FKDE_OK;
+}
+
+int fkde_gpu_nccl_unique_id(unsigned char id[128]) {
+    if (!nccl().loaded) return FKDE_NCCL_ERROR;
+    ncclUniqueId uid;
+    if (nccl().GetUniqueId(&uid) != ncclSuccess) return FKDE_NCCL_ERROR;
+    std::memcpy(id, uid.internal, sizeof(uid.internal));
+    return FKDE_OK;
+}
+
+int fkde_gpu_create_rank(int device, int rank, int world, const unsigned char id[128],
+                         fkde_gpu_ctx** out) {
+    if (!out || world < 1 || rank < 0 || rank >= world) return FKDE_INVALID_ARGUMENT;
+    *out = nullptr;
+    auto* ctx = new fkde_gpu_ctx();
+    ctx->devs.resize(1);
+    ctx->world = world;
+    ctx->per_rank = true;
+    Status s = init_device(ctx->devs[0], device, rank, world);
+    if (!s.ok()) {
+        fkde_gpu_destroy(ctx);
+        return s.code;
+    }
+    if (world > 1) {
+        if (!nccl().loaded || !id) {
+            fkde_gpu_destroy(ctx);
+            return FKDE_NCCL_ERROR;
+        }
+        ncclUniqueId uid;
+        std::memcpy(uid.internal, id, sizeof(uid.internal));
+        if (nccl().CommInitRank(&ctx->devs[0].comm, world, uid, rank) != ncclSuccess) {
+            fkde_gpu_destroy(ctx);
+            return FKDE_NCCL_ERROR;
+        }
+    }
+    *out = ctx;
+    return FKDE_OK;
+}
+
+void fkde_gpu_destroy(fkde_gpu_ctx* ctx) {
+    if (!ctx) return;
+    for (auto& D : ctx->devs) {
+        cudaSetDevice(D.dev);
+        if (D.stream) cudaStreamSynchronize(D.stream);
+        if (D.comm && nccl().loaded) nccl().CommDestroy(D.comm);
+        DevBuf* bufs[] = {&D.X, &D.Y, &D.opA, &D.opB, &D.part0, &D.part1, &D.xsd,
+                          &D.out, &D.aux0, &D.aux1, &D.colpart, &D.scal, &D.err, &D.flags};
+        for (DevBuf* b : bufs)
+            if (b->p) cudaFree(b->p);
+        for (auto& e : D.ev)
+            if (e) cudaEventDestroy(e);
+        if (D.stream) cudaStreamDestroy(D.stream);
+    }
+    delete ctx;
+}
+
+const char* fkde_gpu_last_error(const fkde_gpu_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
+
+int fkde_gpu_set_option(fkde_gpu_ctx* ctx, int key, int64_t value) {
+    if (!ctx) return FKDE_INVALID_ARGUMENT;
+    switch (key) {
+        case FKDE_OPT_ENGINE:
+            if (value != FKDE_ENGINE_TC && value != FKDE_ENGINE_SIMT) return FKDE_INVALID_ARGUMENT;
+            ctx->opt.engine = static_cast<int>(value);
+            return FKDE_OK;
+        case FKDE_OPT_SPLITS:
+            if (value < 0) return FKDE_INVALID_ARGUMENT;
+            ctx->opt.splits = static_cast<int>(value);
+            return FKDE_OK;
+        case FKDE_OPT_TIMING:
+            ctx->opt.timing = value ? 1 : 0;
+            return FKDE_OK;
+        case FKDE_OPT_MAX_CTAS:
+            if (value < 0) return FKDE_INVALID_ARGUMENT;
+            ctx->opt.max_ctas = static_cast<int>(value);
+            return FKDE_OK;
+        default:
+            return FKDE_INVALID_ARGUMENT;
+    }
+}
+
+int fkde_gpu_world(const fkde_gpu_ctx* ctx, int* rank, int* world) {
+    if (!ctx) return FKDE_INVALID_ARGUMENT;
+    if (rank) *rank = ctx->devs[0].rank;
+    if (world) *world = ctx->world;
+    return FKDE_OK;
+}
+
+void* fkde_gpu_stream(fkde_gpu_ctx* ctx) {
+    return ctx ? static_cast<void*>(ctx->devs[0].stream) : nullptr;
+}
+
+int fkde_gpu_last_timing(const fkde_gpu_ctx* ctx, float* ms, int n) {
+    if (!ctx || !ms) return FKDE_INVALID_ARGUMENT;
+    const Device& D = ctx->devs[0];
+    if (!ctx->opt.timing || !D.ev[0]) {
+        for (int i = 0; i < n && i < FKDE_T_COUNT; ++i) ms[i] = 0.f;
+        return FKDE_OK;
+    }
+    cudaSetDevice(D.dev);
+    if (cudaEventSynchronize(D.ev[FKDE_T_TOTAL]) != cudaSuccess) return FKDE_CUDA_ERROR;
+    for (int i = 0; i < n && i < FKDE_T_COUNT; ++i) {
+        float v = 0.f;
+        if (i < FKDE_T_TOTAL)
+            cudaEventElapsedTime(&v, D.ev[i], D.ev[i + 1]);
+        else
+            cudaEventElapsedTime(&v, D.ev[FKDE_T_PREP], D.ev[FKDE_T_TOTAL]);
+        ms[i] = v;
+    }
+    return FKDE_OK;
+}
+
+int64_t fkde_gpu_last_launch_count(const fkde_gpu_ctx* ctx) {
+    return ctx ? ctx->devs[0].launches : 0;
+}
+
+int fkde_gpu_score(fkde_gpu_ctx* ctx, const double* X, size_t n, size_t d, double h_score,
+                   double* scores, size_t* err_index) {
+    if (!ctx) return FKDE_INVALID_ARGUMENT;
+    Status s = validate_set(X, n, d, "train");
+    if (s.ok() && !finite_h(h_score))
+        s = make_status(FKDE_INVALID_ARGUMENT, "Bandwidth: h_score must be positive and finite");
+    if (s.ok() && !scores) s = make_status(FKDE_INVALID_ARGUMENT, "scores: null pointer");
+    if (!s.ok()) return finish(ctx, s);
+    Job J;
+    J.kind = Job::kScore;
+    J.hX = X;
+    J.n = n;
+    J.d = static_cast<int>(d);
+    J.h = h_score;
+    J.h_score = h_score;
+    J.out = scores;
+    return finish(ctx, run_all(ctx, J), err_index);
+}
+
+int fkde_gpu_score_accumulate(fkde_gpu_ctx* ctx, const double* X, size_t n, size_t d,
+                              double h_score, double* phi_sum, double* weighted) {
+    if (!ctx) return FKDE_INVALID_ARGUMENT;
+    Status s = validate_set(X, n, d, "train");
+    if (s.ok() && !finite_h(h_score))
+        s = make_status(FKDE_INVALID_ARGUMENT, "Bandwidth: h_score must be positive and finite");
+    if (s.ok() && (!phi_sum || !weighted))
+        s = make_status(FKDE_INVALID_ARGUMENT, "outputs: null pointer");
+    if (!s.ok()) return finish(ctx, s);
+    Job J;
+    J.kind = Job::kScoreAcc;
+    J.hX = X;
+    J.n = n;
+    J.d = static_cast<int>(d);
+    J.h = h_score;
+    J.h_score = h_score;
+    J.out = phi_sum;
+    J.out2 = weighted;
+    return finish(ctx, run_all(ctx, J));
+}
+
+static Status validate_pair(const void* X, size_t n, const void* Y, size_t m, size_t d, double h) {
+    Status s = validate_set(X, n, d, "train");
+    if (s.ok()) s = validate_set(Y, m, d, "queries");
+    if (s.ok() && !finite_h(h))
+        s = make_status(FKDE_INVALID_ARGUMENT, "Bandwidth: h must be positive and finite");
+    return s;
+}
+
+int fkde_gpu_kde(fkde_gpu_ctx* ctx, const double* X, size_t n, const double* Y, size_t m,
+                 size_t d, double h, int kernel, int fused, double* out) {
+    if (!ctx) return FKDE_INVALID_ARGUMENT;
+    Status s = validate_pair(X, n, Y, m, d, h);
+    if (s.ok() && kernel != FKDE_KERNEL_GAUSSIAN && kernel != FKDE_KERNEL_LAPLACE_CORRECTED)
+        s = make_status(FKDE_INVALID_ARGUMENT, "unknown kernel kind %d", kernel);
+    if (s.ok() && !out) s = make_status(FKDE_INVALID_ARGUMENT, "out: null pointer");
+    if (!s.ok()) return finish(ctx, s);
+    Job J;
+    J.kind = Job::kKde;
+    J.hX = X;
+    J.hY = Y;
+    J.n = n;
+    J.m = m;
+    J.d = static_cast<int>(d);
+    J.h = h;
+    J.kernel = kernel;
+    J.fused = fused;
+    J.out = out;
+    return finish(ctx, run_all(ctx, J));
+}
+
+int fkde_gpu_sdkde(fkde_gpu_ctx* ctx, const double* X, size_t n, const double* Y, size_t m,
+                   size_t d, double h, double h_score, double* out, double* debiased,
+                   size_t* err_index) {
+    if (!ctx) return FKDE_INVALID_ARGUMENT;
+    Status s = validate_pair(X, n, Y, m, d, h);
+    if (s.ok() && !finite_h(h_score))
+        s = make_status(FKDE_INVALID_ARGUMENT, "Bandwidth: h_score must be positive and finite");
+    if (s.ok() && !out) s = make_status(FKDE_INVALID_ARGUMENT, "out: null pointer");
+    if (!s.ok()) return finish(ctx, s);
+    Job J;
+    J.kind = Job::kSdkde;
+    J.hX = X;
+    J.hY = Y;
+    J.n = n;
+    J.m = m;
+    J.d = static_cast<int>(d);
+    J.h = h;
+    J.h_score = h_score;
+    J.out = out;
+    J.out2 = debiased;
+    return finish(ctx, run_all(ctx, J), err_index);
+}
+
+int fkde_gpu_estimate(fkde_gpu_ctx* ctx, const double* X, size_t n, const double* Y, size_t m,
+                      size_t d, int method, double h, double h_score, size_t tile_m,
+                      size_t tile_n, int fused, double* out, double* debiased,
+                      double* negative_mass, size_t* err_index) {
+    if (!ctx) return FKDE_INVALID_ARGUMENT;
+    // EstimatorConfig::validate (types.cpp:74-79)
+    if (!finite_h(h))
+        return finish(ctx, make_status(FKDE_INVALID_ARGUMENT, "Bandwidth: h must be positive and finite"));
+    if (!finite_h(h_score))
+        return finish(ctx, make_status(FKDE_INVALID_ARGUMENT,
+                                       "Bandwidth: h_score must be positive and finite"));
+    if (tile_m == 0 || tile_n == 0)
+        return finish(ctx, make_status(FKDE_INVALID_ARGUMENT,
+                                       "EstimatorConfig: tile_m and tile_n must be >= 1"));
+    int rc;
+    switch (method) {
+        case FKDE_METHOD_KDE:
+            rc = fkde_gpu_kde(ctx, X, n, Y, m, d, h, FKDE_KERNEL_GAUSSIAN, 1, out);
+            break;
+        case FKDE_METHOD_SDKDE:
+            rc = fkde_gpu_sdkde(ctx, X, n, Y, m, d, h, h_score, out, debiased, err_index);
+            break;
+        case FKDE_METHOD_LAPLACE:
+            rc = fkde_gpu_kde(ctx, X, n, Y, m, d, h, FKDE_KERNEL_LAPLACE_CORRECTED, fused, out);
+            if (rc == FKDE_OK && negative_mass) {  // estimator.cpp:14-20
+                double acc = 0.0;
+                for (size_t j = 0; j < m; ++j) acc += std::max(0.0, -out[j]);
+                *negative_mass = acc / static_cast<double>(m);
+            }
+            break;
+        default:
+            return finish(ctx, make_status(FKDE_INVALID_ARGUMENT, "estimate: unknown method"));
+    }
+    return rc;
+}
+
+int fkde_gpu_pairwise_sq_dists(fkde_gpu_ctx* ctx, const double* A, size_t na, const double* B,
+                               size_t nb, size_t d, double* out) {
+    if (!ctx) return FKDE_INVALID_ARGUMENT;
+    Status s = validate_set(A, na, std::min<size_t>(d, 1), "a");
+    if (s.ok()) s = validate_set(B, nb, std::min<size_t>(d, 1), "b");
+    if (s.ok() && d == 0) s = make_status(FKDE_INVALID_ARGUMENT, "SampleSet: n and d must be >= 1");
+    if (s.ok() && !out) s = make_status(FKDE_INVALID_ARGUMENT, "out: null pointer");
+    if (!s.ok()) return finish(ctx, s);
+    for (size_t i = 0; i < na * d; ++i)
+        if (!std::isfinite(A[i])) return finish(ctx, make_status(FKDE_NON_FINITE, "SampleSet: non-finite entry"));
+    for (size_t i = 0; i < nb * d; ++i)
+        if (!std::isfinite(B[i])) return finish(ctx, make_status(FKDE_NON_FINITE, "SampleSet: non-finite entry"));
+    Job J;
+    J.kind = Job::kDist;
+    J.hX = A;
+    J.hY = B;
+    J.n = na;
+    J.m = nb;
+    J.d = static_cast<int>(d);
+    J.out = out;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    return finish(ctx, run_job(ctx->devs[0], ctx->opt, J));
+}
+
+int fkde_gpu_sdkde_device(fkde_gpu_ctx* ctx, const double* dX, size_t n, const double* dY,
+                          size_t m, size_t d, double h, double h_score, double* d_out) {
+    if (!ctx) return FKDE_INVALID_ARGUMENT;
+    if (ctx->devs.size() != 1)
+        return finish(ctx, make_status(FKDE_INVALID_ARGUMENT, "device API needs a 1-device context"));
+    Status s = validate_pair(dX, n, dY, m, d, h);
+    if (s.ok() && !finite_h(h_score))
+        s = make_status(FKDE_INVALID_ARGUMENT, "Bandwidth: h_score must be positive and finite");
+    if (!s.ok()) return finish(ctx, s);
+    Job J;
+    J.kind = Job::kSdkde;
+    J.dX = dX;
+    J.dY = dY;
+    J.n = n;
+    J.m = m;
+    J.d = static_cast<int>(d);
+    J.h = h;
+    J.h_score = h_score;
+    J.d_out = d_out;
+    J.sync = false;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    return finish(ctx, run_job(ctx->devs[0], ctx->opt, J));
+}
+
+int fkde_gpu_kde_device(fkde_gpu_ctx* ctx, const double* dX, size_t n, const double* dY,
+                        size_t m, size_t d, double h, int kernel, int fused, double* d_out) {
+    if (!ctx) return FKDE_INVALID_ARGUMENT;
+    if (ctx->devs.size() != 1)
+        return finish(ctx, make_status(FKDE_INVALID_ARGUMENT, "device API needs a 1-device context"));
+    Status s = validate_pair(dX, n, dY, m, d, h);
+    if (!s.ok()) return finish(ctx, s);
+    Job J;
+    J.kind = Job::kKde;
+    J.dX = dX;
+    J.dY = dY;
+    J.n = n;
+    J.m = m;
+    J.d = static_cast<int>(d);
+    J.h = h;
+    J.kernel = kernel;
+    J.fused = fused;
+    J.d_out = d_out;
+    J.sync = false;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    return finish(ctx, run_job(ctx->devs[0], ctx->opt, J));
+}
+
+}  // extern "C"

@@ -1,0 +1,64 @@
+// layout.cuh -- HBM/SMEM operand layout shared by the pack kernels and the
+// tcgen05 pairwise kernels.
+//
+// Every point becomes one 128-byte row of 64 fp16 values ("operand row").
+// Coordinates are centred on the training mean mu and scaled by
+//   k = sqrt(log2 e) / h * 2^-e
+// so that the single K=64 Gram product of a row-side ("A") and a column-side
+// ("B") operand row is directly log2 of the Gaussian kernel (times 2^-2e):
+//   A_i . B_j = y_i.y_j - |y_i|^2/2 - |y_j|^2/2 = -|y_i - y_j|^2 / 2
+//             = log2 exp(-r_ij^2 / (2 h^2)) * 2^-2e.
+// fp32-class accuracy from fp16 tensor-core operands comes from hi/lo splits
+// (y = y_hi + y_lo, both fp16, 22 significant bits) and a 3-term fp16 split of
+// the half-norms.  16-byte chunks (8 fp16):
+//
+//   chunk   A (row side)                 B (column side)
+//   0-1     y_hi[0:16]                   y_hi[0:16]
+//   2-3     y_hi[0:16]                   y_lo[0:16]
+//   4       a1 a2 a3 1 1 1 0 0           1 1 1 b1 b2 b3 0 0     (a,b = -|y|^2/2 split)
+//   5       0                            0
+//   6-7     y_lo[0:16]                   y_hi[0:16]
+//
+// The B rows double as the MN-major B operand of the score pass's second GEMM
+// (P . [y_hi | y_lo | 1]): its first 48 columns give sum_j phi_ij y_hi_j,
+// sum_j phi_ij y_lo_j and sum_j phi_ij (the ones column -- S comes off the
+// tensor core from the same rounded phi as T).
+//
+// Rows are grouped in tiles of 128 (16 KiB, contiguous) stored exactly as the
+// SWIZZLE_128B shared-memory image: 16-byte chunk c of row r lives at
+// r*128 + ((c ^ (r & 7)) * 16).  A tile is therefore one bulk async copy.
+// Padding rows: A -> all zero; B -> b1=b2=-30000 so that phi = 2^(-60000) = 0.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+namespace fkde_b200 {
+
+constexpr int kTileRows = 128;            // BM = BN = 128
+constexpr int kRowBytes = 128;            // 64 fp16
+constexpr int kTileBytes = kTileRows * kRowBytes;  // 16 KiB
+constexpr int kMaxDim = 16;               // tensor-core path: d <= 16 (zero padded)
+
+// Score pass: P' = phi * 2^15 (phi <= 1) so that phi down to 2^-29 stays a
+// normal fp16 number; finalize divides the sums by 2^15.  Rows whose
+// neighbour mass is still too small for fp16 (S' < 2^-16), and query rows
+// whose Gaussian mass is below 2^-90 (fp32 ex2 flushes below 2^-126), are
+// recomputed exactly in fp64 with a per-row max shift (exact_rows_fp64).
+constexpr int kPScaleExp = 15;
+constexpr float kPScaleF = 15.0f;
+constexpr double kScoreFlagMass = 1.52587890625e-05;   // 2^-16
+constexpr double kDensityFlagMass = 8.077935669463161e-28;  // 2^-90
+
+// Device-side per-pass scalars (written by the prep kernels, read by the
+// pack / pairwise / finalize kernels; no host round trip).
+struct PassScalars {
+    double mu[kMaxDim];      // training mean (centring)
+    unsigned int max_half_norm_bits;  // max_i |y_i|^2/2 before 2^-e scaling (float bits)
+    int e;                   // operand scale exponent (y' = y * 2^-e)
+    float dscale;            // 2^(2e): D = D' * dscale
+    unsigned int nonfinite;  // set when an input entry is NaN/Inf
+};
+
+__host__ __device__ inline size_t round_up(size_t x, size_t m) { return (x + m - 1) / m * m; }
+
+}  // namespace fkde_b200

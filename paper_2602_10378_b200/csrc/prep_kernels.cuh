@@ -1,0 +1,405 @@
+// prep_kernels.cuh -- O(n*d) kernels around the two O(n^2) passes:
+//   column mean (centring), operand scale exponent, operand packing into the
+//   swizzled tile image, score finalize (+ SD shift), density reduction, plus
+//   the fp64 block-distance kernel behind pairwise_sq_dists_block.
+#pragma once
+#include <cuda_fp16.h>
+#include <cstdint>
+
+#include "layout.cuh"
+
+namespace fkde_b200 {
+
+constexpr double kLog2e = 1.4426950408889634073599246810019;
+constexpr double kLn2 = 0.69314718055994530941723212145818;
+
+// ---- deterministic column sums: stage 1 (per-block partials) -----------------
+// Thread t sums column (t % 16) over rows start + (t/16), +16, ...; the 16
+// row-phases are then added in a fixed order.  Same inputs -> same bits on
+// every rank and every run.
+// Also flags non-finite entries (SampleSet::validate, types.cpp:21-33).
+__global__ void colsum_stage1(const double* __restrict__ x, size_t n, int d,
+                              double* __restrict__ part /* [gridDim.x][16] */,
+                              PassScalars* flag) {
+    __shared__ double sm[16][17];
+    const int c = threadIdx.x & 15, g = threadIdx.x >> 4;
+    const size_t b0 = n * blockIdx.x / gridDim.x, b1 = n * (blockIdx.x + 1) / gridDim.x;
+    double acc = 0.0;
+    bool bad = false;
+    if (c < d)
+        for (size_t r = b0 + g; r < b1; r += 16) {
+            const double v = x[r * d + c];
+            bad |= !isfinite(v);
+            acc += v;
+        }
+    if (bad) flag->nonfinite = 1u;
+    sm[g][c] = acc;
+    __syncthreads();
+    if (threadIdx.x < 16) {
+        double s = 0.0;
+        for (int k = 0; k < 16; ++k) s += sm[k][threadIdx.x];
+        part[blockIdx.x * 16 + threadIdx.x] = s;
+    }
+}
+
+// stage 2: one block of 16 threads -> mean into PassScalars.mu
+__global__ void colsum_stage2(const double* __restrict__ part, int nparts, size_t n, int d,
+                              PassScalars* sc) {
+    const int c = threadIdx.x;
+    if (c >= kMaxDim) return;
+    double s = 0.0;
+    for (int b = 0; b < nparts; ++b) s += part[b * 16 + c];
+    sc->mu[c] = (c < d) ? s / static_cast<double>(n) : 0.0;
+}
+
+// ---- operand scale: max_i |(x_i - mu) k|^2 / 2 ------------------------------------
+// center: subtract sc_mu->mu (nullptr -> points already centred)
+__global__ void max_half_norm(const double* __restrict__ x, size_t rows, int d, double k,
+                              const PassScalars* __restrict__ sc_mu, PassScalars* sc_out) {
+    const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    float hn = 0.f;
+    if (i < rows) {
+        double s = 0.0;
+        for (int c = 0; c < d; ++c) {
+            const double raw = x[i * d + c];
+            if (!isfinite(raw)) sc_out->nonfinite = 1u;
+            const double v = (raw - (sc_mu ? sc_mu->mu[c] : 0.0)) * k;
+            s += v * v;
+        }
+        hn = static_cast<float>(0.5 * s);
+        if (!(hn == hn) || hn > 3.0e38f) hn = 3.0e38f;  // NaN/overflow -> saturate
+    }
+    for (int o = 16; o > 0; o >>= 1) hn = fmaxf(hn, __shfl_xor_sync(0xffffffffu, hn, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(&sc_out->max_half_norm_bits, __float_as_uint(hn));
+}
+
+// e = smallest exponent with max|y|^2/2 * 2^-2e <= 2^13 (fp16-safe operands)
+__global__ void set_scale_exponent(PassScalars* sc) {
+    const float hn = __uint_as_float(sc->max_half_norm_bits);
+    int e = 0;
+    while (e < 60 && ldexpf(hn, -2 * e) > 8192.0f) ++e;
+    sc->e = e;
+    sc->dscale = ldexpf(1.0f, 2 * e);
+}
+
+// ---- operand packing ------------------------------------------------------------
+// One thread per operand row (rows_padded threads).  Writes row `out_row0+i`
+// of the tile image.  format 0 = A (row side), 1 = B (column side).
+struct PackArgs {
+    const double* x;         // source points, row-major, d doubles per row
+    size_t rows;             // valid rows
+    size_t rows_padded;      // multiple of kTileRows
+    int d;
+    int format;
+    int center;              // subtract sc->mu
+    double k;                // sqrt(log2 e) / h
+    const PassScalars* sc;   // mu (if center) and e
+    uint4* out;              // rows_padded * 8 uint4
+};
+
+__device__ __forceinline__ uint32_t pack_h2(__half a, __half b) {
+    return static_cast<uint32_t>(__half_as_ushort(a)) |
+           (static_cast<uint32_t>(__half_as_ushort(b)) << 16);
+}
+
+__global__ void pack_operands(PackArgs a) {
+    const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (i >= a.rows_padded) return;
+    __half yh[kMaxDim], yl[kMaxDim];
+    __half n1 = __float2half(0.f), n2 = n1, n3 = n1;
+    const __half one = __float2half(1.f), zero = __float2half(0.f);
+    bool valid = i < a.rows;
+    if (valid) {
+        const double ys = ldexp(a.k, -a.sc->e);
+        double nrm = 0.0;
+#pragma unroll
+        for (int c = 0; c < kMaxDim; ++c) {
+            double y = 0.0;
+            if (c < a.d) y = (a.x[i * a.d + c] - (a.center ? a.sc->mu[c] : 0.0)) * ys;
+            yh[c] = __double2half(y);
+            const double h = static_cast<double>(__half2float(yh[c]));
+            yl[c] = __double2half(y - h);
+            const double l = static_cast<double>(__half2float(yl[c]));
+            nrm += h * h + 2.0 * h * l;  // exactly what the 3-term MMA forms on the diagonal
+        }
+        const double m = -0.5 * nrm;
+        n1 = __double2half(m);
+        const double r1 = m - static_cast<double>(__half2float(n1));
+        n2 = __double2half(r1);
+        n3 = __double2half(r1 - static_cast<double>(__half2float(n2)));
+    } else {
+#pragma unroll
+        for (int c = 0; c < kMaxDim; ++c) yh[c] = yl[c] = zero;
+    }
+    uint32_t ch[8][4];
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            const int k0 = c * 8 + 2 * w;
+            ch[c][w] = pack_h2(yh[k0], yh[k0 + 1]);                       // chunks 0-1: y_hi
+            ch[2 + c][w] = a.format == 0 ? pack_h2(yh[k0], yh[k0 + 1])    // A: y_hi
+                                         : pack_h2(yl[k0], yl[k0 + 1]);   // B: y_lo
+            ch[6 + c][w] = a.format == 0 ? pack_h2(yl[k0], yl[k0 + 1])    // A: y_lo
+                                         : pack_h2(yh[k0], yh[k0 + 1]);   // B: y_hi
+        }
+    if (valid) {
+        if (a.format == 0) {  // a1 a2 a3 1 1 1 0 0
+            ch[4][0] = pack_h2(n1, n2);
+            ch[4][1] = pack_h2(n3, one);
+            ch[4][2] = pack_h2(one, one);
+            ch[4][3] = 0u;
+        } else {              // 1 1 1 b1 b2 b3 0 0
+            ch[4][0] = pack_h2(one, one);
+            ch[4][1] = pack_h2(one, n1);
+            ch[4][2] = pack_h2(n2, n3);
+            ch[4][3] = 0u;
+        }
+    } else {
+        if (a.format == 0) {
+            ch[4][0] = ch[4][1] = ch[4][2] = ch[4][3] = 0u;
+        } else {  // far-away column: b1 + b2 = -60000 -> phi = 0 exactly
+            const __half big = __float2half(-30000.f);
+            ch[4][0] = 0u;
+            ch[4][1] = pack_h2(zero, big);
+            ch[4][2] = pack_h2(big, zero);
+            ch[4][3] = 0u;
+        }
+    }
+#pragma unroll
+    for (int w = 0; w < 4; ++w) ch[5][w] = 0u;
+    const size_t tile = i / kTileRows;
+    const int r = static_cast<int>(i % kTileRows);
+    uint4* base = a.out + tile * (kTileBytes / 16) + r * 8;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) base[c ^ (r & 7)] = make_uint4(ch[c][0], ch[c][1], ch[c][2], ch[c][3]);
+}
+
+// ---- score finalize ----------------------------------------------------------------
+// engine.cpp:322-337 (s = (T - x S) / (h^2 S), ScoreUnderflowError when S == 0)
+// and the SD shift engine.cpp:396-399 (x + h^2/2 s).  Local shard row i is
+// global row g = row0 + i; every output is indexed by g (in-place allgather
+// layout).  part_s: [splits][rows_pad]; part_t: [splits][rows_pad][16] with
+// T' = sum_j phi_ij y'_j in scaled, centred coordinates.
+struct FinalizeArgs {
+    const float* part_s;
+    const float* part_t;
+    int splits;
+    size_t rows_pad;
+    size_t rows;          // rows in this shard
+    size_t row0;          // global index of shard row 0
+    int d;
+    const double* x;      // full training set (fp64, original coordinates)
+    const PassScalars* sc;
+    double k;             // sqrt(log2 e)/h_score
+    double h_score;
+    double shift;         // h^2/2
+    double* score;        // [n][d] or nullptr
+    double* xsd_c;        // [n][d] centred debiased samples or nullptr
+    double* phi_sum;      // [n] raw S or nullptr
+    double* weighted;     // [n][d] raw sum_j phi_ij x_j or nullptr
+    unsigned long long* underflow_row;  // atomicMin of failing global row
+    unsigned int* flag_count;           // rows handed to exact_rows_fp64
+    unsigned int* flag_rows;            // (local indices)
+};
+
+__global__ void finalize_score(FinalizeArgs a) {
+    const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (i >= a.rows) return;
+    // S' and T' exclude the self pair (phi_ii = exp(0) = 1, engine.cpp:43-50
+    // snaps r_ii^2 to 0): S = 1 + S', and T - x_i S = T' - x_i S'.
+    double Sp = 0.0;
+    for (int s = 0; s < a.splits; ++s) Sp += static_cast<double>(a.part_s[s * a.rows_pad + i]);
+    Sp = ldexp(Sp, -kPScaleExp);  // the tc/simt score sums carry phi * 2^15
+    if (Sp < kScoreFlagMass && a.flag_rows) {  // too little neighbour mass for fp16 P
+        a.flag_rows[atomicAdd(a.flag_count, 1u)] = static_cast<unsigned int>(i);
+        return;
+    }
+    const double S = 1.0 + Sp;
+    const double ys = ldexp(a.k, -a.sc->e);
+    const size_t g = a.row0 + i;
+    if (a.phi_sum) a.phi_sum[g] = S;
+    if (!(S > 0.0) || !isfinite(S)) {
+        atomicMin(a.underflow_row, static_cast<unsigned long long>(g));
+        return;
+    }
+    const double inv = 1.0 / (a.h_score * a.h_score * S);
+    for (int c = 0; c < a.d; ++c) {
+        double Tp = 0.0;
+        for (int s = 0; s < a.splits; ++s)
+            Tp += static_cast<double>(a.part_t[(s * a.rows_pad + i) * kMaxDim + c]);
+        const double tc = ldexp(Tp, -kPScaleExp) / ys;  // sum_{j != i} phi_ij xc_j
+        const double x = a.x[g * a.d + c];
+        const double xc = x - a.sc->mu[c];
+        const double s = (tc - xc * Sp) * inv;         // (T - x S) / (h^2 S)
+        if (a.score) a.score[g * a.d + c] = s;
+        if (a.xsd_c) a.xsd_c[g * a.d + c] = xc + a.shift * s;
+        if (a.weighted) a.weighted[g * a.d + c] = (tc + xc) + S * a.sc->mu[c];
+    }
+}
+
+// debiased samples in original coordinates: x_sd = x_sd_c + mu
+__global__ void add_mean(const double* __restrict__ xc, size_t n, int d,
+                         const PassScalars* __restrict__ sc, double* __restrict__ out) {
+    const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (i >= n * d) return;
+    out[i] = xc[i] + sc->mu[i % d];
+}
+
+// ---- density reduction ----------------------------------------------------------------
+// out[j] (+)= scale * (ca * sum_p part0[p][j] + cb * sum_p part1[p][j])
+struct ReduceArgs {
+    const float* part0;
+    const float* part1;   // may be nullptr
+    int nparts;
+    size_t rows_pad;
+    size_t rows;
+    double ca, cb, scale;
+    int accumulate;
+    double* out;
+    unsigned int* flag_count;   // rows whose Gaussian mass underflows fp32 ranges
+    unsigned int* flag_rows;
+};
+
+__global__ void reduce_density(ReduceArgs a) {
+    const size_t j = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (j >= a.rows) return;
+    double s0 = 0.0, s1 = 0.0;
+    for (int p = 0; p < a.nparts; ++p) s0 += static_cast<double>(a.part0[p * a.rows_pad + j]);
+    if (a.part1)
+        for (int p = 0; p < a.nparts; ++p) s1 += static_cast<double>(a.part1[p * a.rows_pad + j]);
+    if (a.flag_rows && s0 < kDensityFlagMass) {
+        a.flag_rows[atomicAdd(a.flag_count, 1u)] = static_cast<unsigned int>(j);
+        return;
+    }
+    const double v = a.scale * (a.ca * s0 + a.cb * s1);
+    a.out[j] = a.accumulate ? a.out[j] + v : v;
+}
+
+// ---- exact fp64 recompute of flagged rows ---------------------------------------------
+// Rows the fp16/fp32 tensor-core path cannot resolve (all neighbours so far
+// away that phi underflows the operand/accumulator range) are recomputed here
+// with direct-subtraction fp64 distances (the oracle's formulation,
+// oracle.cpp:25-32, 53-85) and a per-row max shift, so the result matches the
+// fp64 reference even where phi ~ 1e-300.  One warp per flagged row.
+struct ExactArgs {
+    int mode;                   // kExactScore / kExactGauss / kExactLaplace
+    const unsigned int* count;
+    const unsigned int* rows;   // local row indices
+    const double* rowpts;       // local row 0's point (original coordinates)
+    size_t row0;                // global index of local row 0 (score: the self column)
+    int center_rows;            // subtract sc->mu from the row points
+    const double* cols;         // column points, n x d
+    size_t n;
+    int d;
+    const PassScalars* sc;
+    double h;                   // kernel bandwidth of this pass
+    double shift;               // score: h^2/2 of the SD shift
+    double norm;                // density: gaussian_norm_const(h, d) / n
+    // score outputs (global row layout) / density output (local layout)
+    double* score;
+    double* xsd_c;
+    double* phi_sum;
+    double* weighted;
+    double* out;
+};
+enum { kExactScore = 0, kExactGauss = 1, kExactLaplace = 2 };
+
+__global__ void __launch_bounds__(256) exact_rows_fp64(ExactArgs a) {
+    const int lane = threadIdx.x & 31;
+    const unsigned int nflag = *a.count;
+    const unsigned int warp_g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned int nwarps = (gridDim.x * blockDim.x) >> 5;
+    const double inv_2h2 = 1.0 / (2.0 * a.h * a.h);
+    for (unsigned int k = warp_g; k < nflag; k += nwarps) {
+        const size_t i = a.rows[k];
+        double x[kMaxDim];
+        for (int c = 0; c < a.d; ++c)
+            x[c] = a.rowpts[i * a.d + c] - (a.center_rows ? a.sc->mu[c] : 0.0);
+        const size_t self = a.mode == kExactScore ? a.row0 + i : ~static_cast<size_t>(0);
+        // pass 1: max exponent
+        double m = -INFINITY;
+        for (size_t j = lane; j < a.n; j += 32) {
+            if (j == self) continue;
+            double r2 = 0.0;
+            for (int c = 0; c < a.d; ++c) {
+                const double df = x[c] - a.cols[j * a.d + c];
+                r2 += df * df;
+            }
+            m = fmax(m, -r2 * inv_2h2);
+        }
+        for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+        // pass 2: shifted sums
+        double S = 0.0, L = 0.0, T[kMaxDim];
+        for (int c = 0; c < kMaxDim; ++c) T[c] = 0.0;
+        if (m > -INFINITY) {
+            for (size_t j = lane; j < a.n; j += 32) {
+                if (j == self) continue;
+                double r2 = 0.0;
+                for (int c = 0; c < a.d; ++c) {
+                    const double df = x[c] - a.cols[j * a.d + c];
+                    r2 += df * df;
+                }
+                const double u = r2 * inv_2h2;
+                const double e = exp(-u - m);
+                S += e;
+                if (a.mode == kExactLaplace) L += e * u;
+                if (a.mode == kExactScore)
+                    for (int c = 0; c < a.d; ++c) T[c] += e * (a.cols[j * a.d + c] - x[c]);
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            S += __shfl_xor_sync(0xffffffffu, S, o);
+            L += __shfl_xor_sync(0xffffffffu, L, o);
+            if (a.mode == kExactScore)
+                for (int c = 0; c < a.d; ++c) T[c] += __shfl_xor_sync(0xffffffffu, T[c], o);
+        }
+        if (lane != 0) continue;
+        const double em = m > -INFINITY ? exp(m) : 0.0;
+        if (a.mode == kExactScore) {
+            const size_t g = a.row0 + i;
+            const double Sp = em * S;
+            const double Stot = 1.0 + Sp;                       // + the self pair
+            if (a.phi_sum) a.phi_sum[g] = Stot;
+            const double inv = 1.0 / (a.h * a.h * Stot);
+            for (int c = 0; c < a.d; ++c) {
+                const double num = em * T[c];                   // sum_j phi_ij (x_j - x_i)
+                const double sc = num * inv;
+                if (a.score) a.score[g * a.d + c] = sc;
+                if (a.xsd_c) a.xsd_c[g * a.d + c] = (x[c] - a.sc->mu[c]) + a.shift * sc;
+                if (a.weighted) a.weighted[g * a.d + c] = num + x[c] * Stot;
+            }
+        } else if (a.mode == kExactGauss) {
+            a.out[i] = a.norm * (em * S);
+        } else {
+            a.out[i] = a.norm * (em * ((1.0 + 0.5 * a.d) * S - L));
+        }
+    }
+}
+
+// ---- public block distances (engine.cpp:41-51 / 261-277 semantics, fp64) ---------------
+__global__ void sq_norms_fp64(const double* __restrict__ x, size_t rows, int d,
+                              double* __restrict__ out) {
+    const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (i >= rows) return;
+    double s = 0.0;
+    for (int c = 0; c < d; ++c) s += x[i * d + c] * x[i * d + c];
+    out[i] = s;
+}
+
+__global__ void block_sq_dists_fp64(const double* __restrict__ a, const double* __restrict__ an,
+                                    size_t na, const double* __restrict__ b,
+                                    const double* __restrict__ bn, size_t nb, int d,
+                                    double* __restrict__ out) {
+    const size_t j = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (j >= nb) return;
+    for (size_t i = blockIdx.y; i < na; i += gridDim.y) {
+        double g = 0.0;
+        for (int c = 0; c < d; ++c) g = fma(a[i * d + c], b[j * d + c], g);
+        const double base = bn[j] + an[i];
+        const double v = base - 2.0 * g;
+        out[i * nb + j] = (v < 16.0 * 2.220446049250313e-16 * base) ? 0.0 : v;
+    }
+}
+
+}  // namespace fkde_b200

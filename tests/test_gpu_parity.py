@@ -1,0 +1,395 @@
+"""GPU parity tests: the B200 engine (through the C ABI) against the fp64 CPU
+oracle and the reference's golden fixtures.
+
+Tolerances (fp32-class operands: 3-term fp16 splits, fp32 accumulation,
+fp64 finalize).  BASELINE.json asks for relative error <= 1e-3 on
+log-density and on the score; the bounds below are tighter:
+  densities (KDE, SD-KDE)   max_component_rel  <= 1e-4   (log-density <= 1e-5)
+  Laplace                   max_rel_vs_peak    <= 1e-4
+  scores                    max_rowwise_rel / max_rel_global_floor (1e-2 floors,
+                            proj/tests/test_util.hpp:53-93) <= 1e-3
+  debiased samples          max_rowwise_rel    <= 1e-4
+Mirrors proj/tests/test_engine.cpp and acceptance_main.cpp crit. 1/2 (whose
+fp64 bounds 1e-8/1e-10 are replaced by the fp32-class bounds above).
+"""
+import ctypes
+import os
+
+import numpy as np
+import pytest
+
+from conftest import (GOLDEN, golden, max_component_rel, max_log_rel, max_rel_global_floor,
+                      max_rel_vs_peak, max_rowwise_rel)
+
+import paper_2602_10378_b200 as fk
+from paper_2602_10378_b200 import _native as N
+
+pytestmark = pytest.mark.gpu
+
+TOL_DENS = 1e-4
+TOL_LAP = 1e-4
+TOL_SCORE = 1e-3
+TOL_DEB = 1e-4
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = fk.Context([0])
+    yield c
+    c.close()
+
+
+@pytest.fixture(scope="module")
+def simt():
+    c = fk.Context([0])
+    c.set_option(N.OPT_ENGINE, N.ENGINE_SIMT)
+    yield c
+    c.close()
+
+
+def _mixture_inputs(port, n, m):
+    import oracle as O
+    w, mu, s = O.default_mixture_16d()
+    seed = port.mix64(0 ^ port.mix64(n))        # sweep.cpp:67-69
+    tr = port.sample_mixture(w, mu, s, n, seed)
+    q = port.sample_mixture(w, mu, s, m, port.mix64(seed ^ 0x71))
+    return tr, q
+
+
+# ---- golden fixtures from the reference oracle ------------------------------------
+def test_score_golden_4096_style(ctx):
+    g = golden("score_1024x16")  # test_engine.cpp:99-105 (first 1024 rows of seed 41)
+    s = fk.score_flash(g["train"], float(g["h"]), ctx=ctx).values
+    assert max_rowwise_rel(s, g["score"]) < TOL_SCORE
+    assert max_rel_global_floor(s, g["score"]) < TOL_SCORE
+
+
+def test_kde_golden_1d(ctx):
+    g = golden("kde_1d")  # test_engine.cpp:123-130
+    v = fk.kde_flash(g["train"], g["queries"], float(g["h"]), ctx=ctx).values
+    assert max_component_rel(v, g["values"]) < TOL_DENS
+
+
+@pytest.mark.parametrize("fused", [True, False])
+def test_laplace_golden_2d(ctx, fused):
+    g = golden("laplace_2d")  # test_engine.cpp:132-143
+    v = fk.kde_flash(g["train"], g["queries"], float(g["h"]), fk.KernelKind.LaplaceCorrected,
+                     fused, ctx=ctx).values
+    assert max_rel_vs_peak(v, g["values"]) < TOL_LAP
+
+
+def test_sdkde_golden_512x16(ctx):
+    g = golden("sdkde_512x16")  # test_engine.cpp:156-166
+    r = fk.sdkde_flash(g["train"], g["queries"], fk.Bandwidth(float(g["h"]), float(g["h_score"])),
+                       ctx=ctx)
+    assert max_component_rel(r.values, g["values"]) < TOL_DENS
+    assert max_rowwise_rel(r.debiased_samples.values, g["debiased"]) < TOL_DEB
+
+
+ACCEPT = sorted(f[:-4] for f in os.listdir(GOLDEN) if f.startswith("accept_"))
+
+
+@pytest.mark.parametrize("name", ACCEPT)
+def test_acceptance_instances(ctx, name):
+    # acceptance_main.cpp:65-135 (crit. 1) on the reference's own instances
+    g = golden(name)
+    tr, q, h = g["train"], g["queries"], float(g["h"])
+    assert max_component_rel(fk.kde_flash(tr, q, h, ctx=ctx).values, g["kde"]) < TOL_DENS
+    lap = fk.kde_flash(tr, q, h, fk.KernelKind.LaplaceCorrected, True, ctx=ctx).values
+    assert max_rel_vs_peak(lap, g["laplace"]) < TOL_LAP
+    assert max_rel_global_floor(fk.score_flash(tr, h, ctx=ctx).values, g["score"]) < TOL_SCORE
+    r = fk.sdkde_flash(tr, q, fk.Bandwidth.uniform(h), ctx=ctx)
+    assert max_component_rel(r.values, g["sdkde"]) < TOL_DENS
+    assert max_rowwise_rel(r.debiased_samples.values, g["debiased"]) < TOL_DEB
+
+
+def test_config1_mixture_4096(ctx, port):
+    # BASELINE config 1: 16-D mixture, n = m = 4096, SD-KDE rate bandwidth
+    c = golden("config1")
+    tr, q = _mixture_inputs(port, 4096, 4096)
+    h, hs = float(c["h"]), float(c["h_silverman"])
+    r = fk.sdkde_flash(tr, q, fk.Bandwidth.uniform(h), ctx=ctx)
+    assert max_component_rel(r.values, c["sdkde"]) < TOL_DENS
+    assert max_log_rel(r.values, c["sdkde"]) < 1e-3  # BASELINE.json's stated metric
+    s = fk.score_flash(tr, h, ctx=ctx).values
+    print("config1 score rowwise", max_rowwise_rel(s, c["score"]), "global",
+          max_rel_global_floor(s, c["score"]))
+    assert max_rowwise_rel(s, c["score"]) < TOL_SCORE
+    assert max_rel_global_floor(s, c["score"]) < TOL_SCORE
+    assert max_component_rel(fk.kde_flash(tr, q, hs, ctx=ctx).values, c["kde"]) < TOL_DENS
+    lap = fk.kde_flash(tr, q, hs, fk.KernelKind.LaplaceCorrected, True, ctx=ctx).values
+    assert max_rel_vs_peak(lap, c["laplace"]) < TOL_LAP
+
+
+# ---- engine properties (test_engine.cpp) -------------------------------------------
+def test_score_accumulate_includes_self_term(ctx, port):
+    tr = port.random_gaussian(65, 2, 43, 3.0)      # test_engine.cpp:114-121
+    acc = fk.score_accumulate(tr, 0.5, ctx=ctx)
+    assert (acc.phi_sum >= 0.99).all() and np.isfinite(acc.phi_sum).all()
+    # raw totals agree with the oracle's definition sum_j phi_ij (x_j)
+    d2 = ((tr[:, None, :] - tr[None, :, :]) ** 2).sum(-1)
+    phi = np.exp(-d2 / (2 * 0.5 ** 2))
+    assert max_component_rel(acc.phi_sum, phi.sum(1)) < 1e-4
+    assert max_rowwise_rel(acc.weighted_sum.values, phi @ tr) < 1e-4
+
+
+def test_laplace_fused_vs_nonfused(ctx, port):
+    tr = port.random_gaussian(2048, 16, 55)        # test_engine.cpp:145-154
+    q = port.random_gaussian(256, 16, 56)
+    a = fk.kde_flash(tr, q, 1.2, fk.KernelKind.LaplaceCorrected, True, ctx=ctx).values
+    b = fk.kde_flash(tr, q, 1.2, fk.KernelKind.LaplaceCorrected, False, ctx=ctx).values
+    assert max_rel_vs_peak(a, b) < 1e-5
+
+
+def test_sdkde_single_point_equals_kde(ctx, port):
+    q = port.random_gaussian(8, 1, 59)             # test_engine.cpp:168-175
+    sd = fk.sdkde_flash(np.array([[0.7]]), q, fk.Bandwidth.uniform(0.6), ctx=ctx)
+    kd = port.kde_naive([0.7], q, 0.6)
+    assert max_component_rel(sd.values, kd) < TOL_DENS
+    assert sd.debiased_samples.values[0, 0] == 0.7
+
+
+def test_determinism_bitwise(ctx, port):
+    tr = port.random_gaussian(700, 3, 65)          # test_engine.cpp:245-262
+    q = port.random_gaussian(300, 3, 66)
+    a = fk.sdkde_flash(tr, q, fk.Bandwidth.uniform(0.5), ctx=ctx).values
+    b = fk.sdkde_flash(tr, q, fk.Bandwidth.uniform(0.5), ctx=ctx).values
+    assert np.array_equal(a, b)
+
+
+def test_partition_invariance_over_cta_counts(port):
+    # Same column splits, different persistent-grid sizes -> bitwise equal
+    # (each output row keeps one owner and a fixed accumulation order).
+    tr, q = _mixture_inputs(port, 8192, 2048)
+    h = 1.4
+    outs = []
+    for ctas in (1, 7, 0):
+        c = fk.Context([0])
+        c.set_option(N.OPT_SPLITS, 3)
+        c.set_option(N.OPT_MAX_CTAS, ctas)
+        outs.append(fk.sdkde_flash(tr, q, fk.Bandwidth.uniform(h), ctx=c).values)
+        c.close()
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+
+
+def test_split_count_reassociation(port):
+    # test_engine.cpp:177-216 analogue: every column split agrees within fp32 rounding
+    tr, q = _mixture_inputs(port, 4096, 1024)
+    h = 1.5
+    base = None
+    for splits in (1, 2, 5, 32):
+        c = fk.Context([0])
+        c.set_option(N.OPT_SPLITS, splits)
+        v = fk.sdkde_flash(tr, q, fk.Bandwidth.uniform(h), ctx=c).values
+        s = fk.score_flash(tr, h, ctx=c).values
+        c.close()
+        if base is None:
+            base = (v, s)
+        else:
+            assert max_component_rel(v, base[0]) < 1e-4
+            assert max_rel_global_floor(s, base[1]) < 1e-4
+
+
+def test_tc_engine_matches_simt_engine(ctx, simt, port):
+    tr, q = _mixture_inputs(port, 4096, 2048)
+    h = 1.5
+    for kernel in (fk.KernelKind.Gaussian, fk.KernelKind.LaplaceCorrected):
+        a = fk.kde_flash(tr, q, h, kernel, True, ctx=ctx).values
+        b = fk.kde_flash(tr, q, h, kernel, True, ctx=simt).values
+        assert max_rel_vs_peak(a, b) < 1e-5
+    a = fk.score_flash(tr, h, ctx=ctx).values
+    b = fk.score_flash(tr, h, ctx=simt).values
+    print("tc vs simt score", max_rel_global_floor(a, b), max_rowwise_rel(a, b))
+    assert max_rel_global_floor(a, b) < 1e-3
+
+
+@pytest.mark.parametrize("n,m,d", [(1, 1, 1), (129, 130, 3), (257, 5, 2), (300, 1, 16),
+                                   (1000, 999, 4)])
+def test_ragged_and_small_shapes(ctx, port, n, m, d):
+    tr = port.random_gaussian(n, d, 1000 + n, 1.5)
+    q = port.random_gaussian(m, d, 2000 + m, 1.5)
+    h = 0.75 * np.sqrt(d)
+    assert max_component_rel(fk.kde_flash(tr, q, h, ctx=ctx).values,
+                             port.kde_naive(tr, q, h)) < TOL_DENS
+    ref_v, ref_deb = port.sdkde_naive(tr, q, h)
+    r = fk.sdkde_flash(tr, q, fk.Bandwidth.uniform(h), ctx=ctx)
+    assert max_component_rel(r.values, ref_v) < TOL_DENS
+    assert max_rowwise_rel(r.debiased_samples.values, ref_deb) < TOL_DEB
+
+
+def test_half_variance_score_bandwidth(ctx, port):
+    tr = port.random_gaussian(600, 16, 71)
+    q = port.random_gaussian(100, 16, 72)
+    bw = fk.Bandwidth.half_variance_score(1.1)
+    r = fk.sdkde_flash(tr, q, bw, ctx=ctx)
+    ref_v, ref_deb = port.sdkde_naive(tr, q, bw.h, bw.h_score)
+    assert max_component_rel(r.values, ref_v) < TOL_DENS
+    assert max_rowwise_rel(r.debiased_samples.values, ref_deb) < TOL_DEB
+
+
+def test_large_offset_data_is_centred(ctx, port):
+    # translation invariance (test_oracle.cpp:31-47): far-from-origin data
+    tr = port.random_gaussian(512, 16, 73) + 1000.0
+    q = port.random_gaussian(64, 16, 74) + 1000.0
+    ref = port.kde_naive(tr, q, 0.9)
+    assert max_component_rel(fk.kde_flash(tr, q, 0.9, ctx=ctx).values, ref) < TOL_DENS
+
+
+def test_wide_spread_data_scales_operands(ctx, port):
+    # |y|^2/2 beyond 2^13 -> the operand scale exponent e > 0 path.  Accuracy
+    # of any Gram-expansion engine degrades with |x - mu|^2 / h^2 (fp32
+    # accumulation of the expanded norms); the bound here is looser, stated.
+    centres = np.array([[40.0, 0, 0, 0], [-40.0, 0, 0, 0], [0, 40.0, 0, 0], [0, -40.0, 0, 0]])
+    tr = port.random_gaussian(800, 4, 75) + np.repeat(centres, 200, axis=0)
+    q = port.random_gaussian(80, 4, 76) + np.repeat(centres, 20, axis=0)
+    h = 0.6
+    v = fk.kde_flash(tr, q, h, ctx=ctx).values
+    ref = port.kde_naive(tr, q, h)
+    err = max_component_rel(v, ref)
+    print("wide-spread kde rel err", err)
+    assert err < 2e-2
+    s = fk.score_flash(tr, h, ctx=ctx).values
+    ref_s = port.score_naive(tr, tr, h)
+    err_s = max_rel_global_floor(s, ref_s)
+    print("wide-spread score err", err_s)
+    assert err_s < 5e-2
+
+
+def test_estimate_dispatch(ctx, port):
+    tr = port.random_gaussian(64, 2, 201)          # test_estimator.cpp:23-65
+    q = port.random_gaussian(32, 2, 202, 3.0)
+    lap = fk.estimate(tr, q, fk.EstimatorConfig(fk.Method.LaplaceKde, fk.Bandwidth.uniform(0.5)),
+                      ctx=ctx)
+    assert lap.negative_mass_estimate is not None and lap.negative_mass_estimate >= 0.0
+    kde = fk.estimate(tr, q, fk.EstimatorConfig(fk.Method.Kde, fk.Bandwidth.uniform(0.5)), ctx=ctx)
+    assert kde.negative_mass_estimate is None and kde.debiased_samples is None
+    sd = fk.estimate(tr, q, fk.EstimatorConfig(fk.Method.Sdkde, fk.Bandwidth.uniform(0.5)), ctx=ctx)
+    assert sd.debiased_samples is not None and sd.negative_mass_estimate is None
+    assert max_component_rel(kde.values, port.kde_naive(tr, q, 0.5)) < TOL_DENS
+    ref_lap = port.laplace_naive(tr, q, 0.5)
+    assert max_rel_vs_peak(lap.values, ref_lap) < TOL_LAP
+    assert abs(lap.negative_mass_estimate - np.maximum(0, -ref_lap).mean()) < 1e-4 * np.abs(ref_lap).max()
+
+
+def test_estimate_through_c_abi(ctx, port):
+    tr = port.random_gaussian(300, 16, 81)
+    q = port.random_gaussian(40, 16, 82)
+    lib = N.load()
+    out = np.empty(40)
+    deb = np.empty((300, 16))
+    neg = ctypes.c_double(-1)
+    idx = ctypes.c_size_t(0)
+    dp = ctypes.POINTER(ctypes.c_double)
+    rc = lib.fkde_gpu_estimate(ctx.handle, tr.ctypes.data_as(dp), 300, q.ctypes.data_as(dp), 40, 16,
+                               N.METHOD_SDKDE, 1.1, 1.1, 64, 1024, 1, out.ctypes.data_as(dp),
+                               deb.ctypes.data_as(dp), ctypes.byref(neg), ctypes.byref(idx))
+    assert rc == N.OK
+    ref_v, ref_deb = port.sdkde_naive(tr, q, 1.1)
+    assert max_component_rel(out, ref_v) < TOL_DENS
+    rc = lib.fkde_gpu_estimate(ctx.handle, tr.ctypes.data_as(dp), 300, q.ctypes.data_as(dp), 40, 16,
+                               N.METHOD_KDE, 1.1, 1.1, 0, 1024, 1, out.ctypes.data_as(dp), None,
+                               None, None)
+    assert rc == N.INVALID_ARGUMENT
+
+
+def test_errors(ctx, port):
+    with pytest.raises(fk.UnsupportedDimensionError):
+        fk.kde_flash(port.random_gaussian(10, 17, 1), port.random_gaussian(3, 17, 2), 1.0, ctx=ctx)
+    # device-side non-finite detection through the raw ABI (the host mirror
+    # rejects NaN before the call, like SampleSet::validate)
+    lib = N.load()
+    tr = port.random_gaussian(50, 2, 3)
+    tr[7, 1] = np.nan
+    out = np.empty(5)
+    dp = ctypes.POINTER(ctypes.c_double)
+    q = port.random_gaussian(5, 2, 4)
+    rc = lib.fkde_gpu_kde(ctx.handle, tr.ctypes.data_as(dp), 50, q.ctypes.data_as(dp), 5, 2, 1.0,
+                          0, 1, out.ctypes.data_as(dp))
+    assert rc == N.NON_FINITE
+    # the context stays usable after a reported error
+    tr[7, 1] = 0.0
+    v = fk.kde_flash(tr, q, 1.0, ctx=ctx).values
+    assert max_component_rel(v, port.kde_naive(tr, q, 1.0)) < TOL_DENS
+
+
+# ---- pairwise_sq_dists_block (test_engine.cpp:125-192) --------------------------------
+def test_pairwise_pythagorean_and_identical_rows(ctx, port):
+    d2 = fk.pairwise_sq_dists_block([[0.0, 0.0], [3.0, 4.0]], [[3.0, 4.0]], ctx=ctx).values
+    assert abs(d2[0, 0] - 25.0) < 25.0 * 1e-14 and d2[1, 0] == 0.0
+    for d in (1, 4, 16):
+        a = port.random_gaussian(10, d, 33 + d, 2.5)
+        b = port.random_gaussian(10, d, 34 + d, 2.5)
+        b[7] = a[2]
+        assert fk.pairwise_sq_dists_block(a, b, ctx=ctx).values[2, 7] == 0.0
+
+
+def test_pairwise_never_negative_and_tight(ctx, port):
+    eps = np.finfo(float).eps
+    a = port.random_gaussian(32, 4, 31, 1e-4) + 100.0
+    b = port.random_gaussian(32, 4, 32, 1e-4) + 100.0
+    d2 = fk.pairwise_sq_dists_block(a, b, ctx=ctx).values
+    direct = ((a[:, None] - b[None]) ** 2).sum(-1)
+    na = (a * a).sum(1)[:, None] + (b * b).sum(1)[None]
+    assert (d2 >= 0).all()
+    assert (np.abs(d2 - direct) < 16 * eps * na).all()
+
+
+# ---- device-resident and multi-rank entry points ------------------------------------------
+def test_device_resident_api_matches_host_api(ctx, port):
+    torch = pytest.importorskip("torch")
+    tr, q = _mixture_inputs(port, 3000, 700)
+    h = 1.5
+    host = fk.sdkde_flash(tr, q, fk.Bandwidth.uniform(h), ctx=ctx).values
+    dX = torch.from_numpy(tr).cuda()
+    dY = torch.from_numpy(q).cuda()
+    dO = torch.empty(700, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    lib = N.load()
+    rc = lib.fkde_gpu_sdkde_device(ctx.handle, dX.data_ptr(), 3000, dY.data_ptr(), 700, 16, h, h,
+                                   dO.data_ptr())
+    assert rc == N.OK
+    s = torch.cuda.ExternalStream(ctx.stream())
+    s.synchronize()
+    assert np.array_equal(dO.cpu().numpy(), host)
+    assert ctx.last_launch_count() >= 8
+
+
+def test_rank_context_world1_matches(ctx, port):
+    tr, q = _mixture_inputs(port, 2000, 500)
+    r1 = fk.sdkde_flash(tr, q, fk.Bandwidth.uniform(1.5), ctx=ctx).values
+    rc = fk.Context(rank=0, world=1, device=0)
+    r2 = fk.sdkde_flash(tr, q, fk.Bandwidth.uniform(1.5), ctx=rc).values
+    rc.close()
+    assert np.array_equal(r1, r2)
+
+
+# ---- full-size configurations: size-independent checks on row subsamples ------------------
+@pytest.mark.slow
+def test_config5_headline_subsample(ctx, port):
+    # n = 2^20, m = 2^17 (BASELINE config 5).  The oracle is exactly linear in
+    # evaluated rows, so parity is checked on a deterministic row subsample.
+    n, m = 1 << 20, 1 << 17
+    tr, q = _mixture_inputs(port, n, m)
+    h = port.sdkde_bandwidth(tr, port.silverman_prefactor(16))
+    r = fk.sdkde_flash(tr, q, fk.Bandwidth.uniform(h), ctx=ctx)
+    v, deb = r.values, r.debiased_samples.values
+    assert np.isfinite(v).all() and (v > 0).all()
+    rows = np.linspace(0, n - 1, 24).astype(int)
+    sc = port.score_naive(tr, tr[rows], h, threads=os.cpu_count())
+    ref_deb = tr[rows] + 0.5 * h * h * sc
+    assert max_rowwise_rel(deb[rows], ref_deb) < TOL_DEB
+    qs = np.linspace(0, m - 1, 48).astype(int)
+    ref_v = port.kde_naive(deb, q[qs], h, threads=os.cpu_count())
+    assert max_component_rel(v[qs], ref_v) < TOL_DENS
+    assert max_log_rel(v[qs], ref_v) < 1e-3
+
+
+@pytest.mark.slow
+def test_config4_laplace_subsample(ctx, port):
+    n, m = 262144, 65536
+    tr, q = _mixture_inputs(port, n, m)
+    h = port.silverman_bandwidth(tr)
+    v = fk.kde_flash(tr, q, h, fk.KernelKind.LaplaceCorrected, True, ctx=ctx).values
+    qs = np.linspace(0, m - 1, 64).astype(int)
+    ref = port.laplace_naive(tr, q[qs], h, threads=os.cpu_count())
+    assert max_rel_vs_peak(v[qs], ref) < TOL_LAP
