@@ -1,0 +1,347 @@
+#!/usr/bin/env python3
+"""Benchmark: Flash-SD-KDE headline workload (BASELINE config 5) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one full SD-KDE over n = 2^20 training points and m = 2^17 queries
+in d = 16 (score pass -> x + h^2/2 s -> density pass), inputs drawn from the
+reference's 16-D Gaussian mixture with its runtime-sweep seeds and SD-KDE
+rate bandwidth.  N > 1 runs under torchrun, one process per GPU: rows are
+sharded for the score pass, the debiased samples are allgathered (NCCL),
+queries are sharded for the density pass (total work fixed: strong scaling).
+
+value  = queries/s of the whole job, inputs resident in HBM (fp64), timed on
+         the engine's stream with CUDA events, max over ranks.
+e2e    = same metric through the host C ABI call (fkde_gpu_sdkde) from pinned
+         host buffers: H2D of X and Y, D2H of densities and debiased samples.
+--impl reference: the reference's own CPU oracle (oracle/_ref, or the C port
+         when _ref is absent) on a bounded row sample, all host threads,
+         extrapolated linearly in evaluated rows (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_TRAIN = 1 << 20
+N_QUERY = 1 << 17
+DIM = 16
+METRIC = "SD-KDE wall s & queries/sec, n=1M d=16, 131k queries, at 1/2/4/8 B200 vs CPU ref"
+PAPER_WALL_S = 2.3  # PAPER.md:30, 592 (RTX A6000), BASELINE.md section 1
+MUFU_EX2_PER_CLK_SM = 16
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f), "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+# ---- clocks sampler ------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---- inputs -------------------------------------------------------------------------
+def make_inputs(n, m):
+    from paper_2602_10378_b200 import fixtures as F
+    X, Y = F.runtime_sweep_inputs(n, m, seed=0)
+    h = F.sdkde_bandwidth(X)  # BandwidthPolicy Auto for SD-KDE (sweep.cpp:31-61)
+    return X, Y, h
+
+
+# ---- CPU baseline (the reference oracle, bounded sample) ------------------------------
+def cpu_oracle_sample(X, Y, h, rows_score=128, rows_query=128):
+    """Times the reference's naive oracle on a row sample; returns (extrapolated
+    full-workload seconds, details).  Cost is exactly linear in evaluated rows."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    kind = "reference" if O.reference_available() else "port"
+    orc = O.get(kind)
+    threads = os.cpu_count() or 1
+    n, m = X.shape[0], Y.shape[0]
+    rs = np.linspace(0, n - 1, rows_score).astype(np.int64)
+    t0 = time.perf_counter()
+    orc.score_naive(X, X[rs], h, threads=threads)
+    t1 = time.perf_counter()
+    qs = np.linspace(0, m - 1, rows_query).astype(np.int64)
+    orc.kde_naive(X, Y[qs], h, threads=threads)  # same cost as against the debiased set
+    t2 = time.perf_counter()
+    full = (t1 - t0) * n / rows_score + (t2 - t1) * m / rows_query
+    sample = (f"score_naive on {rows_score} of {n} rows + kde_naive on {rows_query} of {m} "
+              f"queries (x {n} train), {threads} threads, extrapolated linearly in rows")
+    return full, {"kind": kind, "cores": threads, "sample": sample,
+                  "sample_s": t2 - t0}
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    X, Y, h = make_inputs(N_TRAIN, N_QUERY)
+    for _ in range(args.warmup):
+        cpu_oracle_sample(X, Y, h, 32, 32)
+    walls = []
+    info = None
+    for _ in range(args.steps):
+        full, info = cpu_oracle_sample(X, Y, h)
+        walls.append(full)
+    wall = float(np.median(walls))
+    qps = N_QUERY / wall
+    line = {
+        "impl": "reference", "metric": METRIC, "value": qps, "unit": "queries/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": wall * 1e3, "wall_s": wall, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: reference 16-D Gaussian mixture, runtime-sweep seeds",
+        "config": {"workload": f"SD-KDE n={N_TRAIN} m={N_QUERY} d={DIM} (BASELINE config 5)",
+                   "h": h, "parallelism": "host threads"},
+        "cpu_baseline": dict(info, value=qps, unit="queries/s"),
+        "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---- our arm ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import paper_2602_10378_b200 as fk
+    from paper_2602_10378_b200 import _native as N
+
+    rank, world, local = env_rank()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        uid = [fk.engine.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx = fk.Context(rank=rank, world=world, device=local, nccl_id=uid[0])
+    else:
+        torch.cuda.set_device(0)
+        ctx = fk.Context([local])
+    lib = N.load()
+    dev = torch.device("cuda", local)
+
+    X, Y, h = make_inputs(N_TRAIN, N_QUERY)
+    n, m, d = X.shape[0], Y.shape[0], X.shape[1]
+    dX = torch.from_numpy(X).to(dev)
+    dY = torch.from_numpy(Y).to(dev)
+    dO = torch.empty(m, dtype=torch.float64, device=dev)
+    stream = torch.cuda.ExternalStream(ctx.stream(), device=dev)
+    ctx.set_option(N.OPT_TIMING, 1)
+
+    def step():
+        rc = lib.fkde_gpu_sdkde_device(ctx.handle, dX.data_ptr(), n, dY.data_ptr(), m, d, h, h,
+                                       dO.data_ptr())
+        if rc != 0:
+            raise RuntimeError(ctx.last_error())
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        stream.synchronize()
+        if dist:
+            dist.barrier()
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    barrier()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    score_ms, query_ms, launches = [], [], 0
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+        t = ctx.last_timing()  # syncs on this step's last event
+        score_ms.append(t[N.T_SCORE])
+        query_ms.append(t[N.T_QUERY])
+        launches += ctx.last_launch_count()
+    ev1.record(stream)
+    barrier()
+    dev_ms = ev0.elapsed_time(ev1)
+    clocks = sampler.stop()
+
+    # e2e through the host C ABI (pinned host buffers, H2D + D2H inside)
+    pX = torch.from_numpy(X).pin_memory()
+    pY = torch.from_numpy(Y).pin_memory()
+    pO = torch.empty(m, dtype=torch.float64).pin_memory()
+    pD = torch.empty((n, d), dtype=torch.float64).pin_memory()
+    import ctypes
+    dp = ctypes.POINTER(ctypes.c_double)
+    idx = ctypes.c_size_t(0)
+
+    def host_step():
+        rc = lib.fkde_gpu_sdkde(ctx.handle, ctypes.cast(pX.data_ptr(), dp), n,
+                                ctypes.cast(pY.data_ptr(), dp), m, d, h, h,
+                                ctypes.cast(pO.data_ptr(), dp), ctypes.cast(pD.data_ptr(), dp),
+                                ctypes.byref(idx))
+        if rc != 0:
+            raise RuntimeError(ctx.last_error())
+
+    host_step()
+    barrier()
+    e2e_steps = max(1, min(args.steps, 3))
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        host_step()
+    barrier()
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    out_ok = bool(np.isfinite(pO.numpy()).all() and (pO.numpy() > 0).all())
+
+    # max over ranks
+    vals = torch.tensor([dev_ms, e2e_s, float(np.mean(score_ms)), float(np.mean(query_ms))],
+                        dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+        lsum = torch.tensor([launches], dtype=torch.float64, device=dev)
+        dist.all_reduce(lsum)
+        launches = int(lsum.item())
+    dev_ms, e2e_s, score_avg, query_avg = [float(v) for v in vals.tolist()]
+
+    if rank == 0:
+        ms_step = dev_ms / args.steps
+        wall = ms_step / 1e3
+        qps = m / wall
+        peaks, src = measured_peaks()
+        sm_mhz = clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
+        max_mhz = peaks.get("sm_max_mhz", 1965.0)
+        # dominant kernel: the score pass; per-launch algorithmic work on this rank
+        rows_rank = -(-n // world)
+        exps = rows_rank * n
+        achieved = exps / (score_avg / 1e3) / 1e9          # Gexp/s
+        peak = 148 * MUFU_EX2_PER_CLK_SM * max_mhz * 1e6 / 1e9
+        tflops = 4 * d * exps / (score_avg / 1e3) / 1e12    # 2 GEMMs x 2d flop per pair
+        prof = os.path.join(ROOT, "profiles", "ncu_score_pass.json")
+        traffic = None
+        if os.path.exists(prof):
+            with open(prof) as f:
+                traffic = json.load(f).get("dram_bytes_per_launch")
+        line = {
+            "metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": world,
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_step,
+            "wall_s": wall, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": qps / (N_QUERY / PAPER_WALL_S),
+            "vs_baseline_note": "paper's 2.3 s on one RTX A6000 (PAPER.md:30), same workload",
+            "dtype": "f32 (fp16 hi/lo split tensor-core operands, f32 accumulate, f64 finalize)",
+            "data": "synthetic: reference 16-D Gaussian mixture (configs/mixture-16d-default.json),"
+                    " reference RNG + runtime-sweep seeds, SD-KDE rate bandwidth",
+            "config": {"workload": f"SD-KDE n={n} m={m} d={d} (BASELINE config 5)", "h": h,
+                       "n_train": n, "n_query": m, "d": d,
+                       "parallelism": f"dp{world}: score rows sharded, 1 NCCL allgather of "
+                                      f"debiased samples, queries sharded",
+                       "l2": "inputs larger than L2 (X fp64 128 MiB; B-operand tiles 128 MiB)"},
+            "phases_ms": {"score_pass": score_avg, "density_pass": query_avg},
+            "clocks": clocks,
+            "e2e": {"value": m / e2e_s, "unit": "queries/s", "wall_s": e2e_s,
+                    "h2d_bytes_per_step": (n + m) * d * 8,
+                    "d2h_bytes_per_step": m * 8 + n * d * 8, "outputs_finite": out_ok},
+            "gpu_launches": launches,
+            "roofline": {"bound": "mufu", "kernel": "pairwise_tc_kernel<Score>",
+                         "achieved": achieved, "peak": peak, "unit": "Gexp/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "peak_source": f"nominal 16 ex2/clk/SM x 148 SMs x sm_max_mhz "
+                                        f"{max_mhz:.0f} ({src} MEASURED_PEAKS)",
+                         "frac_at_observed_clock": exps / (score_avg / 1e3) /
+                         (148 * MUFU_EX2_PER_CLK_SM * sm_mhz * 1e6),
+                         "tensor": {"achieved_tflops": tflops,
+                                    "peak_tflops": peaks.get("bf16_tflops"),
+                                    "frac": tflops / peaks.get("bf16_tflops", 1590.0),
+                                    "note": "algorithmic 2x(2d) flop/pair vs dense bf16 peak"}},
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            full, info = cpu_oracle_sample(X, Y, h)
+            line["cpu_baseline"] = dict(info, value=N_QUERY / full, unit="queries/s",
+                                        wall_s=full)
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -142,6 +142,18 @@ int fkde_gpu_sdkde_device(fkde_gpu_ctx* ctx, const double* dX, size_t n, const d
 int fkde_gpu_kde_device(fkde_gpu_ctx* ctx, const double* dX, size_t n, const double* dY,
                         size_t m, size_t d, double h, int kernel, int fused, double* d_out);
 
+/* ---- host-side input fixtures (bench / CLI), not on the device path -------
+ * Bitwise reproductions of the reference's RNG (rng.cpp, mixture.cpp:40-67,
+ * test_util.hpp:12-20) and bandwidth rules (bandwidth.cpp:9-58). */
+uint64_t fkde_host_mix64(uint64_t x);
+void fkde_host_random_gaussian(size_t n, size_t d, uint64_t seed, double scale, double* out);
+int fkde_host_sample_mixture(const double* weights, const double* means, const double* sigmas,
+                             size_t k, size_t d, size_t n, uint64_t seed, double* out);
+double fkde_host_mean_stddev(const double* x, size_t n, size_t d);
+double fkde_host_silverman_prefactor(size_t d);
+double fkde_host_silverman_bandwidth(const double* x, size_t n, size_t d);
+double fkde_host_sdkde_bandwidth(const double* x, size_t n, size_t d, double c);
+
 #ifdef __cplusplus
 }
 #endif

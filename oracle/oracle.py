@@ -223,9 +223,10 @@ def reference_available() -> bool:
 
 
 def default_mixture_16d():
-    """configs/mixture-16d-default.json, frozen into tests/golden/mixture_16d.json."""
+    """The reference's configs/mixture-16d-default.json (data file shipped with the package)."""
     import json
-    path = os.path.join(os.path.dirname(HERE), "tests", "golden", "mixture_16d.json")
+    path = os.path.join(os.path.dirname(HERE), "paper_2602_10378_b200", "configs",
+                        "mixture-16d-default.json")
     with open(path) as f:
         j = json.load(f)
     return (np.asarray(j["weights"], dtype=np.float64), np.asarray(j["means"], dtype=np.float64),

@@ -40,6 +40,11 @@ EXPORTED_SYMBOLS = (
     "fkde_gpu_estimate", "fkde_gpu_pairwise_sq_dists", "fkde_gpu_sdkde_device",
     "fkde_gpu_kde_device", "fkde_gpu_shard_range",
 )
+HOST_SYMBOLS = (
+    "fkde_host_mix64", "fkde_host_random_gaussian", "fkde_host_sample_mixture",
+    "fkde_host_mean_stddev", "fkde_host_silverman_prefactor", "fkde_host_silverman_bandwidth",
+    "fkde_host_sdkde_bandwidth",
+)
 
 _lib = None
 
@@ -81,6 +86,18 @@ def _declare(lib):
     lib.fkde_gpu_kde_device.argtypes = [_vp, _vp, _sz, _vp, _sz, _sz, ctypes.c_double,
                                         ctypes.c_int, ctypes.c_int, _vp]
     lib.fkde_gpu_shard_range.argtypes = [_sz, ctypes.c_int, ctypes.c_int, _sz, _szp, _szp, _szp]
+    lib.fkde_host_mix64.argtypes = [ctypes.c_uint64]
+    lib.fkde_host_mix64.restype = ctypes.c_uint64
+    lib.fkde_host_random_gaussian.argtypes = [_sz, _sz, ctypes.c_uint64, ctypes.c_double, _dp]
+    lib.fkde_host_random_gaussian.restype = None
+    lib.fkde_host_sample_mixture.argtypes = [_dp, _dp, _dp, _sz, _sz, _sz, ctypes.c_uint64, _dp]
+    for f in ("fkde_host_mean_stddev", "fkde_host_silverman_bandwidth"):
+        getattr(lib, f).argtypes = [_dp, _sz, _sz]
+        getattr(lib, f).restype = ctypes.c_double
+    lib.fkde_host_silverman_prefactor.argtypes = [_sz]
+    lib.fkde_host_silverman_prefactor.restype = ctypes.c_double
+    lib.fkde_host_sdkde_bandwidth.argtypes = [_dp, _sz, _sz, ctypes.c_double]
+    lib.fkde_host_sdkde_bandwidth.restype = ctypes.c_double
     return lib
 
 

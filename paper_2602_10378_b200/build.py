@@ -15,7 +15,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libfkde_b200.so")
-SOURCES = ["fkde_gpu.cu"]
+SOURCES = ["fkde_gpu.cu", "host_fixtures.cpp"]
 HEADERS = ["ptx.cuh", "layout.cuh", "pairwise_tc.cuh", "pairwise_simt.cuh", "prep_kernels.cuh"]
 
 NVCC_FLAGS = [

@@ -18,7 +18,7 @@ from paper_2602_10378_b200 import _native as N
 
 def header_symbols():
     src = open(os.path.join(ROOT, "include", "fkde_gpu.h")).read()
-    return sorted(set(re.findall(r"\b(fkde_gpu_\w+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(fkde_(?:gpu|host)_\w+)\s*\(", src)))
 
 
 def test_library_exports_every_declared_symbol():
@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     assert len(syms) >= 19
     for s in syms:
         assert hasattr(lib, s), s
-    assert set(syms) == set(N.EXPORTED_SYMBOLS)
+    assert set(syms) == set(N.EXPORTED_SYMBOLS) | set(N.HOST_SYMBOLS)
 
 
 def test_library_is_sm100a_only():
@@ -136,3 +136,20 @@ def test_product_package_does_not_import_oracle():
                 src = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in src and "liboracle" not in src, f
                 assert "fkde_oracle" not in src and "libfkde_ref" not in src, f
+
+
+def test_host_fixtures_match_reference_rng(port):
+    # the product's input generators reproduce the reference's RNG bitwise
+    from paper_2602_10378_b200 import fixtures as F
+    assert F.mix64(12345) == port.mix64(12345)
+    assert np.array_equal(F.random_gaussian(100, 3, 41, 1.5), port.random_gaussian(100, 3, 41, 1.5))
+    w, mu, s = F.mixture_16d()
+    seed = F.cell_data_seed(0, 4096)
+    a = F.sample_mixture(w, mu, s, 500, seed)
+    assert np.array_equal(a, port.sample_mixture(w, mu, s, 500, seed))
+    assert F.sdkde_bandwidth(a) == port.sdkde_bandwidth(a, port.silverman_prefactor(16))
+    assert F.silverman_bandwidth(a) == port.silverman_bandwidth(a)
+    tr, q = F.runtime_sweep_inputs(4096, 64)
+    from conftest import golden
+    c = golden("config1")
+    assert np.array_equal(tr[:8], c["train_head"]) and np.array_equal(q[:8], c["query_head"])

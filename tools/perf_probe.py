@@ -67,6 +67,8 @@ def run(ctx, kind, n, m, reps=5, seed=0):
 def main():
     ctx = fk.Context([0])
     which = sys.argv[1:] or ["small", "big"]
+    if "sd32k" in which:
+        run(ctx, "sdkde", 32768, 32768, reps=1)
     if "small" in which:
         run(ctx, "sdkde", 4096, 4096)
         run(ctx, "sdkde", 32768, 32768)
