@@ -67,7 +67,9 @@ enum {
     FKDE_OPT_ENGINE = 1,      /* FKDE_ENGINE_TC (default) | FKDE_ENGINE_SIMT     */
     FKDE_OPT_SPLITS = 2,      /* 0 = auto; >0 forces column splits per row tile  */
     FKDE_OPT_TIMING = 3,      /* 1 = record per-phase CUDA-event times            */
-    FKDE_OPT_MAX_CTAS = 4     /* 0 = all SMs; >0 caps the persistent grid        */
+    FKDE_OPT_MAX_CTAS = 4,    /* 0 = all SMs; >0 caps the persistent grid        */
+    FKDE_OPT_FLUSH_TILES = 5  /* score pass: drain the TMEM accumulator to fp64
+                                 registers every k column tiles (default 2)    */
 };
 enum { FKDE_ENGINE_TC = 0, FKDE_ENGINE_SIMT = 1 };
 

@@ -10,7 +10,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfkde_b200.so")
+# FKDE_B200_LIB overrides the library path (A/B timing of two in-tree builds)
+LIB_PATH = os.environ.get("FKDE_B200_LIB") or os.path.join(HERE, "libfkde_b200.so")
 
 # fkde_status
 OK = 0
@@ -27,7 +28,7 @@ KERNEL_GAUSSIAN = 0
 KERNEL_LAPLACE_CORRECTED = 1
 METHOD_KDE, METHOD_SDKDE, METHOD_LAPLACE = 0, 1, 2
 
-OPT_ENGINE, OPT_SPLITS, OPT_TIMING, OPT_MAX_CTAS = 1, 2, 3, 4
+OPT_ENGINE, OPT_SPLITS, OPT_TIMING, OPT_MAX_CTAS, OPT_FLUSH_TILES = 1, 2, 3, 4, 5
 ENGINE_TC, ENGINE_SIMT = 0, 1
 
 T_PREP, T_SCORE, T_FINALIZE, T_GATHER, T_QUERY, T_REDUCE, T_TOTAL, T_COUNT = range(8)

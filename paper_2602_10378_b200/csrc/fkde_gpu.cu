@@ -152,6 +152,7 @@ struct Options {
     int splits = 0;
     int timing = 0;
     int max_ctas = 0;
+    int flush_tiles = 2;
 };
 
 struct Device {
@@ -294,7 +295,7 @@ Status density_pass(Device& D, const Options& o, int mode, size_t rows_pad, size
     const size_t nparts = static_cast<size_t>(splits) * 2;
     STATUS_TRY(ensure(D.part0, nparts * rows_pad * sizeof(float)));
     if (mode == kModeLaplace) STATUS_TRY(ensure(D.part1, nparts * rows_pad * sizeof(float)));
-    PairArgs a;
+    PairArgs a{};
     a.opA = D.opA.as<uint8_t>();
     a.opB = D.opB.as<uint8_t>();
     a.n_row_tiles = static_cast<int>(rt);
@@ -303,6 +304,7 @@ Status density_pass(Device& D, const Options& o, int mode, size_t rows_pad, size
     a.sc = sc;
     a.part0 = D.part0.as<float>();
     a.part1 = mode == kModeLaplace ? D.part1.as<float>() : nullptr;
+    a.flush_tiles = 1;
     a.rows_pad = rows_pad;
     a.diag_tile0 = -1;
     if (mode == kModeGauss)
@@ -377,17 +379,19 @@ Status score_program(Device& D, const Options& o, const Job& J, const double* dX
     const size_t rt = rows_pad / kTileRows, ct = cols_pad / kTileRows;
     const int ctas = o.max_ctas > 0 ? std::min(o.max_ctas, D.num_sms) : D.num_sms;
     const int splits = o.engine == FKDE_ENGINE_SIMT ? 1 : choose_splits(o, rt, ct, ctas);
-    STATUS_TRY(ensure(D.part0, static_cast<size_t>(splits) * rows_pad * sizeof(float)));
-    STATUS_TRY(ensure(D.part1, static_cast<size_t>(splits) * rows_pad * kMaxDim * sizeof(float)));
-    PairArgs a;
+    // fp64 partials per (split, column half)
+    STATUS_TRY(ensure(D.part0, 2 * static_cast<size_t>(splits) * rows_pad * sizeof(double)));
+    STATUS_TRY(ensure(D.part1, 2 * static_cast<size_t>(splits) * rows_pad * kMaxDim * sizeof(double)));
+    PairArgs a{};
     a.opA = D.opA.as<uint8_t>();
     a.opB = D.opB.as<uint8_t>();
     a.n_row_tiles = static_cast<int>(rt);
     a.n_col_tiles = static_cast<int>(ct);
     a.splits = splits;
     a.sc = sc;
-    a.part0 = D.part0.as<float>();
-    a.part1 = D.part1.as<float>();
+    a.dpart0 = D.part0.as<double>();
+    a.dpart1 = D.part1.as<double>();
+    a.flush_tiles = std::max(1, o.flush_tiles);
     a.rows_pad = rows_pad;
     a.diag_tile0 = static_cast<int>(sh.begin / kTileRows);
     STATUS_TRY(launch_pairwise<kModeScore>(D, o, a, n));
@@ -395,9 +399,9 @@ Status score_program(Device& D, const Options& o, const Job& J, const double* dX
 
     const size_t nrows_g = sh.chunk * D.world;  // gather layout
     FinalizeArgs f{};
-    f.part_s = D.part0.as<float>();
-    f.part_t = D.part1.as<float>();
-    f.splits = splits;
+    f.part_s = D.part0.as<double>();
+    f.part_t = D.part1.as<double>();
+    f.splits = 2 * splits;
     f.rows_pad = rows_pad;
     f.rows = sh.rows;
     f.row0 = sh.begin;
@@ -870,6 +874,10 @@ int fkde_gpu_set_option(fkde_gpu_ctx* ctx, int key, int64_t value) {
         case FKDE_OPT_MAX_CTAS:
             if (value < 0) return FKDE_INVALID_ARGUMENT;
             ctx->opt.max_ctas = static_cast<int>(value);
+            return FKDE_OK;
+        case FKDE_OPT_FLUSH_TILES:
+            if (value < 1 || value > 1 << 20) return FKDE_INVALID_ARGUMENT;
+            ctx->opt.flush_tiles = static_cast<int>(value);
             return FKDE_OK;
         default:
             return FKDE_INVALID_ARGUMENT;

@@ -14,15 +14,16 @@
 //
 //   chunk   A (row side)                 B (column side)
 //   0-1     y_hi[0:16]                   y_hi[0:16]
-//   2-3     y_hi[0:16]                   y_lo[0:16]
-//   4       a1 a2 a3 1 1 1 0 0           1 1 1 b1 b2 b3 0 0     (a,b = -|y|^2/2 split)
-//   5       0                            0
+//   2       a1 a2 a3 1 1 1 0 0           1 1 1 b1 b2 b3 0 0     (a,b = -|y|^2/2 split)
+//   3       0                            0
+//   4-5     y_hi[0:16]                   y_lo[0:16]
 //   6-7     y_lo[0:16]                   y_hi[0:16]
 //
 // The B rows double as the MN-major B operand of the score pass's second GEMM
-// (P . [y_hi | y_lo | 1]): its first 48 columns give sum_j phi_ij y_hi_j,
-// sum_j phi_ij y_lo_j and sum_j phi_ij (the ones column -- S comes off the
-// tensor core from the same rounded phi as T).
+// (P . B[:, 0:48]): output columns 0-15 = sum_j phi_ij y_hi_j, 16-18 =
+// sum_j phi_ij (the ones -- S comes off the tensor core from the same rounded
+// phi as T), 32-47 = sum_j phi_ij y_lo_j.  The first 32 columns (T_hi, S) are
+// drained to fp64 every few tiles; T_lo (2^-11 smaller) only at the end.
 //
 // Rows are grouped in tiles of 128 (16 KiB, contiguous) stored exactly as the
 // SWIZZLE_128B shared-memory image: 16-byte chunk c of row r lives at

@@ -23,7 +23,7 @@ __device__ __forceinline__ void unpack_y(const uint8_t* tiles, size_t row, bool 
     const uint4* base = reinterpret_cast<const uint4*>(tiles + tile * kTileBytes + r * kRowBytes);
     __align__(16) __half hi[16];
     __align__(16) __half lo[16];
-    const int lo_chunk = a_format ? 6 : 2;
+    const int lo_chunk = a_format ? 6 : 4;
     for (int c = 0; c < 2; ++c) {
         reinterpret_cast<uint4*>(hi)[c] = base[c ^ (r & 7)];
         reinterpret_cast<uint4*>(lo)[c] = base[(lo_chunk + c) ^ (r & 7)];
@@ -72,10 +72,15 @@ __global__ void __launch_bounds__(128) pairwise_simt_kernel(PairArgs args, size_
             }
         }
     }
-    args.part0[row] = s0;
     if constexpr (MODE == kModeScore) {
-        for (int k = 0; k < 16; ++k) args.part1[row * kMaxDim + k] = t[k];
+        args.dpart0[row] = s0;
+        args.dpart0[args.rows_pad + row] = 0.0;  // second column half (tc layout) is empty
+        for (int k = 0; k < 16; ++k) {
+            args.dpart1[row * kMaxDim + k] = t[k];
+            args.dpart1[(args.rows_pad + row) * kMaxDim + k] = 0.0;
+        }
     } else {
+        args.part0[row] = s0;
         args.part0[args.rows_pad + row] = 0.f;  // second column half (tc layout) is empty
         if constexpr (MODE == kModeLaplace) {
             args.part1[row] = s1;

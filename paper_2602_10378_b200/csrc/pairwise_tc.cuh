@@ -50,8 +50,11 @@ struct PairArgs {
     int n_col_tiles;
     int splits;           // column ranges per row tile
     const PassScalars* sc;
-    float* part0;         // SCORE: S [splits][rows_pad]; KDE: [splits*2][rows_pad]
-    float* part1;         // SCORE: T [splits][rows_pad][16]; Laplace: [splits*2][rows_pad]
+    float* part0;         // KDE: [splits*2][rows_pad]
+    float* part1;         // Laplace: [splits*2][rows_pad]
+    double* dpart0;       // SCORE: S' [splits*2][rows_pad]   (fp64, per column half)
+    double* dpart1;       // SCORE: T' [splits*2][rows_pad][16] (fp64)
+    int flush_tiles;      // SCORE: O is drained to fp64 registers every this many tiles
     size_t rows_pad;
     // SCORE: column tile holding row tile 0's diagonal (rows and columns are
     // the same point set, row shard start = diag_tile0 * 128); the self pair
@@ -67,11 +70,21 @@ struct TcConfig {
     static constexpr int kThreads = 320;
     static constexpr uint32_t kOffA = 0;
     static constexpr uint32_t kOffB = 2 * kTileBytes;
-    static constexpr uint32_t kOffBar = kOffB + kStages * kTileBytes;
-    static constexpr uint32_t kNumBars = 4 + 2 * kStages + 4 + 4 + 2;
+    // score: fp64 drain accumulators, [2 halves][128 rows][kAccStride] doubles
+    static constexpr uint32_t kAccStride = 17;
+    static constexpr uint32_t kOffAcc = kOffB + kStages * kTileBytes;
+    static constexpr uint32_t kAccBytes = kScore ? 2 * 128 * kAccStride * 8 : 0;
+    static constexpr uint32_t kOffBar = kOffAcc + kAccBytes;
+    // S accumulators in TMEM (128 columns each).  Score: 3 (S/P of tiles
+    // t, t+1, t+2 in flight, GEMM2 lags GEMM1 by two tiles) + O[2] at 384.
+    // KDE: 4.
+    static constexpr int kSBuf = kScore ? 3 : 4;
+    static constexpr int kLag = kSBuf - 1;   // score: GEMM2(t) issued after GEMM1(t + kLag)
+    static constexpr uint32_t kNumBars = 4 + 2 * kStages + 4 * 4 + 4 + 2;
     static constexpr uint32_t kSmemBytes = kOffBar + kNumBars * 8 + 16 + 1024;  // + align slack
     static constexpr uint32_t kTmemCols = 512;
-    static constexpr uint32_t kTmemO = 256;   // O accumulator column (score)
+    static constexpr uint32_t kTmemO = 384;   // score: O_hi[2] (2 x 32 cols: T_hi, S)
+    static constexpr uint32_t kTmemOlo = 448; // score: O_lo (16 cols: T_lo), per unit
     static constexpr uint32_t kN2 = 48;       // GEMM2 N
 };
 
@@ -91,13 +104,15 @@ __global__ void __launch_bounds__(320, 1) pairwise_tc_kernel(PairArgs args) {
     uint64_t* a_empty = bars + 2;         // [2]
     uint64_t* b_full = bars + 4;          // [kStages]
     uint64_t* b_empty = b_full + kStages; // [kStages]
-    uint64_t* s_full = b_empty + kStages; // [2]
-    uint64_t* s_empty = s_full + 2;       // [2]
-    uint64_t* p_full = s_empty + 2;       // [2]
-    uint64_t* p_empty = p_full + 2;       // [2]
-    uint64_t* o_full = p_empty + 2;       // [1]
-    uint64_t* o_empty = o_full + 1;       // [1]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 1);
+    uint64_t* s_full = b_empty + kStages; // [4]
+    uint64_t* s_empty = s_full + 4;       // [4]
+    uint64_t* p_full = s_empty + 4;       // [4]
+    uint64_t* p_empty = p_full + 4;       // [4] (unused: P lives in TMEM)
+    uint64_t* o_full = p_empty + 4;       // [2]
+    uint64_t* o_empty = o_full + 2;       // [2]
+    uint64_t* lo_full = o_empty + 2;      // [1]
+    uint64_t* lo_empty = lo_full + 1;     // [1]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lo_empty + 1);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -106,17 +121,24 @@ __global__ void __launch_bounds__(320, 1) pairwise_tc_kernel(PairArgs args) {
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(&a_full[i], 1);
             ptx::mbar_init(&a_empty[i], 1);
+        }
+        for (int i = 0; i < 4; ++i) {
             ptx::mbar_init(&s_full[i], 1);
             ptx::mbar_init(&s_empty[i], 8);
             ptx::mbar_init(&p_full[i], 8);
-            ptx::mbar_init(&p_empty[i], 1);  // unused (P lives in TMEM)
+            ptx::mbar_init(&p_empty[i], 1);
         }
         for (int i = 0; i < kStages; ++i) {
             ptx::mbar_init(&b_full[i], 1);
             ptx::mbar_init(&b_empty[i], 1);
         }
-        ptx::mbar_init(o_full, 1);
-        ptx::mbar_init(o_empty, 4);
+        for (int i = 0; i < 2; ++i) {
+            ptx::mbar_init(&o_full[i], 1);
+            ptx::mbar_init(&o_empty[i], 4);
+        }
+        ptx::mbar_init(lo_full, 1);
+        ptx::mbar_init(lo_empty, 4);
+
         ptx::fence_barrier_init();
     }
     if (warp == 1) ptx::tmem_alloc<Cfg::kTmemCols>(tmem_slot);
@@ -166,7 +188,9 @@ __global__ void __launch_bounds__(320, 1) pairwise_tc_kernel(PairArgs args) {
         // once and advanced by adding (byte offset >> 4) to the start-address
         // field, so each MMA costs a uniform add + the instruction.
         constexpr uint32_t idesc1 = ptx::idesc_f16_f32(128, 128, false, false);
-        constexpr uint32_t idesc2 = ptx::idesc_f16_f32(128, Cfg::kN2, false, true);
+        constexpr uint32_t idesc2h = ptx::idesc_f16_f32(128, 32, false, true);  // T_hi, S
+        constexpr uint32_t idesc2l = ptx::idesc_f16_f32(128, 16, false, true);  // T_lo
+        uint32_t it_lo = 0;  // units whose O_lo GEMM2 chain has started
         const uint64_t descA = ptx::smem_desc_sw128(ptx::smem_u32(smA), 16, 1024);
         const uint64_t descB = ptx::smem_desc_sw128(ptx::smem_u32(smB), 16, 1024);
         const uint64_t descBmn = ptx::smem_desc_sw128(ptx::smem_u32(smB), kTileBytes, 1024);
@@ -175,28 +199,49 @@ __global__ void __launch_bounds__(320, 1) pairwise_tc_kernel(PairArgs args) {
         // Warp-group hf of the epilogue stored, in S buffer sb's columns
         // [hf*64, hf*64+64): P_hi (packed fp16 pairs) for K = hf*64..+63 in
         // the first 32 columns, P_lo in the next 32.
-        auto gemm2 = [&](uint32_t st, uint32_t sb, uint32_t its, bool first, bool last) {
-            ptx::mbar_wait(&p_full[sb], (its >> 1) & 1);
-            if (first) ptx::mbar_wait(o_empty, (it_u & 1) ^ 1);
+        // O is accumulated in TMEM over `flush_tiles` column tiles (a
+        // "sub-unit"), then drained by the epilogue into fp64 registers; two O
+        // buffers alternate so the drain overlaps the next sub-unit.  This
+        // bounds the tensor core's fp32 accumulation length (its truncation
+        // error grows with the accumulator magnitude x the number of steps).
+        const int F = args.flush_tiles;
+        int sub_left = 0;   // tiles left in the current O sub-unit (no integer modulo)
+        auto gemm2 = [&](uint32_t st, uint32_t sb, uint32_t its, int idx, int ntiles) {
+            if (idx == 0) sub_left = F;
+            const bool first = sub_left == F;
+            --sub_left;
+            const bool last = sub_left == 0 || idx == ntiles - 1;
+            if (last) sub_left = F;
+            const uint32_t ob = it_u & 1;
+            ptx::mbar_wait(&p_full[sb], (its / Cfg::kSBuf) & 1);
+            if (first) ptx::mbar_wait(&o_empty[ob], ((it_u >> 1) & 1) ^ 1);
+            if (idx == 0) ptx::mbar_wait(lo_empty, (it_lo & 1) ^ 1);
             ptx::tc_fence_after();
             if (ptx::elect_one()) {
                 const uint64_t db0 = descBmn + ((st * kTileBytes) >> 4);
                 const uint32_t ta0 = tmem_base + sb * 128;
+                const uint32_t toh = tmem_base + Cfg::kTmemO + ob * 32;
+                const uint32_t tol = tmem_base + Cfg::kTmemOlo;
 #pragma unroll
                 for (int part = 0; part < 2; ++part) {
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
-                        ptx::umma_f16_ts(tmem_base + Cfg::kTmemO,
-                                         ta0 + (k >> 2) * 64 + part * 32 + (k & 3) * 8,
-                                         db0 + ((k * 2048) >> 4), idesc2,
-                                         (first && part == 0 && k == 0) ? 0u : 1u);
+                        const uint32_t ta = ta0 + (k >> 2) * 64 + part * 32 + (k & 3) * 8;
+                        const uint64_t db = db0 + ((k * 2048) >> 4);
+                        // B columns 0-31 (y_hi, ones) -> O_hi (drained every F tiles);
+                        // columns 32-47 (y_lo, 2^-11 smaller) -> O_lo (once per unit)
+                        ptx::umma_f16_ts(toh, ta, db, idesc2h, (first && part == 0 && k == 0) ? 0u : 1u);
+                        ptx::umma_f16_ts(tol, ta, db + (64 >> 4), idesc2l,
+                                         (idx == 0 && part == 0 && k == 0) ? 0u : 1u);
                     }
                 }
                 ptx::umma_commit(&b_empty[st]);
-                if (last) ptx::umma_commit(o_full);
+                if (last) ptx::umma_commit(&o_full[ob]);
+                if (idx == ntiles - 1) ptx::umma_commit(lo_full);
             }
             __syncwarp();
             if (last) ++it_u;
+            if (idx == ntiles - 1) ++it_lo;
         };
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
             const int sp = u % args.splits;
@@ -205,14 +250,13 @@ __global__ void __launch_bounds__(320, 1) pairwise_tc_kernel(PairArgs args) {
             const int ab = it_a & 1;
             ptx::mbar_wait(&a_full[ab], (it_a >> 1) & 1);
             ptx::tc_fence_after();
-            uint32_t prev_st = 0, prev_sb = 0, prev_its = 0;
             for (int ct = ct0; ct < ct1; ++ct) {
                 const uint32_t st = it_b % kStages;
-                const uint32_t sb = it_s & 1;
+                const uint32_t sb = it_s % Cfg::kSBuf;
                 ptx::mbar_wait(&b_full[st], (it_b / kStages) & 1);
-                // KDE: the epilogue frees S after loading it.  SCORE: S/P of
-                // tile it_s-2 was consumed by GEMM2, issued (in order) above.
-                if constexpr (!kScore) ptx::mbar_wait(&s_empty[sb], ((it_s >> 1) & 1) ^ 1);
+                // KDE: the epilogue frees S after loading it.  SCORE: S/P of tile
+                // it_s - kSBuf was consumed by its GEMM2, issued (in order) earlier.
+                if constexpr (!kScore) ptx::mbar_wait(&s_empty[sb], ((it_s / Cfg::kSBuf) & 1) ^ 1);
                 ptx::tc_fence_after();
                 if (ptx::elect_one()) {
                     const uint64_t da0 = descA + ((ab * kTileBytes) >> 4);
@@ -222,7 +266,7 @@ __global__ void __launch_bounds__(320, 1) pairwise_tc_kernel(PairArgs args) {
                     // hi/lo cross terms are added.
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
-                        const int k = kk == 0 ? 2 : (kk == 3 ? 3 : kk - 1);  // 2, 0, 1, 3
+                        const int k = kk == 0 ? 1 : (kk == 1 ? 0 : kk);  // 1 (norms), 0, 2, 3
                         ptx::umma_f16(tmem_base + sb * 128, da0 + ((k * 32) >> 4),
                                       db0 + ((k * 32) >> 4), idesc1, kk > 0 ? 1u : 0u);
                     }
@@ -231,10 +275,10 @@ __global__ void __launch_bounds__(320, 1) pairwise_tc_kernel(PairArgs args) {
                 }
                 __syncwarp();
                 if constexpr (kScore) {
-                    if (ct > ct0) gemm2(prev_st, prev_sb, prev_its, ct - 1 == ct0, false);
-                    prev_st = st;
-                    prev_sb = sb;
-                    prev_its = it_s;
+                    if (ct - Cfg::kLag >= ct0) {
+                        const uint32_t b_ = it_b - Cfg::kLag, s_ = it_s - Cfg::kLag;
+                        gemm2(b_ % kStages, s_ % Cfg::kSBuf, s_, ct - Cfg::kLag - ct0, ct1 - ct0);
+                    }
                 }
                 ++it_b;
                 ++it_s;
@@ -243,7 +287,12 @@ __global__ void __launch_bounds__(320, 1) pairwise_tc_kernel(PairArgs args) {
             __syncwarp();
             ++it_a;
             if constexpr (kScore) {
-                if (ct1 > ct0) gemm2(prev_st, prev_sb, prev_its, ct1 - 1 == ct0, true);
+                // the last kLag tiles' GEMM2s
+                for (int t = ct1 - Cfg::kLag > ct0 ? ct1 - Cfg::kLag : ct0; t < ct1; ++t) {
+                    const uint32_t back = static_cast<uint32_t>(ct1 - t);
+                    const uint32_t b_ = it_b - back, s_ = it_s - back;
+                    gemm2(b_ % kStages, s_ % Cfg::kSBuf, s_, t - ct0, ct1 - ct0);
+                }
             }
         }
     } else {
@@ -253,19 +302,33 @@ __global__ void __launch_bounds__(320, 1) pairwise_tc_kernel(PairArgs args) {
         const int r = q * 32 + lane;        // row within the 128-row tile
         const float dsc = args.sc->dscale;
         const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
-        uint32_t it_s = 0, it_u = 0;
+        uint32_t it_s = 0, it_u = 0, it_lo_e = 0;
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
             const int rt = u / args.splits, sp = u % args.splits;
             const int ct0 = static_cast<int>((long long)sp * args.n_col_tiles / args.splits);
             const int ct1 = static_cast<int>((long long)(sp + 1) * args.n_col_tiles / args.splits);
-            float acc0[4] = {0.f, 0.f, 0.f, 0.f};
-            float acc1[4] = {0.f, 0.f, 0.f, 0.f};
+            float2 acc2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+            float2 accl2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+            // score: fp64 running sums of the drained O sub-unit accumulators,
+            // kept in shared memory (registers are the epilogue's scarce resource)
+            double* acc = reinterpret_cast<double*>(smem + Cfg::kOffAcc) +
+                          (hf * 128 + r) * Cfg::kAccStride;
+            if constexpr (kScore) {
+#pragma unroll
+                for (int c = 0; c <= kMaxDim; ++c) acc[c] = 0.0;
+            }
+            // O_hi sub-unit accumulators are drained alternately by the two
+            // column halves (sub-unit s by half s & 1 -- which is also its
+            // TMEM buffer), one tile late, with the drain's tcgen05.ld merged
+            // into the next tile's S loads (one wait::ld).
+            int pending = -1;      // O buffer-use index awaiting this half's drain
+            int pending_ct = 0;    // first tile at whose end it may be drained
+            int sub_left_e = 0;    // tiles left in the current O sub-unit
             for (int ct = ct0; ct < ct1; ++ct) {
-                const uint32_t sb = it_s & 1;
-                ptx::mbar_wait(&s_full[sb], (it_s >> 1) & 1);
+                const uint32_t sb = it_s % Cfg::kSBuf;
+                ptx::mbar_wait(&s_full[sb], (it_s / Cfg::kSBuf) & 1);
                 ptx::tc_fence_after();
                 uint32_t v0[32], v1[32];
-                uint32_t hi_w[32], lo_w[32];
                 const uint32_t ta = lane_addr + sb * 128 + hf * 64;
                 ptx::tmem_ld32(ta, v0);
                 ptx::tmem_ld32(ta + 32, v1);
@@ -284,76 +347,123 @@ __global__ void __launch_bounds__(320, 1) pairwise_tc_kernel(PairArgs args) {
                             if (j + 32 == jj) v1[j] = 0xFF800000u;
                         }
                     }
-                    // phi' = phi * 2^15 split into fp16 hi + lo; v0/v1 are reused as
-                    // the packed P_hi / P_lo words (32 each: 64 columns, 2 per word)
+                    // phi' = phi * 2^15 split exactly into fp16 hi + lo: hi keeps
+                    // the top 11 significant bits (mask), lo = phi' - hi (exact),
+                    // both convert to fp16 exactly / to nearest.  (S may exceed 0
+                    // by rounding for coincident points: phi' <= 2^15 (1 + 1e-5),
+                    // well inside fp16, so no clamp.)
+                    const float2 dsc2 = make_float2(dsc, dsc);
+                    const float2 off2 = make_float2(kPScaleF, kPScaleF);
+                    const float2 neg1 = make_float2(-1.f, -1.f);
+                    const uint32_t tp = lane_addr + sb * 128 + hf * 64;
+                    uint32_t hi_w[32], lo_w[32];
 #pragma unroll
                     for (int w = 0; w < 32; ++w) {
                         const uint32_t ra = w < 16 ? v0[2 * w] : v1[2 * w - 32];
                         const uint32_t rb = w < 16 ? v0[2 * w + 1] : v1[2 * w + 1 - 32];
-                        const float p0 = ptx::ex2(fminf(fmaf(__uint_as_float(ra), dsc, kPScaleF), kPScaleF));
-                        const float p1 = ptx::ex2(fminf(fmaf(__uint_as_float(rb), dsc, kPScaleF), kPScaleF));
-                        const __half2 h = __floats2half2_rn(p0, p1);
-                        const float2 hf2 = __half22float2(h);
-                        const __half2 l = __floats2half2_rn(p0 - hf2.x, p1 - hf2.y);
-                        hi_w[w] = *reinterpret_cast<const uint32_t*>(&h);
-                        lo_w[w] = *reinterpret_cast<const uint32_t*>(&l);
+                        const float2 t = ptx::ffma2(make_float2(__uint_as_float(ra), __uint_as_float(rb)),
+                                                    dsc2, off2);
+                        const float2 p = make_float2(ptx::ex2(t.x), ptx::ex2(t.y));
+                        const float2 h = make_float2(__uint_as_float(__float_as_uint(p.x) & 0xFFFFE000u),
+                                                     __uint_as_float(__float_as_uint(p.y) & 0xFFFFE000u));
+                        const float2 l = ptx::ffma2(h, neg1, p);
+                        hi_w[w] = ptx::cvt_f16x2(h.x, h.y);
+                        lo_w[w] = ptx::cvt_f16x2(l.x, l.y);
                     }
-                    const uint32_t tp = lane_addr + sb * 128 + hf * 64;
                     ptx::tmem_st32(tp, hi_w);
                     ptx::tmem_st32(tp + 32, lo_w);
                     ptx::tmem_st_wait();
                     ptx::tc_fence_before();
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(&p_full[sb]);
-                } else {
+                    // drain this half's pending sub-unit two tiles late (its last GEMM2
+                    // has certainly completed, so the wait below never stalls)
+                    if (pending >= 0 && ct >= pending_ct) {
+                        uint32_t od[16], os_;
+                        const uint32_t to = lane_addr + Cfg::kTmemO + (pending & 1) * 32;
+                        ptx::mbar_wait(&o_full[pending & 1], (pending >> 1) & 1);
+                        ptx::tc_fence_after();
+                        ptx::tmem_ld16(to, od);
+                        ptx::tmem_ld1(to + 16, os_);
+                        ptx::tmem_ld_wait();
+                        ptx::tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) ptx::mbar_arrive(&o_empty[pending & 1]);
+                        acc[kMaxDim] += static_cast<double>(__uint_as_float(os_));
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const float d0 = fminf(__uint_as_float(v0[j]) * dsc, 0.f);
-                        const float p0 = ptx::ex2(d0);
-                        acc0[j & 3] += p0;
-                        if constexpr (MODE == kModeLaplace) acc1[j & 3] = fmaf(p0, d0, acc1[j & 3]);
+                        for (int c = 0; c < kMaxDim; ++c) acc[c] += static_cast<double>(__uint_as_float(od[c]));
+                        pending = -1;
                     }
+                    {
+                        if (ct == ct0) sub_left_e = args.flush_tiles;
+                        --sub_left_e;
+                        if (sub_left_e == 0 || ct == ct1 - 1) {
+                            sub_left_e = args.flush_tiles;
+                            if ((it_u & 1) == static_cast<uint32_t>(hf)) {
+                                pending = static_cast<int>(it_u);
+                                pending_ct = ct + 1;
+                            }
+                            ++it_u;
+                        }
+                    }
+                } else {
+                    // (phi <= 1 up to the expansion's rounding: no clamp needed)
+                    const float2 dsc2 = make_float2(dsc, dsc);
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const float d1 = fminf(__uint_as_float(v1[j]) * dsc, 0.f);
-                        const float p1 = ptx::ex2(d1);
-                        acc0[j & 3] += p1;
-                        if constexpr (MODE == kModeLaplace) acc1[j & 3] = fmaf(p1, d1, acc1[j & 3]);
+                    for (int j = 0; j < 64; j += 2) {
+                        const uint32_t ra = j < 32 ? v0[j] : v1[j - 32];
+                        const uint32_t rb = j < 32 ? v0[j + 1] : v1[j + 1 - 32];
+                        const float2 dd = ptx::fmul2(make_float2(__uint_as_float(ra), __uint_as_float(rb)),
+                                                     dsc2);
+                        const float2 p = make_float2(ptx::ex2(dd.x), ptx::ex2(dd.y));
+                        const int a = (j >> 1) & 1;
+                        acc2[a] = ptx::fadd2(acc2[a], p);
+                        if constexpr (MODE == kModeLaplace) accl2[a] = ptx::ffma2(p, dd, accl2[a]);
                     }
                 }
                 ++it_s;
             }
             const size_t row = static_cast<size_t>(rt) * kTileRows + r;
             if constexpr (kScore) {
-                if (hf == 0) {
-                    ptx::mbar_wait(o_full, it_u & 1);
+                if (pending >= 0) {
+                    uint32_t od[16], os_;
+                    const uint32_t to = lane_addr + Cfg::kTmemO + (pending & 1) * 32;
+                    ptx::mbar_wait(&o_full[pending & 1], (pending >> 1) & 1);
                     ptx::tc_fence_after();
-                    uint32_t o0[32], o1[16];
-                    ptx::tmem_ld32(lane_addr + Cfg::kTmemO, o0);
-                    ptx::tmem_ld16(lane_addr + Cfg::kTmemO + 32, o1);
+                    ptx::tmem_ld16(to, od);
+                    ptx::tmem_ld1(to + 16, os_);
                     ptx::tmem_ld_wait();
                     ptx::tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(o_empty);
-                    const size_t idx = static_cast<size_t>(sp) * args.rows_pad + row;
-                    args.part0[idx] = __uint_as_float(o1[0]);
-                    float4* t = reinterpret_cast<float4*>(args.part1 + idx * kMaxDim);
+                    if (lane == 0) ptx::mbar_arrive(&o_empty[pending & 1]);
+                    acc[kMaxDim] += static_cast<double>(__uint_as_float(os_));
 #pragma unroll
-                    for (int w = 0; w < 4; ++w) {
-                        float4 f;
-                        f.x = __uint_as_float(o0[4 * w + 0]) + __uint_as_float(o0[16 + 4 * w + 0]);
-                        f.y = __uint_as_float(o0[4 * w + 1]) + __uint_as_float(o0[16 + 4 * w + 1]);
-                        f.z = __uint_as_float(o0[4 * w + 2]) + __uint_as_float(o0[16 + 4 * w + 2]);
-                        f.w = __uint_as_float(o0[4 * w + 3]) + __uint_as_float(o0[16 + 4 * w + 3]);
-                        t[w] = f;
-                    }
+                    for (int c = 0; c < kMaxDim; ++c) acc[c] += static_cast<double>(__uint_as_float(od[c]));
                 }
-                ++it_u;
+                if (hf == 1) {   // T_lo, accumulated over the whole unit (2^-11 of T_hi)
+                    uint32_t ol[16];
+                    ptx::mbar_wait(lo_full, it_lo_e & 1);
+                    ptx::tc_fence_after();
+                    ptx::tmem_ld16(lane_addr + Cfg::kTmemOlo, ol);
+                    ptx::tmem_ld_wait();
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(lo_empty);
+#pragma unroll
+                    for (int c = 0; c < kMaxDim; ++c) acc[c] += static_cast<double>(__uint_as_float(ol[c]));
+                }
+                ++it_lo_e;
+                // one partial per (split, column half): the halves drained disjoint sub-units
+                const size_t idx = static_cast<size_t>(sp * 2 + hf) * args.rows_pad + row;
+                args.dpart0[idx] = acc[kMaxDim];
+                double2* t = reinterpret_cast<double2*>(args.dpart1 + idx * kMaxDim);
+#pragma unroll
+                for (int w = 0; w < kMaxDim / 2; ++w) t[w] = make_double2(acc[2 * w], acc[2 * w + 1]);
             } else {
                 const size_t idx = static_cast<size_t>(sp * 2 + hf) * args.rows_pad + row;
-                args.part0[idx] = (acc0[0] + acc0[1]) + (acc0[2] + acc0[3]);
+                args.part0[idx] = (acc2[0].x + acc2[0].y) + (acc2[1].x + acc2[1].y);
                 if constexpr (MODE == kModeLaplace)
-                    args.part1[idx] = (acc1[0] + acc1[1]) + (acc1[2] + acc1[3]);
+                    args.part1[idx] = (accl2[0].x + accl2[0].y) + (accl2[1].x + accl2[1].y);
             }
         }
     }

@@ -131,43 +131,49 @@ __global__ void pack_operands(PackArgs a) {
 #pragma unroll
         for (int c = 0; c < kMaxDim; ++c) yh[c] = yl[c] = zero;
     }
+    // chunk layout (see layout.cuh):      A                 B
+    //   0-1  y_hi                          y_hi              y_hi
+    //   2    norms                         a1 a2 a3 1 1 1    1 1 1 b1 b2 b3
+    //   3    zero
+    //   4-5                                y_hi              y_lo
+    //   6-7                                y_lo              y_hi
     uint32_t ch[8][4];
 #pragma unroll
     for (int c = 0; c < 2; ++c)
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
             const int k0 = c * 8 + 2 * w;
-            ch[c][w] = pack_h2(yh[k0], yh[k0 + 1]);                       // chunks 0-1: y_hi
-            ch[2 + c][w] = a.format == 0 ? pack_h2(yh[k0], yh[k0 + 1])    // A: y_hi
-                                         : pack_h2(yl[k0], yl[k0 + 1]);   // B: y_lo
-            ch[6 + c][w] = a.format == 0 ? pack_h2(yl[k0], yl[k0 + 1])    // A: y_lo
-                                         : pack_h2(yh[k0], yh[k0 + 1]);   // B: y_hi
+            ch[c][w] = pack_h2(yh[k0], yh[k0 + 1]);
+            ch[4 + c][w] = a.format == 0 ? pack_h2(yh[k0], yh[k0 + 1])
+                                         : pack_h2(yl[k0], yl[k0 + 1]);
+            ch[6 + c][w] = a.format == 0 ? pack_h2(yl[k0], yl[k0 + 1])
+                                         : pack_h2(yh[k0], yh[k0 + 1]);
         }
     if (valid) {
         if (a.format == 0) {  // a1 a2 a3 1 1 1 0 0
-            ch[4][0] = pack_h2(n1, n2);
-            ch[4][1] = pack_h2(n3, one);
-            ch[4][2] = pack_h2(one, one);
-            ch[4][3] = 0u;
+            ch[2][0] = pack_h2(n1, n2);
+            ch[2][1] = pack_h2(n3, one);
+            ch[2][2] = pack_h2(one, one);
+            ch[2][3] = 0u;
         } else {              // 1 1 1 b1 b2 b3 0 0
-            ch[4][0] = pack_h2(one, one);
-            ch[4][1] = pack_h2(one, n1);
-            ch[4][2] = pack_h2(n2, n3);
-            ch[4][3] = 0u;
+            ch[2][0] = pack_h2(one, one);
+            ch[2][1] = pack_h2(one, n1);
+            ch[2][2] = pack_h2(n2, n3);
+            ch[2][3] = 0u;
         }
     } else {
         if (a.format == 0) {
-            ch[4][0] = ch[4][1] = ch[4][2] = ch[4][3] = 0u;
+            ch[2][0] = ch[2][1] = ch[2][2] = ch[2][3] = 0u;
         } else {  // far-away column: b1 + b2 = -60000 -> phi = 0 exactly
             const __half big = __float2half(-30000.f);
-            ch[4][0] = 0u;
-            ch[4][1] = pack_h2(zero, big);
-            ch[4][2] = pack_h2(big, zero);
-            ch[4][3] = 0u;
+            ch[2][0] = 0u;
+            ch[2][1] = pack_h2(zero, big);
+            ch[2][2] = pack_h2(big, zero);
+            ch[2][3] = 0u;
         }
     }
 #pragma unroll
-    for (int w = 0; w < 4; ++w) ch[5][w] = 0u;
+    for (int w = 0; w < 4; ++w) ch[3][w] = 0u;
     const size_t tile = i / kTileRows;
     const int r = static_cast<int>(i % kTileRows);
     uint4* base = a.out + tile * (kTileBytes / 16) + r * 8;
@@ -182,8 +188,8 @@ __global__ void pack_operands(PackArgs a) {
 // layout).  part_s: [splits][rows_pad]; part_t: [splits][rows_pad][16] with
 // T' = sum_j phi_ij y'_j in scaled, centred coordinates.
 struct FinalizeArgs {
-    const float* part_s;
-    const float* part_t;
+    const double* part_s;
+    const double* part_t;
     int splits;
     size_t rows_pad;
     size_t rows;          // rows in this shard
@@ -209,7 +215,7 @@ __global__ void finalize_score(FinalizeArgs a) {
     // S' and T' exclude the self pair (phi_ii = exp(0) = 1, engine.cpp:43-50
     // snaps r_ii^2 to 0): S = 1 + S', and T - x_i S = T' - x_i S'.
     double Sp = 0.0;
-    for (int s = 0; s < a.splits; ++s) Sp += static_cast<double>(a.part_s[s * a.rows_pad + i]);
+    for (int s = 0; s < a.splits; ++s) Sp += a.part_s[s * a.rows_pad + i];
     Sp = ldexp(Sp, -kPScaleExp);  // the tc/simt score sums carry phi * 2^15
     if (Sp < kScoreFlagMass && a.flag_rows) {  // too little neighbour mass for fp16 P
         a.flag_rows[atomicAdd(a.flag_count, 1u)] = static_cast<unsigned int>(i);
@@ -227,7 +233,7 @@ __global__ void finalize_score(FinalizeArgs a) {
     for (int c = 0; c < a.d; ++c) {
         double Tp = 0.0;
         for (int s = 0; s < a.splits; ++s)
-            Tp += static_cast<double>(a.part_t[(s * a.rows_pad + i) * kMaxDim + c]);
+            Tp += a.part_t[(s * a.rows_pad + i) * kMaxDim + c];
         const double tc = ldexp(Tp, -kPScaleExp) / ys;  // sum_{j != i} phi_ij xc_j
         const double x = a.x[g * a.d + c];
         const double xc = x - a.sc->mu[c];
