@@ -203,11 +203,15 @@ Shard shard_of(size_t n, int world, int rank, size_t align = 1) {
 
 int choose_splits(const Options& o, size_t row_tiles, size_t col_tiles, int ctas) {
     if (o.splits > 0) return static_cast<int>(std::min<size_t>(o.splits, col_tiles));
-    // minimise rounds * (tiles per unit + pipeline fill) over S in [1, min(col_tiles, 64)]
+    // Units run chunk-major, so one column chunk's B tiles are the L2 working
+    // set: keep a chunk <= 32 MiB (2048 tiles) so the operand stream is read
+    // from HBM about once.  Then minimise rounds * (tiles per unit + pipeline
+    // fill) over S in [s_min, min(col_tiles, 64)].
+    const size_t s_min = std::min<size_t>(col_tiles, (col_tiles + 2047) / 2048);
     double best = 1e300;
-    int best_s = 1;
-    const size_t smax = std::min<size_t>(col_tiles, 64);
-    for (size_t s = 1; s <= smax; ++s) {
+    int best_s = static_cast<int>(std::max<size_t>(s_min, 1));
+    const size_t smax = std::max<size_t>(std::min<size_t>(col_tiles, 64), s_min);
+    for (size_t s = std::max<size_t>(s_min, 1); s <= smax; ++s) {
         const size_t units = row_tiles * s;
         const size_t rounds = (units + ctas - 1) / ctas;
         const double per_unit = static_cast<double>((col_tiles + s - 1) / s) + 2.0;
@@ -379,9 +383,9 @@ Status score_program(Device& D, const Options& o, const Job& J, const double* dX
     const size_t rt = rows_pad / kTileRows, ct = cols_pad / kTileRows;
     const int ctas = o.max_ctas > 0 ? std::min(o.max_ctas, D.num_sms) : D.num_sms;
     const int splits = o.engine == FKDE_ENGINE_SIMT ? 1 : choose_splits(o, rt, ct, ctas);
-    // fp64 partials per (split, column half)
-    STATUS_TRY(ensure(D.part0, 2 * static_cast<size_t>(splits) * rows_pad * sizeof(double)));
-    STATUS_TRY(ensure(D.part1, 2 * static_cast<size_t>(splits) * rows_pad * kMaxDim * sizeof(double)));
+    // fp64 partials per split
+    STATUS_TRY(ensure(D.part0, static_cast<size_t>(splits) * rows_pad * sizeof(double)));
+    STATUS_TRY(ensure(D.part1, static_cast<size_t>(splits) * rows_pad * kMaxDim * sizeof(double)));
     PairArgs a{};
     a.opA = D.opA.as<uint8_t>();
     a.opB = D.opB.as<uint8_t>();
@@ -401,7 +405,7 @@ Status score_program(Device& D, const Options& o, const Job& J, const double* dX
     FinalizeArgs f{};
     f.part_s = D.part0.as<double>();
     f.part_t = D.part1.as<double>();
-    f.splits = 2 * splits;
+    f.splits = splits;
     f.rows_pad = rows_pad;
     f.rows = sh.rows;
     f.row0 = sh.begin;

@@ -74,11 +74,7 @@ __global__ void __launch_bounds__(128) pairwise_simt_kernel(PairArgs args, size_
     }
     if constexpr (MODE == kModeScore) {
         args.dpart0[row] = s0;
-        args.dpart0[args.rows_pad + row] = 0.0;  // second column half (tc layout) is empty
-        for (int k = 0; k < 16; ++k) {
-            args.dpart1[row * kMaxDim + k] = t[k];
-            args.dpart1[(args.rows_pad + row) * kMaxDim + k] = 0.0;
-        }
+        for (int k = 0; k < 16; ++k) args.dpart1[row * kMaxDim + k] = t[k];
     } else {
         args.part0[row] = s0;
         args.part0[args.rows_pad + row] = 0.f;  // second column half (tc layout) is empty

@@ -52,8 +52,8 @@ struct PairArgs {
     const PassScalars* sc;
     float* part0;         // KDE: [splits*2][rows_pad]
     float* part1;         // Laplace: [splits*2][rows_pad]
-    double* dpart0;       // SCORE: S' [splits*2][rows_pad]   (fp64, per column half)
-    double* dpart1;       // SCORE: T' [splits*2][rows_pad][16] (fp64)
+    double* dpart0;       // SCORE: S' [splits][rows_pad]   (fp64)
+    double* dpart1;       // SCORE: T' [splits][rows_pad][16] (fp64)
     int flush_tiles;      // SCORE: O is drained to fp64 registers every this many tiles
     size_t rows_pad;
     // SCORE: column tile holding row tile 0's diagonal (rows and columns are
@@ -156,7 +156,9 @@ __global__ void __launch_bounds__(320, 1) pairwise_tc_kernel(PairArgs args) {
         const uint64_t pol_b = ptx::policy_evict_last();
         uint32_t it_a = 0, it_b = 0;
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-            const int rt = u / args.splits, sp = u % args.splits;
+            // chunk-major unit order: CTAs running concurrently share one column
+            // chunk, which therefore stays L2-resident while they stream it
+            const int sp = u / args.n_row_tiles, rt = u % args.n_row_tiles;
             const int ct0 = static_cast<int>((long long)sp * args.n_col_tiles / args.splits);
             const int ct1 = static_cast<int>((long long)(sp + 1) * args.n_col_tiles / args.splits);
             const int ab = it_a & 1;
@@ -244,7 +246,7 @@ __global__ void __launch_bounds__(320, 1) pairwise_tc_kernel(PairArgs args) {
             if (idx == ntiles - 1) ++it_lo;
         };
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-            const int sp = u % args.splits;
+            const int sp = u / args.n_row_tiles;
             const int ct0 = static_cast<int>((long long)sp * args.n_col_tiles / args.splits);
             const int ct1 = static_cast<int>((long long)(sp + 1) * args.n_col_tiles / args.splits);
             const int ab = it_a & 1;
@@ -304,7 +306,7 @@ __global__ void __launch_bounds__(320, 1) pairwise_tc_kernel(PairArgs args) {
         const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
         uint32_t it_s = 0, it_u = 0, it_lo_e = 0;
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-            const int rt = u / args.splits, sp = u % args.splits;
+            const int sp = u / args.n_row_tiles, rt = u % args.n_row_tiles;
             const int ct0 = static_cast<int>((long long)sp * args.n_col_tiles / args.splits);
             const int ct1 = static_cast<int>((long long)(sp + 1) * args.n_col_tiles / args.splits);
             float2 acc2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
@@ -453,12 +455,20 @@ __global__ void __launch_bounds__(320, 1) pairwise_tc_kernel(PairArgs args) {
                     for (int c = 0; c < kMaxDim; ++c) acc[c] += static_cast<double>(__uint_as_float(ol[c]));
                 }
                 ++it_lo_e;
-                // one partial per (split, column half): the halves drained disjoint sub-units
-                const size_t idx = static_cast<size_t>(sp * 2 + hf) * args.rows_pad + row;
-                args.dpart0[idx] = acc[kMaxDim];
-                double2* t = reinterpret_cast<double2*>(args.dpart1 + idx * kMaxDim);
+                // the two halves drained disjoint sub-units: merge them through
+                // shared memory (named barrier over the 8 epilogue warps) and
+                // write one fp64 partial per (split, row)
+                asm volatile("bar.sync 1, 256;" ::: "memory");
+                if (hf == 0) {
+                    const double* other = acc + 128 * Cfg::kAccStride;
+                    const size_t idx = static_cast<size_t>(sp) * args.rows_pad + row;
+                    args.dpart0[idx] = acc[kMaxDim] + other[kMaxDim];
+                    double2* t = reinterpret_cast<double2*>(args.dpart1 + idx * kMaxDim);
 #pragma unroll
-                for (int w = 0; w < kMaxDim / 2; ++w) t[w] = make_double2(acc[2 * w], acc[2 * w + 1]);
+                    for (int w = 0; w < kMaxDim / 2; ++w)
+                        t[w] = make_double2(acc[2 * w] + other[2 * w], acc[2 * w + 1] + other[2 * w + 1]);
+                }
+                asm volatile("bar.sync 1, 256;" ::: "memory");   // acc is re-zeroed next unit
             } else {
                 const size_t idx = static_cast<size_t>(sp * 2 + hf) * args.rows_pad + row;
                 args.part0[idx] = (acc2[0].x + acc2[0].y) + (acc2[1].x + acc2[1].y);

@@ -1,15 +1,21 @@
 #!/bin/bash
 # Runs on the GPU box (under gpurun).  Produces, in gpurun_out/:
-#   launches.csv   every kernel launch of a short bench run with its device time
-#   prof_score.ncu-rep / prof_kde.ncu-rep   ncu --set full of the two hot kernels
+#   launches.csv            every kernel launch of a short bench run with its device time
+#   prof_1m.ncu-rep         ncu --set full of the score-pass and density-pass kernels
+#                           at the headline size (n = 2^20, m = 2^17)
+#   prof_32k.ncu-rep        the same at n = m = 32768
 set -u
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
-    --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline \
+    --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline \
     > gpurun_out/launches_bench.log 2>&1
 echo "launch list rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on \
-    -k regex:pairwise_tc_kernel -s 2 -c 2 -o gpurun_out/prof_tc -f \
-    python tools/perf_probe.py sd32k > gpurun_out/prof_tc.log 2>&1
-echo "ncu full rc=$?"
+    -k regex:pairwise_tc_kernel -s 0 -c 2 -o gpurun_out/prof_1m -f \
+    python tools/perf_probe.py sd1m > gpurun_out/prof_1m.log 2>&1
+echo "ncu 1m rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on \
+    -k regex:pairwise_tc_kernel -s 2 -c 2 -o gpurun_out/prof_32k -f \
+    python tools/perf_probe.py sd32k > gpurun_out/prof_32k.log 2>&1
+echo "ncu 32k rc=$?"
