@@ -153,6 +153,7 @@ struct Options {
     int timing = 0;
     int max_ctas = 0;
     int flush_tiles = 2;
+    long long* trace = nullptr;   // debug: device buffer for pairwise_tc_kernel's clock trace
 };
 
 struct Device {
@@ -398,6 +399,7 @@ Status score_program(Device& D, const Options& o, const Job& J, const double* dX
     a.flush_tiles = std::max(1, o.flush_tiles);
     a.rows_pad = rows_pad;
     a.diag_tile0 = static_cast<int>(sh.begin / kTileRows);
+    a.trace = o.trace;
     STATUS_TRY(launch_pairwise<kModeScore>(D, o, a, n));
     record(D, o, FKDE_T_FINALIZE);
 
@@ -878,6 +880,9 @@ int fkde_gpu_set_option(fkde_gpu_ctx* ctx, int key, int64_t value) {
         case FKDE_OPT_MAX_CTAS:
             if (value < 0) return FKDE_INVALID_ARGUMENT;
             ctx->opt.max_ctas = static_cast<int>(value);
+            return FKDE_OK;
+        case FKDE_OPT_TRACE_PTR:
+            ctx->opt.trace = reinterpret_cast<long long*>(value);
             return FKDE_OK;
         case FKDE_OPT_FLUSH_TILES:
             if (value < 1 || value > 1 << 20) return FKDE_INVALID_ARGUMENT;

@@ -61,13 +61,25 @@ struct PairArgs {
     // phi_ii = 1 is excluded from the tensor-core sums and added back exactly
     // in finalize_score, so that T - x S never cancels against the self term.
     int diag_tile0;       // -1: no diagonal
+    // debug: per-event clock64 trace of block 0 (nullptr = off).  Layout
+    // [role(0..9 warp)][event slot][tile] -> long long
+    long long* trace;
 };
+#define FKDE_TRACE(slot, tile)                                                               \
+    do {                                                                                     \
+        if (args.trace && blockIdx.x == 0 && lane == 0 && (tile) < 256)                      \
+            args.trace[(warp * 8 + (slot)) * 256 + (tile)] = clock64();                      \
+    } while (0)
 
 template <int MODE>
 struct TcConfig {
     static constexpr bool kScore = MODE == kModeScore;
     static constexpr int kStages = 8;
-    static constexpr int kThreads = 320;
+    // warps: 0 producer, 1 GEMM1 issuer (+ TMEM owner), 2..9 epilogue,
+    // 10 GEMM2 issuer (score only).  tcgen05.mma issue blocks while the
+    // tensor core is busy, so GEMM1 and GEMM2 get their own issuing warps and
+    // the tensor core never idles behind a GEMM2 that waits for P.
+    static constexpr int kThreads = kScore ? 352 : 320;
     static constexpr uint32_t kOffA = 0;
     static constexpr uint32_t kOffB = 2 * kTileBytes;
     // score: fp64 drain accumulators, [2 halves][128 rows][kAccStride] doubles
@@ -80,16 +92,15 @@ struct TcConfig {
     // KDE: 4.
     static constexpr int kSBuf = kScore ? 3 : 4;
     static constexpr int kLag = kSBuf - 1;   // score: GEMM2(t) issued after GEMM1(t + kLag)
-    static constexpr uint32_t kNumBars = 4 + 2 * kStages + 4 * 4 + 4 + 2;
+    static constexpr uint32_t kNumBars = 4 + 2 * kStages + 4 * 4 + 4;
     static constexpr uint32_t kSmemBytes = kOffBar + kNumBars * 8 + 16 + 1024;  // + align slack
     static constexpr uint32_t kTmemCols = 512;
-    static constexpr uint32_t kTmemO = 384;   // score: O_hi[2] (2 x 32 cols: T_hi, S)
-    static constexpr uint32_t kTmemOlo = 448; // score: O_lo (16 cols: T_lo), per unit
+    static constexpr uint32_t kTmemO = 384;   // score: O[2] (2 x 64 cols: T_hi, S, T_lo)
     static constexpr uint32_t kN2 = 48;       // GEMM2 N
 };
 
 template <int MODE>
-__global__ void __launch_bounds__(320, 1) pairwise_tc_kernel(PairArgs args) {
+__global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kernel(PairArgs args) {
     using Cfg = TcConfig<MODE>;
     constexpr bool kScore = Cfg::kScore;
     constexpr int kStages = Cfg::kStages;
@@ -107,12 +118,10 @@ __global__ void __launch_bounds__(320, 1) pairwise_tc_kernel(PairArgs args) {
     uint64_t* s_full = b_empty + kStages; // [4]
     uint64_t* s_empty = s_full + 4;       // [4]
     uint64_t* p_full = s_empty + 4;       // [4]
-    uint64_t* p_empty = p_full + 4;       // [4] (unused: P lives in TMEM)
-    uint64_t* o_full = p_empty + 4;       // [2]
+    uint64_t* s_free = p_full + 4;        // [4] score: GEMM2 done reading P (S buffer reusable)
+    uint64_t* o_full = s_free + 4;        // [2]
     uint64_t* o_empty = o_full + 2;       // [2]
-    uint64_t* lo_full = o_empty + 2;      // [1]
-    uint64_t* lo_empty = lo_full + 1;     // [1]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lo_empty + 1);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -126,7 +135,7 @@ __global__ void __launch_bounds__(320, 1) pairwise_tc_kernel(PairArgs args) {
             ptx::mbar_init(&s_full[i], 1);
             ptx::mbar_init(&s_empty[i], 8);
             ptx::mbar_init(&p_full[i], 8);
-            ptx::mbar_init(&p_empty[i], 1);
+            ptx::mbar_init(&s_free[i], 1);
         }
         for (int i = 0; i < kStages; ++i) {
             ptx::mbar_init(&b_full[i], 1);
@@ -136,8 +145,7 @@ __global__ void __launch_bounds__(320, 1) pairwise_tc_kernel(PairArgs args) {
             ptx::mbar_init(&o_full[i], 1);
             ptx::mbar_init(&o_empty[i], 4);
         }
-        ptx::mbar_init(lo_full, 1);
-        ptx::mbar_init(lo_empty, 4);
+
 
         ptx::fence_barrier_init();
     }
@@ -182,120 +190,112 @@ __global__ void __launch_bounds__(320, 1) pairwise_tc_kernel(PairArgs args) {
                 ++it_b;
             }
         }
-    } else if (warp == 1) {
-        // ===================== MMA issuer =====================
+    } else if (warp == 1 || (kScore && warp == 10)) {
+        // ===================== MMA issuers =====================
         // Whole warp in the loop, one elected lane issues every tcgen05 op
         // (commits must come from the issuing thread; elect.sync on a
         // converged warp always picks the same lane).  Descriptors are built
         // once and advanced by adding (byte offset >> 4) to the start-address
         // field, so each MMA costs a uniform add + the instruction.
         constexpr uint32_t idesc1 = ptx::idesc_f16_f32(128, 128, false, false);
-        constexpr uint32_t idesc2h = ptx::idesc_f16_f32(128, 32, false, true);  // T_hi, S
-        constexpr uint32_t idesc2l = ptx::idesc_f16_f32(128, 16, false, true);  // T_lo
-        uint32_t it_lo = 0;  // units whose O_lo GEMM2 chain has started
+        constexpr uint32_t idesc2 = ptx::idesc_f16_f32(128, Cfg::kN2, false, true);
         const uint64_t descA = ptx::smem_desc_sw128(ptx::smem_u32(smA), 16, 1024);
         const uint64_t descB = ptx::smem_desc_sw128(ptx::smem_u32(smB), 16, 1024);
         const uint64_t descBmn = ptx::smem_desc_sw128(ptx::smem_u32(smB), kTileBytes, 1024);
         uint32_t it_a = 0, it_b = 0, it_s = 0, it_u = 0;
-        // GEMM2 of a finished tile: O += P_hi.B + P_lo.B, P read from TMEM.
-        // Warp-group hf of the epilogue stored, in S buffer sb's columns
-        // [hf*64, hf*64+64): P_hi (packed fp16 pairs) for K = hf*64..+63 in
-        // the first 32 columns, P_lo in the next 32.
-        // O is accumulated in TMEM over `flush_tiles` column tiles (a
-        // "sub-unit"), then drained by the epilogue into fp64 registers; two O
-        // buffers alternate so the drain overlaps the next sub-unit.  This
+        const bool g1 = warp == 1;
+        // GEMM2 (warp 10): O += P_hi.B + P_lo.B, P read from TMEM.  Epilogue
+        // warp-group hf stored, in S buffer sb's columns [hf*64, hf*64+64):
+        // P_hi (packed fp16 pairs) for K = hf*64..+63 in the first 32 columns,
+        // P_lo in the next 32.  O is accumulated in TMEM over `flush_tiles`
+        // column tiles (a "sub-unit"), then drained by the epilogue into fp64;
+        // two O buffers alternate so the drain overlaps the next sub-unit.  This
         // bounds the tensor core's fp32 accumulation length (its truncation
         // error grows with the accumulator magnitude x the number of steps).
         const int F = args.flush_tiles;
-        int sub_left = 0;   // tiles left in the current O sub-unit (no integer modulo)
-        auto gemm2 = [&](uint32_t st, uint32_t sb, uint32_t its, int idx, int ntiles) {
-            if (idx == 0) sub_left = F;
-            const bool first = sub_left == F;
-            --sub_left;
-            const bool last = sub_left == 0 || idx == ntiles - 1;
-            if (last) sub_left = F;
-            const uint32_t ob = it_u & 1;
-            ptx::mbar_wait(&p_full[sb], (its / Cfg::kSBuf) & 1);
-            if (first) ptx::mbar_wait(&o_empty[ob], ((it_u >> 1) & 1) ^ 1);
-            if (idx == 0) ptx::mbar_wait(lo_empty, (it_lo & 1) ^ 1);
-            ptx::tc_fence_after();
-            if (ptx::elect_one()) {
-                const uint64_t db0 = descBmn + ((st * kTileBytes) >> 4);
-                const uint32_t ta0 = tmem_base + sb * 128;
-                const uint32_t toh = tmem_base + Cfg::kTmemO + ob * 32;
-                const uint32_t tol = tmem_base + Cfg::kTmemOlo;
-#pragma unroll
-                for (int part = 0; part < 2; ++part) {
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        const uint32_t ta = ta0 + (k >> 2) * 64 + part * 32 + (k & 3) * 8;
-                        const uint64_t db = db0 + ((k * 2048) >> 4);
-                        // B columns 0-31 (y_hi, ones) -> O_hi (drained every F tiles);
-                        // columns 32-47 (y_lo, 2^-11 smaller) -> O_lo (once per unit)
-                        ptx::umma_f16_ts(toh, ta, db, idesc2h, (first && part == 0 && k == 0) ? 0u : 1u);
-                        ptx::umma_f16_ts(tol, ta, db + (64 >> 4), idesc2l,
-                                         (idx == 0 && part == 0 && k == 0) ? 0u : 1u);
-                    }
-                }
-                ptx::umma_commit(&b_empty[st]);
-                if (last) ptx::umma_commit(&o_full[ob]);
-                if (idx == ntiles - 1) ptx::umma_commit(lo_full);
-            }
-            __syncwarp();
-            if (last) ++it_u;
-            if (idx == ntiles - 1) ++it_lo;
-        };
+        int sub_left = 0;
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
             const int sp = u / args.n_row_tiles;
             const int ct0 = static_cast<int>((long long)sp * args.n_col_tiles / args.splits);
             const int ct1 = static_cast<int>((long long)(sp + 1) * args.n_col_tiles / args.splits);
             const int ab = it_a & 1;
-            ptx::mbar_wait(&a_full[ab], (it_a >> 1) & 1);
-            ptx::tc_fence_after();
+            if (g1) {
+                ptx::mbar_wait(&a_full[ab], (it_a >> 1) & 1);
+                ptx::tc_fence_after();
+            }
             for (int ct = ct0; ct < ct1; ++ct) {
                 const uint32_t st = it_b % kStages;
                 const uint32_t sb = it_s % Cfg::kSBuf;
-                ptx::mbar_wait(&b_full[st], (it_b / kStages) & 1);
-                // KDE: the epilogue frees S after loading it.  SCORE: S/P of tile
-                // it_s - kSBuf was consumed by its GEMM2, issued (in order) earlier.
-                if constexpr (!kScore) ptx::mbar_wait(&s_empty[sb], ((it_s / Cfg::kSBuf) & 1) ^ 1);
-                ptx::tc_fence_after();
-                if (ptx::elect_one()) {
-                    const uint64_t da0 = descA + ((ab * kTileBytes) >> 4);
-                    const uint64_t db0 = descB + ((st * kTileBytes) >> 4);
-                    // K-step order: the half-norm chunk first, then y_hi.y_hi, so the
-                    // large terms cancel inside one fused MMA step before the small
-                    // hi/lo cross terms are added.
+                const uint32_t ph = (it_s / Cfg::kSBuf) & 1;
+                if (g1) {
+                    FKDE_TRACE(0, it_s);
+                    ptx::mbar_wait(&b_full[st], (it_b / kStages) & 1);
+                    FKDE_TRACE(1, it_s);
+                    // KDE: the epilogue frees S after loading it.  SCORE: GEMM2 of
+                    // the tile that last used this buffer has finished reading P.
+                    if constexpr (!kScore) ptx::mbar_wait(&s_empty[sb], ph ^ 1);
+                    else ptx::mbar_wait(&s_free[sb], ph ^ 1);
+                    ptx::tc_fence_after();
+                    if (ptx::elect_one()) {
+                        const uint64_t da0 = descA + ((ab * kTileBytes) >> 4);
+                        const uint64_t db0 = descB + ((st * kTileBytes) >> 4);
+                        // K-step order: the half-norm chunk first, then y_hi.y_hi, so the
+                        // large terms cancel inside one fused MMA step before the small
+                        // hi/lo cross terms are added.
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) {
-                        const int k = kk == 0 ? 1 : (kk == 1 ? 0 : kk);  // 1 (norms), 0, 2, 3
-                        ptx::umma_f16(tmem_base + sb * 128, da0 + ((k * 32) >> 4),
-                                      db0 + ((k * 32) >> 4), idesc1, kk > 0 ? 1u : 0u);
+                        for (int kk = 0; kk < 4; ++kk) {
+                            const int k = kk == 0 ? 1 : (kk == 1 ? 0 : kk);  // 1 (norms), 0, 2, 3
+                            ptx::umma_f16(tmem_base + sb * 128, da0 + ((k * 32) >> 4),
+                                          db0 + ((k * 32) >> 4), idesc1, kk > 0 ? 1u : 0u);
+                        }
+                        ptx::umma_commit(&s_full[sb]);
+                        if constexpr (!kScore) ptx::umma_commit(&b_empty[st]);
                     }
-                    ptx::umma_commit(&s_full[sb]);
-                    if constexpr (!kScore) ptx::umma_commit(&b_empty[st]);
-                }
-                __syncwarp();
-                if constexpr (kScore) {
-                    if (ct - Cfg::kLag >= ct0) {
-                        const uint32_t b_ = it_b - Cfg::kLag, s_ = it_s - Cfg::kLag;
-                        gemm2(b_ % kStages, s_ % Cfg::kSBuf, s_, ct - Cfg::kLag - ct0, ct1 - ct0);
+                    __syncwarp();
+                    FKDE_TRACE(4, it_s);
+                } else if constexpr (kScore) {
+                    const int idx = ct - ct0;
+                    if (idx == 0) sub_left = F;
+                    const bool first = sub_left == F;
+                    --sub_left;
+                    const bool last = sub_left == 0 || ct == ct1 - 1;
+                    if (last) sub_left = F;
+                    const uint32_t ob = it_u & 1;
+                    FKDE_TRACE(2, it_s);
+                    ptx::mbar_wait(&p_full[sb], ph);
+                    FKDE_TRACE(3, it_s);
+                    if (first) ptx::mbar_wait(&o_empty[ob], ((it_u >> 1) & 1) ^ 1);
+                    ptx::tc_fence_after();
+                    if (ptx::elect_one()) {
+                        const uint64_t db0 = descBmn + ((st * kTileBytes) >> 4);
+                        const uint32_t ta0 = tmem_base + sb * 128;
+                        const uint32_t to = tmem_base + Cfg::kTmemO + ob * 64;
+#pragma unroll
+                        for (int part = 0; part < 2; ++part) {
+#pragma unroll
+                            for (int k = 0; k < 8; ++k) {
+                                // one N=48 MMA per K step: columns 0-15 T_hi, 16 S, 32-47 T_lo
+                                ptx::umma_f16_ts(to, ta0 + (k >> 2) * 64 + part * 32 + (k & 3) * 8,
+                                                 db0 + ((k * 2048) >> 4), idesc2,
+                                                 (first && part == 0 && k == 0) ? 0u : 1u);
+                            }
+                        }
+                        ptx::umma_commit(&b_empty[st]);
+                        ptx::umma_commit(&s_free[sb]);
+                        if (last) ptx::umma_commit(&o_full[ob]);
                     }
+                    __syncwarp();
+                    FKDE_TRACE(5, it_s);
+                    if (last) ++it_u;
                 }
                 ++it_b;
                 ++it_s;
             }
-            if (ptx::elect_one()) ptx::umma_commit(&a_empty[ab]);
-            __syncwarp();
-            ++it_a;
-            if constexpr (kScore) {
-                // the last kLag tiles' GEMM2s
-                for (int t = ct1 - Cfg::kLag > ct0 ? ct1 - Cfg::kLag : ct0; t < ct1; ++t) {
-                    const uint32_t back = static_cast<uint32_t>(ct1 - t);
-                    const uint32_t b_ = it_b - back, s_ = it_s - back;
-                    gemm2(b_ % kStages, s_ % Cfg::kSBuf, s_, t - ct0, ct1 - ct0);
-                }
+            if (g1) {
+                if (ptx::elect_one()) ptx::umma_commit(&a_empty[ab]);
+                __syncwarp();
             }
+            ++it_a;
         }
     } else {
         // ===================== epilogue warps =====================
@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(320, 1) pairwise_tc_kernel(PairArgs args) {
         const int r = q * 32 + lane;        // row within the 128-row tile
         const float dsc = args.sc->dscale;
         const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
-        uint32_t it_s = 0, it_u = 0, it_lo_e = 0;
+        uint32_t it_s = 0, it_u = 0;
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
             const int sp = u / args.n_row_tiles, rt = u % args.n_row_tiles;
             const int ct0 = static_cast<int>((long long)sp * args.n_col_tiles / args.splits);
@@ -328,7 +328,9 @@ __global__ void __launch_bounds__(320, 1) pairwise_tc_kernel(PairArgs args) {
             int sub_left_e = 0;    // tiles left in the current O sub-unit
             for (int ct = ct0; ct < ct1; ++ct) {
                 const uint32_t sb = it_s % Cfg::kSBuf;
+                FKDE_TRACE(0, it_s);
                 ptx::mbar_wait(&s_full[sb], (it_s / Cfg::kSBuf) & 1);
+                FKDE_TRACE(1, it_s);
                 ptx::tc_fence_after();
                 uint32_t v0[32], v1[32];
                 const uint32_t ta = lane_addr + sb * 128 + hf * 64;
@@ -378,23 +380,27 @@ __global__ void __launch_bounds__(320, 1) pairwise_tc_kernel(PairArgs args) {
                     ptx::tc_fence_before();
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(&p_full[sb]);
+                    FKDE_TRACE(2, it_s);
                     // drain this half's pending sub-unit two tiles late (its last GEMM2
                     // has certainly completed, so the wait below never stalls)
                     if (pending >= 0 && ct >= pending_ct) {
-                        uint32_t od[16], os_;
-                        const uint32_t to = lane_addr + Cfg::kTmemO + (pending & 1) * 32;
+                        uint32_t od[16], ol[16], os_;
+                        const uint32_t to = lane_addr + Cfg::kTmemO + (pending & 1) * 64;
                         ptx::mbar_wait(&o_full[pending & 1], (pending >> 1) & 1);
                         ptx::tc_fence_after();
                         ptx::tmem_ld16(to, od);
                         ptx::tmem_ld1(to + 16, os_);
+                        ptx::tmem_ld16(to + 32, ol);
                         ptx::tmem_ld_wait();
                         ptx::tc_fence_before();
                         __syncwarp();
                         if (lane == 0) ptx::mbar_arrive(&o_empty[pending & 1]);
                         acc[kMaxDim] += static_cast<double>(__uint_as_float(os_));
 #pragma unroll
-                        for (int c = 0; c < kMaxDim; ++c) acc[c] += static_cast<double>(__uint_as_float(od[c]));
+                        for (int c = 0; c < kMaxDim; ++c)
+                            acc[c] += static_cast<double>(__uint_as_float(od[c]) + __uint_as_float(ol[c]));
                         pending = -1;
+                        FKDE_TRACE(3, it_s);
                     }
                     {
                         if (ct == ct0) sub_left_e = args.flush_tiles;
@@ -403,7 +409,7 @@ __global__ void __launch_bounds__(320, 1) pairwise_tc_kernel(PairArgs args) {
                             sub_left_e = args.flush_tiles;
                             if ((it_u & 1) == static_cast<uint32_t>(hf)) {
                                 pending = static_cast<int>(it_u);
-                                pending_ct = ct + 1;
+                                pending_ct = ct + 2;
                             }
                             ++it_u;
                         }
@@ -428,33 +434,22 @@ __global__ void __launch_bounds__(320, 1) pairwise_tc_kernel(PairArgs args) {
             const size_t row = static_cast<size_t>(rt) * kTileRows + r;
             if constexpr (kScore) {
                 if (pending >= 0) {
-                    uint32_t od[16], os_;
-                    const uint32_t to = lane_addr + Cfg::kTmemO + (pending & 1) * 32;
+                    uint32_t od[16], ol[16], os_;
+                    const uint32_t to = lane_addr + Cfg::kTmemO + (pending & 1) * 64;
                     ptx::mbar_wait(&o_full[pending & 1], (pending >> 1) & 1);
                     ptx::tc_fence_after();
                     ptx::tmem_ld16(to, od);
                     ptx::tmem_ld1(to + 16, os_);
+                    ptx::tmem_ld16(to + 32, ol);
                     ptx::tmem_ld_wait();
                     ptx::tc_fence_before();
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(&o_empty[pending & 1]);
                     acc[kMaxDim] += static_cast<double>(__uint_as_float(os_));
 #pragma unroll
-                    for (int c = 0; c < kMaxDim; ++c) acc[c] += static_cast<double>(__uint_as_float(od[c]));
+                    for (int c = 0; c < kMaxDim; ++c)
+                        acc[c] += static_cast<double>(__uint_as_float(od[c]) + __uint_as_float(ol[c]));
                 }
-                if (hf == 1) {   // T_lo, accumulated over the whole unit (2^-11 of T_hi)
-                    uint32_t ol[16];
-                    ptx::mbar_wait(lo_full, it_lo_e & 1);
-                    ptx::tc_fence_after();
-                    ptx::tmem_ld16(lane_addr + Cfg::kTmemOlo, ol);
-                    ptx::tmem_ld_wait();
-                    ptx::tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(lo_empty);
-#pragma unroll
-                    for (int c = 0; c < kMaxDim; ++c) acc[c] += static_cast<double>(__uint_as_float(ol[c]));
-                }
-                ++it_lo_e;
                 // the two halves drained disjoint sub-units: merge them through
                 // shared memory (named barrier over the 8 epilogue warps) and
                 // write one fp64 partial per (split, row)
