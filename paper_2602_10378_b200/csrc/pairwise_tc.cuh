@@ -337,6 +337,7 @@ __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kerne
                 ptx::tmem_ld32(ta, v0);
                 ptx::tmem_ld32(ta + 32, v1);
                 ptx::tmem_ld_wait();
+                FKDE_TRACE(6, it_s);
                 if constexpr (!kScore) {
                     ptx::tc_fence_before();
                     __syncwarp();
@@ -376,6 +377,7 @@ __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kerne
                     }
                     ptx::tmem_st32(tp, hi_w);
                     ptx::tmem_st32(tp + 32, lo_w);
+                    FKDE_TRACE(7, it_s);
                     ptx::tmem_st_wait();
                     ptx::tc_fence_before();
                     __syncwarp();

@@ -29,6 +29,11 @@ def main():
     per = np.diff(t[2, 0, lo:hi + 1])
     print(f"  epilogue tile period (warp 2): mean {per.mean():.0f}  min {per.min():.0f}  max {per.max():.0f}")
     for w in range(2, 10):
+        ldl = t[w, 6, lo:hi] - t[w, 1, lo:hi]
+        cmp_ = t[w, 7, lo:hi] - t[w, 6, lo:hi]
+        stl = t[w, 2, lo:hi] - t[w, 7, lo:hi]
+        print(f"  warp {w}: LDTM latency {ldl.mean():5.0f}  compute {cmp_.mean():5.0f}  STTM wait+arrive {stl.mean():5.0f}")
+    for w in range(2, 10):
         s_wait = t[w, 1, lo:hi] - t[w, 0, lo:hi]
         comp = t[w, 2, lo:hi] - t[w, 1, lo:hi]
         d = t[w, 3, lo:hi] - t[w, 2, lo:hi]
