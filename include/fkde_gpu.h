@@ -68,8 +68,9 @@ enum {
     FKDE_OPT_SPLITS = 2,      /* 0 = auto; >0 forces column splits per row tile  */
     FKDE_OPT_TIMING = 3,      /* 1 = record per-phase CUDA-event times            */
     FKDE_OPT_MAX_CTAS = 4,    /* 0 = all SMs; >0 caps the persistent grid        */
-    FKDE_OPT_FLUSH_TILES = 5, /* score pass: drain the TMEM accumulator to fp64
-                                 registers every k column tiles (default 2)    */
+    FKDE_OPT_FLUSH_TILES = 5, /* score pass: drain the TMEM accumulator to the
+                                 extended-precision register sums every k column
+                                 tiles; k a power of two in [1, 2^20] (default 2) */
     FKDE_OPT_TRACE_PTR = 6    /* debug: device pointer (11*8*256 int64) receiving
                                  clock64 stamps of the score kernel's block 0   */
 };

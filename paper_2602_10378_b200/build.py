@@ -42,19 +42,26 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps if os.path.exists(p))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str = OUT, defines=()) -> str:
+    """Build the library (``out``; extra ``-D`` ``defines`` for tool variants,
+    e.g. ``FKDE_ENABLE_TRACE`` for the clock64 trace build used by tools/)."""
+    if out == OUT and not defines and not force and not _stale():
         return OUT
     cmd = [nvcc()] + NVCC_FLAGS + (["-Xptxas", "-v"] if verbose else []) + \
-        ["-o", OUT] + [os.path.join(CSRC, s) for s in SOURCES] + ["-ldl"]
+        ["-D" + d for d in defines] + \
+        ["-o", out] + [os.path.join(CSRC, s) for s in SOURCES] + ["-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed building libfkde_b200.so")
     if verbose:
         sys.stderr.write(r.stderr)
-    return OUT
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    if "--trace" in sys.argv:   # python -m paper_2602_10378_b200.build --trace ab/lib_trace.so
+        print(build(out=os.path.abspath(sys.argv[sys.argv.index("--trace") + 1]),
+                    defines=["FKDE_ENABLE_TRACE"]))
+    else:
+        print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

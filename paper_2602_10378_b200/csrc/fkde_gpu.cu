@@ -309,7 +309,7 @@ Status density_pass(Device& D, const Options& o, int mode, size_t rows_pad, size
     a.sc = sc;
     a.part0 = D.part0.as<float>();
     a.part1 = mode == kModeLaplace ? D.part1.as<float>() : nullptr;
-    a.flush_tiles = 1;
+    a.flush_log2 = 0;
     a.rows_pad = rows_pad;
     a.diag_tile0 = -1;
     if (mode == kModeGauss)
@@ -396,7 +396,8 @@ Status score_program(Device& D, const Options& o, const Job& J, const double* dX
     a.sc = sc;
     a.dpart0 = D.part0.as<double>();
     a.dpart1 = D.part1.as<double>();
-    a.flush_tiles = std::max(1, o.flush_tiles);
+    a.flush_log2 = 0;
+    while ((2 << a.flush_log2) <= o.flush_tiles) ++a.flush_log2;
     a.rows_pad = rows_pad;
     a.diag_tile0 = static_cast<int>(sh.begin / kTileRows);
     a.trace = o.trace;
@@ -885,7 +886,7 @@ int fkde_gpu_set_option(fkde_gpu_ctx* ctx, int key, int64_t value) {
             ctx->opt.trace = reinterpret_cast<long long*>(value);
             return FKDE_OK;
         case FKDE_OPT_FLUSH_TILES:
-            if (value < 1 || value > 1 << 20) return FKDE_INVALID_ARGUMENT;
+            if (value < 1 || value > 1 << 20 || (value & (value - 1))) return FKDE_INVALID_ARGUMENT;
             ctx->opt.flush_tiles = static_cast<int>(value);
             return FKDE_OK;
         default:

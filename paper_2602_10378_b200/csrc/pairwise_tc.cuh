@@ -22,9 +22,9 @@
 // The n x n kernel matrix never leaves the SM; per column tile the SMEM
 // traffic is the 16 KiB B tile read by both GEMMs and the 16 KiB A tile.
 //
-// Warp roles (320 threads): warp 0 = bulk-copy producer, warp 1 = TMEM owner +
-// single-thread MMA issuer, warps 2..9 = epilogue (warp w reads TMEM lane
-// quadrant w%4, column half (w-2)/4).  Pipelines (mbarriers): A tiles x2,
+// Warp roles (320/352 threads): warp 0 = bulk-copy producer, warp 1 = TMEM
+// owner + GEMM1 issuer, warp 10 (score) = GEMM2 issuer, warps 2..9 = epilogue
+// (warp w reads TMEM lane quadrant w%4 of every other tile, parity (w-2)/4).  Pipelines (mbarriers): A tiles x2,
 // B tiles x kStages, S/P accumulators x2 (TMEM), O x1 (TMEM).  The MMA
 // thread's tcgen05 ops execute in issue order, so GEMM1(t+2) overwriting the
 // S/P buffer of tile t is ordered after GEMM2(t) reading P(t) from it.
@@ -54,22 +54,28 @@ struct PairArgs {
     float* part1;         // Laplace: [splits*2][rows_pad]
     double* dpart0;       // SCORE: S' [splits][rows_pad]   (fp64)
     double* dpart1;       // SCORE: T' [splits][rows_pad][16] (fp64)
-    int flush_tiles;      // SCORE: O is drained to fp64 registers every this many tiles
+    int flush_log2;       // SCORE: O is drained every 2^flush_log2 column tiles (a sub-unit)
     size_t rows_pad;
     // SCORE: column tile holding row tile 0's diagonal (rows and columns are
     // the same point set, row shard start = diag_tile0 * 128); the self pair
     // phi_ii = 1 is excluded from the tensor-core sums and added back exactly
     // in finalize_score, so that T - x S never cancels against the self term.
     int diag_tile0;       // -1: no diagonal
-    // debug: per-event clock64 trace of block 0 (nullptr = off).  Layout
-    // [role(0..9 warp)][event slot][tile] -> long long
+    // debug (builds with -DFKDE_ENABLE_TRACE only): per-event clock64 trace of
+    // block 0 (nullptr = off).  Layout [warp][event slot][tile] -> long long
     long long* trace;
 };
+#ifdef FKDE_ENABLE_TRACE
 #define FKDE_TRACE(slot, tile)                                                               \
     do {                                                                                     \
         if (args.trace && blockIdx.x == 0 && lane == 0 && (tile) < 256)                      \
             args.trace[(warp * 8 + (slot)) * 256 + (tile)] = clock64();                      \
     } while (0)
+#else
+#define FKDE_TRACE(slot, tile) \
+    do {                       \
+    } while (0)
+#endif
 
 template <int MODE>
 struct TcConfig {
@@ -79,7 +85,13 @@ struct TcConfig {
     // 10 GEMM2 issuer (score only).  tcgen05.mma issue blocks while the
     // tensor core is busy, so GEMM1 and GEMM2 get their own issuing warps and
     // the tensor core never idles behind a GEMM2 that waits for P.
-    static constexpr int kThreads = kScore ? 352 : 320;
+    // score: GEMM2 issuer warp (10; 11 would put it on the sub-partition
+    // without another control warp -- measured no difference)
+#ifndef FKDE_G2_WARP
+#define FKDE_G2_WARP 10
+#endif
+    static constexpr int kG2Warp = FKDE_G2_WARP;
+    static constexpr int kThreads = kScore ? (kG2Warp + 1) * 32 : 320;
     static constexpr uint32_t kOffA = 0;
     static constexpr uint32_t kOffB = 2 * kTileBytes;
     // score: fp64 drain accumulators, [2 halves][128 rows][kAccStride] doubles
@@ -98,6 +110,13 @@ struct TcConfig {
     static constexpr uint32_t kTmemO = 384;   // score: O[2] (2 x 64 cols: T_hi, S, T_lo)
     static constexpr uint32_t kN2 = 48;       // GEMM2 N
 };
+
+// score epilogue: pairs w (of the 16 per 32-column chunk) whose exponentials
+// are evaluated on the FMA pipe (ptx::ex2_poly2) instead of MUFU
+#ifndef FKDE_POLY_MASK
+#define FKDE_POLY_MASK 0x0000
+#endif
+constexpr uint32_t kPolyMask = FKDE_POLY_MASK;
 
 template <int MODE>
 __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kernel(PairArgs args) {
@@ -133,8 +152,8 @@ __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kerne
         }
         for (int i = 0; i < 4; ++i) {
             ptx::mbar_init(&s_full[i], 1);
-            ptx::mbar_init(&s_empty[i], 8);
-            ptx::mbar_init(&p_full[i], 8);
+            ptx::mbar_init(&s_empty[i], 4);
+            ptx::mbar_init(&p_full[i], 4);
             ptx::mbar_init(&s_free[i], 1);
         }
         for (int i = 0; i < kStages; ++i) {
@@ -190,7 +209,7 @@ __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kerne
                 ++it_b;
             }
         }
-    } else if (warp == 1 || (kScore && warp == 10)) {
+    } else if (warp == 1 || (kScore && warp == Cfg::kG2Warp)) {
         // ===================== MMA issuers =====================
         // Whole warp in the loop, one elected lane issues every tcgen05 op
         // (commits must come from the issuing thread; elect.sync on a
@@ -204,16 +223,15 @@ __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kerne
         const uint64_t descBmn = ptx::smem_desc_sw128(ptx::smem_u32(smB), kTileBytes, 1024);
         uint32_t it_a = 0, it_b = 0, it_s = 0, it_u = 0;
         const bool g1 = warp == 1;
-        // GEMM2 (warp 10): O += P_hi.B + P_lo.B, P read from TMEM.  Epilogue
-        // warp-group hf stored, in S buffer sb's columns [hf*64, hf*64+64):
-        // P_hi (packed fp16 pairs) for K = hf*64..+63 in the first 32 columns,
-        // P_lo in the next 32.  O is accumulated in TMEM over `flush_tiles`
-        // column tiles (a "sub-unit"), then drained by the epilogue into fp64;
+        // GEMM2 (warp 10): O += P_hi.B + P_lo.B, P read from TMEM.  The
+        // epilogue stored, for each 32-column chunk c of S buffer sb, P_hi
+        // (packed fp16 pairs) for K = 32c..32c+31 in the chunk's first 16
+        // columns and P_lo in the next 16.  O is accumulated in TMEM over
+        // 2^flush_log2 column tiles (a "sub-unit"), then drained by the epilogue;
         // two O buffers alternate so the drain overlaps the next sub-unit.  This
         // bounds the tensor core's fp32 accumulation length (its truncation
         // error grows with the accumulator magnitude x the number of steps).
-        const int F = args.flush_tiles;
-        int sub_left = 0;
+        const int fmask = (1 << args.flush_log2) - 1;
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
             const int sp = u / args.n_row_tiles;
             const int ct0 = static_cast<int>((long long)sp * args.n_col_tiles / args.splits);
@@ -235,6 +253,7 @@ __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kerne
                     // the tile that last used this buffer has finished reading P.
                     if constexpr (!kScore) ptx::mbar_wait(&s_empty[sb], ph ^ 1);
                     else ptx::mbar_wait(&s_free[sb], ph ^ 1);
+                    FKDE_TRACE(5, it_s);
                     ptx::tc_fence_after();
                     if (ptx::elect_one()) {
                         const uint64_t da0 = descA + ((ab * kTileBytes) >> 4);
@@ -254,12 +273,9 @@ __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kerne
                     __syncwarp();
                     FKDE_TRACE(4, it_s);
                 } else if constexpr (kScore) {
-                    const int idx = ct - ct0;
-                    if (idx == 0) sub_left = F;
-                    const bool first = sub_left == F;
-                    --sub_left;
-                    const bool last = sub_left == 0 || ct == ct1 - 1;
-                    if (last) sub_left = F;
+                    const int rel = ct - ct0;
+                    const bool first = (rel & fmask) == 0;
+                    const bool last = (rel & fmask) == fmask || ct == ct1 - 1;
                     const uint32_t ob = it_u & 1;
                     FKDE_TRACE(2, it_s);
                     ptx::mbar_wait(&p_full[sb], ph);
@@ -271,11 +287,11 @@ __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kerne
                         const uint32_t ta0 = tmem_base + sb * 128;
                         const uint32_t to = tmem_base + Cfg::kTmemO + ob * 64;
 #pragma unroll
-                        for (int part = 0; part < 2; ++part) {
+                        for (int k = 0; k < 8; ++k) {
 #pragma unroll
-                            for (int k = 0; k < 8; ++k) {
+                            for (int part = 0; part < 2; ++part) {
                                 // one N=48 MMA per K step: columns 0-15 T_hi, 16 S, 32-47 T_lo
-                                ptx::umma_f16_ts(to, ta0 + (k >> 2) * 64 + part * 32 + (k & 3) * 8,
+                                ptx::umma_f16_ts(to, ta0 + (k >> 1) * 32 + part * 16 + (k & 1) * 8,
                                                  db0 + ((k * 2048) >> 4), idesc2,
                                                  (first && part == 0 && k == 0) ? 0u : 1u);
                             }
@@ -297,166 +313,188 @@ __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kerne
             }
             ++it_a;
         }
-    } else {
+    } else if (warp >= 2 && warp < 10) {
         // ===================== epilogue warps =====================
+        // Warp w reads TMEM lane quadrant w%4 and handles every other column
+        // tile (parity (w-2)/4), all 128 columns of it.  The two warps sharing
+        // an SM sub-partition (and a lane quadrant) therefore work on
+        // different tiles, out of phase: while one waits for its S tile or
+        // for tcgen05.ld the other keeps the MUFU pipe busy.  The loop visits
+        // only this warp's own tiles; all per-tile bookkeeping is a few
+        // integer ops (the two warps per sub-partition cannot hide long
+        // dependent scalar chains).
         const int q = warp & 3;             // TMEM lane quadrant
-        const int hf = (warp - 2) >> 2;     // column half of each tile
+        const int par = (warp - 2) >> 2;    // tile parity handled by this warp
         const int r = q * 32 + lane;        // row within the 128-row tile
         const float dsc = args.sc->dscale;
         const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
-        uint32_t it_s = 0, it_u = 0;
+        const int lf = args.flush_log2;
+        uint32_t it_s = 0, it_u = 0;        // global tile / O sub-unit counters (all parities)
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
             const int sp = u / args.n_row_tiles, rt = u % args.n_row_tiles;
             const int ct0 = static_cast<int>((long long)sp * args.n_col_tiles / args.splits);
             const int ct1 = static_cast<int>((long long)(sp + 1) * args.n_col_tiles / args.splits);
+            const int len = ct1 - ct0;
             float2 acc2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
             float2 accl2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-            // score: fp64 running sums of the drained O sub-unit accumulators,
-            // kept in shared memory (registers are the epilogue's scarce resource)
-            double* acc = reinterpret_cast<double*>(smem + Cfg::kOffAcc) +
-                          (hf * 128 + r) * Cfg::kAccStride;
-            if constexpr (kScore) {
+            // score: running sums of the drained O sub-unit accumulators as
+            // unevaluated float pairs (hi + lo, ~48-bit significand): 2Sum on
+            // the FMA pipe instead of fp64 conversions + adds
+            float ahi[kMaxDim + 1], alo[kMaxDim + 1];
 #pragma unroll
-                for (int c = 0; c <= kMaxDim; ++c) acc[c] = 0.0;
-            }
-            // O_hi sub-unit accumulators are drained alternately by the two
-            // column halves (sub-unit s by half s & 1 -- which is also its
-            // TMEM buffer), one tile late, with the drain's tcgen05.ld merged
-            // into the next tile's S loads (one wait::ld).
-            int pending = -1;      // O buffer-use index awaiting this half's drain
-            int pending_ct = 0;    // first tile at whose end it may be drained
-            int sub_left_e = 0;    // tiles left in the current O sub-unit
-            for (int ct = ct0; ct < ct1; ++ct) {
-                const uint32_t sb = it_s % Cfg::kSBuf;
-                FKDE_TRACE(0, it_s);
-                ptx::mbar_wait(&s_full[sb], (it_s / Cfg::kSBuf) & 1);
-                FKDE_TRACE(1, it_s);
+            for (int c = 0; c <= kMaxDim; ++c) ahi[c] = alo[c] = 0.f;
+            // O sub-unit j (tiles [j << lf, (j+1) << lf) of this unit, global
+            // index it_u + j, TMEM buffer (it_u + j) & 1) is drained by the
+            // parity equal to its global index's, at this warp's first own tile
+            // at least two tiles after its last (its GEMM2 has then completed,
+            // so the o_full wait does not stall), or at the unit end.
+            const int nsub = (len + (1 << lf) - 1) >> lf;
+            int j = (par - static_cast<int>(it_u)) & 1;
+            int drain_at = j < nsub ? min((j + 1) << lf, len) + 1 : INT_MAX;
+            auto drain = [&](int jj) {
+                const uint32_t g = it_u + jj;
+                uint32_t od[16], ol[16], os_;
+                const uint32_t to = lane_addr + Cfg::kTmemO + (g & 1) * 64;
+                ptx::mbar_wait(&o_full[g & 1], (g >> 1) & 1);
+                FKDE_TRACE(4, it_s);
                 ptx::tc_fence_after();
-                uint32_t v0[32], v1[32];
-                const uint32_t ta = lane_addr + sb * 128 + hf * 64;
-                ptx::tmem_ld32(ta, v0);
-                ptx::tmem_ld32(ta + 32, v1);
+                ptx::tmem_ld16(to, od);
+                ptx::tmem_ld1(to + 16, os_);
+                ptx::tmem_ld16(to + 32, ol);
                 ptx::tmem_ld_wait();
-                FKDE_TRACE(6, it_s);
-                if constexpr (!kScore) {
-                    ptx::tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(&s_empty[sb]);
-                }
-                if constexpr (kScore) {
-                    if (args.diag_tile0 >= 0 && ct == args.diag_tile0 + rt) {
-                        const int jj = r - hf * 64;  // this row's diagonal column in v0|v1
+                FKDE_TRACE(5, it_s);
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&o_empty[g & 1]);
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            if (j == jj) v0[j] = 0xFF800000u;        // -inf -> phi = 0
-                            if (j + 32 == jj) v1[j] = 0xFF800000u;
-                        }
-                    }
-                    // phi' = phi * 2^15 split exactly into fp16 hi + lo: hi keeps
-                    // the top 11 significant bits (mask), lo = phi' - hi (exact),
-                    // both convert to fp16 exactly / to nearest.  (S may exceed 0
-                    // by rounding for coincident points: phi' <= 2^15 (1 + 1e-5),
-                    // well inside fp16, so no clamp.)
-                    const float2 dsc2 = make_float2(dsc, dsc);
+                for (int c = 0; c <= kMaxDim; ++c) {
+                    const float x = c < kMaxDim ? __uint_as_float(od[c]) + __uint_as_float(ol[c])
+                                                : __uint_as_float(os_);
+                    const float s2 = ahi[c] + x;           // 2Sum(ahi, x)
+                    const float bb = s2 - ahi[c];
+                    const float e = (ahi[c] - (s2 - bb)) + (x - bb);
+                    ahi[c] = s2;
+                    alo[c] += e;
+                }
+            };
+            // this warp's first own tile and its S buffer / phase
+            int rel = (par - static_cast<int>(it_s)) & 1;
+            uint32_t sidx = it_s + rel;
+            uint32_t sb = sidx % Cfg::kSBuf, ph = (sidx / Cfg::kSBuf) & 1;
+            const int diag_rel = args.diag_tile0 >= 0 ? args.diag_tile0 + rt - ct0 : -1;
+            for (; rel < len; rel += 2) {
+                FKDE_TRACE(0, it_s + rel);
+                ptx::mbar_wait(&s_full[sb], ph);
+                FKDE_TRACE(1, it_s + rel);
+                ptx::tc_fence_after();
+                const uint32_t ts = lane_addr + sb * 128;
+                const float2 dsc2 = make_float2(dsc, dsc);
+                if constexpr (kScore) {
+                    const bool diag = rel == diag_rel;
                     const float2 off2 = make_float2(kPScaleF, kPScaleF);
                     const float2 neg1 = make_float2(-1.f, -1.f);
-                    const uint32_t tp = lane_addr + sb * 128 + hf * 64;
-                    uint32_t hi_w[32], lo_w[32];
+#pragma unroll 1
+                    for (int h2 = 0; h2 < 2; ++h2) {
+                        uint32_t v0[32], v1[32];
+                        ptx::tmem_ld32(ts + h2 * 64, v0);
+                        ptx::tmem_ld32(ts + h2 * 64 + 32, v1);
+                        ptx::tmem_ld_wait();
+                        if (diag) {
+                            const int jj = r - h2 * 64;   // this row's diagonal column
 #pragma unroll
-                    for (int w = 0; w < 32; ++w) {
-                        const uint32_t ra = w < 16 ? v0[2 * w] : v1[2 * w - 32];
-                        const uint32_t rb = w < 16 ? v0[2 * w + 1] : v1[2 * w + 1 - 32];
-                        const float2 t = ptx::ffma2(make_float2(__uint_as_float(ra), __uint_as_float(rb)),
-                                                    dsc2, off2);
-                        const float2 p = make_float2(ptx::ex2(t.x), ptx::ex2(t.y));
-                        const float2 h = make_float2(__uint_as_float(__float_as_uint(p.x) & 0xFFFFE000u),
-                                                     __uint_as_float(__float_as_uint(p.y) & 0xFFFFE000u));
-                        const float2 l = ptx::ffma2(h, neg1, p);
-                        hi_w[w] = ptx::cvt_f16x2(h.x, h.y);
-                        lo_w[w] = ptx::cvt_f16x2(l.x, l.y);
+                            for (int c = 0; c < 32; ++c) {   // -inf -> phi = 0
+                                v0[c] = ptx::sel_eq(v0[c], c, jj, 0xFF800000u);
+                                v1[c] = ptx::sel_eq(v1[c], c + 32, jj, 0xFF800000u);
+                            }
+                        }
+                        // phi' = phi * 2^15 split exactly into fp16 hi + lo: hi keeps
+                        // the top 11 significant bits (mask), lo = phi' - hi (exact),
+                        // both convert to fp16 exactly / to nearest.  (S may exceed 0
+                        // by rounding for coincident points: phi' <= 2^15 (1 + 1e-5),
+                        // well inside fp16, so no clamp.)  Column chunk c (32 S
+                        // columns) is overwritten by its own P: hi words in its
+                        // first 16 columns, lo words in the next 16.
+#pragma unroll
+                        for (int cc = 0; cc < 2; ++cc) {
+                            uint32_t hi_w[16], lo_w[16];
+#pragma unroll
+                            for (int w = 0; w < 16; ++w) {
+                                const uint32_t ra = cc == 0 ? v0[2 * w] : v1[2 * w];
+                                const uint32_t rb = cc == 0 ? v0[2 * w + 1] : v1[2 * w + 1];
+                                const float2 t = ptx::ffma2(
+                                    make_float2(__uint_as_float(ra), __uint_as_float(rb)), dsc2, off2);
+                                const float2 p = ((kPolyMask >> w) & 1)
+                                                     ? ptx::ex2_poly2(t)
+                                                     : make_float2(ptx::ex2(t.x), ptx::ex2(t.y));
+                                const float2 h = make_float2(
+                                    __uint_as_float(__float_as_uint(p.x) & 0xFFFFE000u),
+                                    __uint_as_float(__float_as_uint(p.y) & 0xFFFFE000u));
+                                const float2 l = ptx::ffma2(h, neg1, p);
+                                hi_w[w] = ptx::cvt_f16x2(h.x, h.y);
+                                lo_w[w] = ptx::cvt_f16x2(l.x, l.y);
+                            }
+                            ptx::tmem_st16(ts + h2 * 64 + cc * 32, hi_w);
+                            ptx::tmem_st16(ts + h2 * 64 + cc * 32 + 16, lo_w);
+                        }
                     }
-                    ptx::tmem_st32(tp, hi_w);
-                    ptx::tmem_st32(tp + 32, lo_w);
-                    FKDE_TRACE(7, it_s);
+                    FKDE_TRACE(7, it_s + rel);
                     ptx::tmem_st_wait();
                     ptx::tc_fence_before();
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(&p_full[sb]);
-                    FKDE_TRACE(2, it_s);
-                    // drain this half's pending sub-unit two tiles late (its last GEMM2
-                    // has certainly completed, so the wait below never stalls)
-                    if (pending >= 0 && ct >= pending_ct) {
-                        uint32_t od[16], ol[16], os_;
-                        const uint32_t to = lane_addr + Cfg::kTmemO + (pending & 1) * 64;
-                        ptx::mbar_wait(&o_full[pending & 1], (pending >> 1) & 1);
-                        ptx::tc_fence_after();
-                        ptx::tmem_ld16(to, od);
-                        ptx::tmem_ld1(to + 16, os_);
-                        ptx::tmem_ld16(to + 32, ol);
-                        ptx::tmem_ld_wait();
-                        ptx::tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) ptx::mbar_arrive(&o_empty[pending & 1]);
-                        acc[kMaxDim] += static_cast<double>(__uint_as_float(os_));
-#pragma unroll
-                        for (int c = 0; c < kMaxDim; ++c)
-                            acc[c] += static_cast<double>(__uint_as_float(od[c]) + __uint_as_float(ol[c]));
-                        pending = -1;
-                        FKDE_TRACE(3, it_s);
-                    }
-                    {
-                        if (ct == ct0) sub_left_e = args.flush_tiles;
-                        --sub_left_e;
-                        if (sub_left_e == 0 || ct == ct1 - 1) {
-                            sub_left_e = args.flush_tiles;
-                            if ((it_u & 1) == static_cast<uint32_t>(hf)) {
-                                pending = static_cast<int>(it_u);
-                                pending_ct = ct + 2;
-                            }
-                            ++it_u;
-                        }
+                    FKDE_TRACE(2, it_s + rel);
+                    if (rel >= drain_at) {
+                        drain(j);
+                        j += 2;
+                        drain_at = j < nsub ? min((j + 1) << lf, len) + 1 : INT_MAX;
+                        FKDE_TRACE(3, it_s + rel);
                     }
                 } else {
                     // (phi <= 1 up to the expansion's rounding: no clamp needed)
-                    const float2 dsc2 = make_float2(dsc, dsc);
+#pragma unroll 1
+                    for (int h2 = 0; h2 < 2; ++h2) {
+                        uint32_t v0[32], v1[32];
+                        ptx::tmem_ld32(ts + h2 * 64, v0);
+                        ptx::tmem_ld32(ts + h2 * 64 + 32, v1);
+                        ptx::tmem_ld_wait();
+                        if (h2 == 1) {
+                            ptx::tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) ptx::mbar_arrive(&s_empty[sb]);
+                        }
 #pragma unroll
-                    for (int j = 0; j < 64; j += 2) {
-                        const uint32_t ra = j < 32 ? v0[j] : v1[j - 32];
-                        const uint32_t rb = j < 32 ? v0[j + 1] : v1[j + 1 - 32];
-                        const float2 dd = ptx::fmul2(make_float2(__uint_as_float(ra), __uint_as_float(rb)),
-                                                     dsc2);
-                        const float2 p = make_float2(ptx::ex2(dd.x), ptx::ex2(dd.y));
-                        const int a = (j >> 1) & 1;
-                        acc2[a] = ptx::fadd2(acc2[a], p);
-                        if constexpr (MODE == kModeLaplace) accl2[a] = ptx::ffma2(p, dd, accl2[a]);
+                        for (int c = 0; c < 64; c += 2) {
+                            const uint32_t ra = c < 32 ? v0[c] : v1[c - 32];
+                            const uint32_t rb = c < 32 ? v0[c + 1] : v1[c + 1 - 32];
+                            const float2 dd = ptx::fmul2(
+                                make_float2(__uint_as_float(ra), __uint_as_float(rb)), dsc2);
+                            const float2 p = make_float2(ptx::ex2(dd.x), ptx::ex2(dd.y));
+                            const int a = (c >> 1) & 1;
+                            acc2[a] = ptx::fadd2(acc2[a], p);
+                            if constexpr (MODE == kModeLaplace) accl2[a] = ptx::ffma2(p, dd, accl2[a]);
+                        }
                     }
                 }
-                ++it_s;
+                // next own tile: buffer index advances by 2 (mod kSBuf)
+                sb += 2;
+                if (sb >= Cfg::kSBuf) {
+                    sb -= Cfg::kSBuf;
+                    ph ^= 1;
+                }
             }
             const size_t row = static_cast<size_t>(rt) * kTileRows + r;
             if constexpr (kScore) {
-                if (pending >= 0) {
-                    uint32_t od[16], ol[16], os_;
-                    const uint32_t to = lane_addr + Cfg::kTmemO + (pending & 1) * 64;
-                    ptx::mbar_wait(&o_full[pending & 1], (pending >> 1) & 1);
-                    ptx::tc_fence_after();
-                    ptx::tmem_ld16(to, od);
-                    ptx::tmem_ld1(to + 16, os_);
-                    ptx::tmem_ld16(to + 32, ol);
-                    ptx::tmem_ld_wait();
-                    ptx::tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(&o_empty[pending & 1]);
-                    acc[kMaxDim] += static_cast<double>(__uint_as_float(os_));
-#pragma unroll
-                    for (int c = 0; c < kMaxDim; ++c)
-                        acc[c] += static_cast<double>(__uint_as_float(od[c]) + __uint_as_float(ol[c]));
-                }
-                // the two halves drained disjoint sub-units: merge them through
+                for (; j < nsub; j += 2) drain(j);
+                // the two parities drained disjoint sub-units: merge them through
                 // shared memory (named barrier over the 8 epilogue warps) and
                 // write one fp64 partial per (split, row)
+                double* acc = reinterpret_cast<double*>(smem + Cfg::kOffAcc) +
+                              (par * 128 + r) * Cfg::kAccStride;
+#pragma unroll
+                for (int c = 0; c <= kMaxDim; ++c)
+                    acc[c] = static_cast<double>(ahi[c]) + static_cast<double>(alo[c]);
                 asm volatile("bar.sync 1, 256;" ::: "memory");
-                if (hf == 0) {
+                if (par == 0) {
                     const double* other = acc + 128 * Cfg::kAccStride;
                     const size_t idx = static_cast<size_t>(sp) * args.rows_pad + row;
                     args.dpart0[idx] = acc[kMaxDim] + other[kMaxDim];
@@ -465,13 +503,15 @@ __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kerne
                     for (int w = 0; w < kMaxDim / 2; ++w)
                         t[w] = make_double2(acc[2 * w] + other[2 * w], acc[2 * w + 1] + other[2 * w + 1]);
                 }
-                asm volatile("bar.sync 1, 256;" ::: "memory");   // acc is re-zeroed next unit
+                asm volatile("bar.sync 1, 256;" ::: "memory");   // acc is rewritten next unit
+                it_u += nsub;
             } else {
-                const size_t idx = static_cast<size_t>(sp * 2 + hf) * args.rows_pad + row;
+                const size_t idx = static_cast<size_t>(sp * 2 + par) * args.rows_pad + row;
                 args.part0[idx] = (acc2[0].x + acc2[0].y) + (acc2[1].x + acc2[1].y);
                 if constexpr (MODE == kModeLaplace)
                     args.part1[idx] = (accl2[0].x + accl2[0].y) + (accl2[1].x + accl2[1].y);
             }
+            it_s += len;
         }
     }
 

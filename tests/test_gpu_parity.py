@@ -192,6 +192,29 @@ def test_split_count_reassociation(port):
             assert max_rel_global_floor(s, base[1]) < 1e-4
 
 
+def test_flush_interval_and_ragged_units(port):
+    # O sub-unit drains (FKDE_OPT_FLUSH_TILES) with units of odd length (32 column
+    # tiles over 5 / 3 splits -> 6-7 and 10-11 tiles): the two epilogue parities
+    # and the drain schedule must cover every tile exactly once for any interval.
+    tr = _mixture_inputs(port, 4096, 16)[0]
+    h = 1.5
+    ref = port.score_naive(tr, tr, h)
+    for splits in (5, 3):
+        for flush in (1, 2, 4, 1 << 20):
+            c = fk.Context([0])
+            c.set_option(N.OPT_SPLITS, splits)
+            c.set_option(N.OPT_FLUSH_TILES, flush)
+            s = fk.score_flash(tr, h, ctx=c).values
+            c.close()
+            assert max_rel_global_floor(s, ref) < TOL_SCORE, (splits, flush)
+
+
+def test_flush_interval_must_be_power_of_two(ctx):
+    for bad in (0, 3, 6, (1 << 20) + 1):
+        with pytest.raises(fk.InvalidArgumentError):
+            ctx.set_option(N.OPT_FLUSH_TILES, bad)
+
+
 def test_tc_engine_matches_simt_engine(ctx, simt, port):
     tr, q = _mixture_inputs(port, 4096, 2048)
     h = 1.5

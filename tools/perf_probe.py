@@ -42,9 +42,13 @@ def run(ctx, kind, n, m, reps=5, seed=0):
         assert rc == 0, ctx.last_error()
 
     torch.cuda.synchronize()
+    s0 = torch.cuda.Event(enable_timing=True)
+    e0 = torch.cuda.Event(enable_timing=True)
+    s0.record(stream)
     once()
-    stream.synchronize()
-    times = [0.0]
+    e0.record(stream)
+    e0.synchronize()
+    times = [s0.elapsed_time(e0)]
     for _ in range(reps):
         s = torch.cuda.Event(enable_timing=True)
         e = torch.cuda.Event(enable_timing=True)
@@ -69,6 +73,8 @@ def main():
     which = sys.argv[1:] or ["small", "big"]
     if "sd1m" in which:
         run(ctx, "sdkde", 1 << 20, 1 << 17, reps=0)
+    if "sd256k" in which:
+        run(ctx, "sdkde", 1 << 18, 1 << 14, reps=0)
     if "sd32k" in which:
         run(ctx, "sdkde", 32768, 32768, reps=1)
     if "small" in which:

@@ -26,25 +26,33 @@ def main():
     t = buf.view(11, 8, 256).cpu().numpy().astype(np.float64)
     lo, hi = 16, 200
     print(f"n={n} flush={flush}: tiles {lo}..{hi} of block 0 (cycles)")
-    per = np.diff(t[2, 0, lo:hi + 1])
-    print(f"  epilogue tile period (warp 2): mean {per.mean():.0f}  min {per.min():.0f}  max {per.max():.0f}")
     for w in range(2, 10):
-        ldl = t[w, 6, lo:hi] - t[w, 1, lo:hi]
-        cmp_ = t[w, 7, lo:hi] - t[w, 6, lo:hi]
-        stl = t[w, 2, lo:hi] - t[w, 7, lo:hi]
-        print(f"  warp {w}: LDTM latency {ldl.mean():5.0f}  compute {cmp_.mean():5.0f}  STTM wait+arrive {stl.mean():5.0f}")
-    for w in range(2, 10):
-        s_wait = t[w, 1, lo:hi] - t[w, 0, lo:hi]
-        comp = t[w, 2, lo:hi] - t[w, 1, lo:hi]
-        d = t[w, 3, lo:hi] - t[w, 2, lo:hi]
-        d = d[(t[w, 3, lo:hi] > 0) & (d > 0) & (d < 1e6)]
-        print(f"  warp {w}: s_full wait {s_wait.mean():6.0f}  ld+exp+P store {comp.mean():6.0f}  "
-              f"drain {d.mean() if d.size else 0:6.0f} ({d.size} drains)")
+        own = np.arange(lo, hi)
+        own = own[t[w, 1, own] > 0]          # tiles this warp processed (its parity)
+        per = np.diff(t[w, 1, own])
+        s_wait = t[w, 1, own] - t[w, 0, own]
+        ldl = t[w, 6, own] - t[w, 1, own]
+        comp = t[w, 7, own] - t[w, 1, own]
+        stl = t[w, 2, own] - t[w, 7, own]
+        d = t[w, 3, own] - t[w, 2, own]
+        d = d[(t[w, 3, own] > 0) & (d > 0) & (d < 1e6)]
+        gap = t[w, 0, own[1:]] - t[w, 2, own[:-1]]
+        dr = (t[w, 3, own[:-1]] > 0)
+        gd = gap[dr] - (t[w, 3, own[:-1]] - t[w, 2, own[:-1]])[dr]
+        ow = (t[w, 4, own] - t[w, 2, own])[t[w, 3, own] > 0]
+        lw = (t[w, 5, own] - t[w, 4, own])[t[w, 3, own] > 0]
+        aw = (t[w, 3, own] - t[w, 5, own])[t[w, 3, own] > 0]
+        print(f"      drain: o_full wait {ow.mean():5.0f}  ld {lw.mean():5.0f}  accumulate {aw.mean():5.0f}; "
+              f"after-drain gap {gd.mean():5.0f}  no-drain gap {gap[~dr].mean():5.0f}")
+        print(f"  warp {w}: {own.size} tiles, period {per.mean():6.0f}  s_full wait {s_wait.mean():5.0f}  "
+              f"first ld {ldl.mean():4.0f}  ld+exp+st issue {comp.mean():6.0f}  st wait+arrive {stl.mean():4.0f}  "
+              f"drain {d.mean() if d.size else 0:5.0f} ({d.size})  other {gap.mean():5.0f}")
     bwait = t[1, 1, lo:hi] - t[1, 0, lo:hi]
     pwait = t[10, 3, lo:hi] - t[10, 2, lo:hi]
     g2 = t[10, 5, lo:hi] - t[10, 3, lo:hi]
-    g1 = t[1, 4, lo:hi] - t[1, 1, lo:hi]
-    print(f"  GEMM1 warp: b_full+s_free wait {bwait.mean():.0f}  GEMM1 issue {g1.mean():.0f}")
+    fwait = t[1, 5, lo:hi] - t[1, 1, lo:hi]
+    g1 = t[1, 4, lo:hi] - t[1, 5, lo:hi]
+    print(f"  GEMM1 warp: b_full wait {bwait.mean():.0f}  s_free wait {fwait.mean():.0f}  GEMM1 issue {g1.mean():.0f}")
     print(f"  GEMM2 warp: p_full wait {pwait.mean():.0f}  GEMM2 issue {g2.mean():.0f}")
     extra(t, lo, hi)
 
@@ -52,12 +60,15 @@ def main():
 
 
 def extra(t, lo=16, hi=200):
-    arr = t[2:10, 2, lo:hi]            # P-arrive times of the 8 epilogue warps
-    spread = arr.max(0) - arr.min(0)
+    arr = t[2:10, 2, lo:hi]            # P-arrive times of the epilogue warps (0 = not its tile)
+    arr = np.where(arr > 0, arr, np.nan)
+    spread = np.nanmax(arr, 0) - np.nanmin(arr, 0)
     print(f"  P-arrive spread across warps per tile: mean {spread.mean():.0f} max {spread.max():.0f}")
     g1 = t[1, 4, lo:hi]                # GEMM1(t) issued
-    ready = t[2:10, 1, lo:hi].min(0)   # first warp passing s_full(t)
+    ready = np.nanmin(np.where(t[2:10, 1, lo:hi] > 0, t[2:10, 1, lo:hi], np.nan), 0)
     print(f"  GEMM1 issue -> first s_full pass: mean {np.mean(ready - g1):.0f}")
+    per = np.diff(t[1, 4, lo:hi + 1])
+    print(f"  GEMM1 tile period: mean {per.mean():.0f}")
     last_arrive = arr.max(0)
     print(f"  GEMM1(t) issue minus last P-arrive(t-3): {np.mean(g1[3:] - last_arrive[:-3]):.0f}")
     print(f"  GEMM1(t) issue minus last P-arrive(t-2): {np.mean(g1[2:] - last_arrive[:-2]):.0f}")
