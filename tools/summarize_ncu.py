@@ -12,6 +12,7 @@ import csv
 import io
 import json
 import os
+import re
 import shutil
 import subprocess
 
@@ -56,10 +57,18 @@ def stalls(rep):
     for r in csv.reader(io.StringIO(out)):
         if r and r[0] == "Kernel Name":
             kern = r[1]
+            kern = norm(kern)
             per[kern] = []
         elif kern and r and r[0].startswith("0x") and len(r) > 3:
             per[kern].append((int(r[2] or 0), r[1].strip()))
     return per
+
+
+def norm(name):
+    """Kernel names differ between ncu pages ('void pairwise_tc_kernel<0>(PairArgs)'
+    on the raw page, 'void fkde_b200::pairwise_tc_kernel<(int)0>(fkde_b200::PairArgs)'
+    on the source page): strip namespaces and template-argument casts."""
+    return re.sub(r"\w+::", "", name).replace("(int)", "").strip()
 
 
 def fnum(x):
@@ -96,7 +105,7 @@ def main():
                 if key in k:
                     md.append(f"| {label} (`{key}`) | {k[key]} {k['_units'].get(key, '')} |")
             md.append("")
-            samples = sp.get(name, [])
+            samples = sp.get(norm(name), [])
             tot = sum(s for s, _ in samples) or 1
             top = sorted(samples, reverse=True)[:8]
             if top:
@@ -105,7 +114,7 @@ def main():
                 for s, ins in top:
                     md.append(f"- {100.0 * s / tot:5.1f}%  `{ins}`")
                 md.append("")
-            if "<(int)0>" in name and "1m" in os.path.basename(rep):
+            if "pairwise_tc_kernel<0>" in norm(name) and "1m" in os.path.basename(rep):
                 rd = fnum(k.get("dram__bytes_read.sum"))
                 wr = fnum(k.get("dram__bytes_write.sum"))
                 unit = k["_units"].get("dram__bytes_read.sum", "byte")
