@@ -70,7 +70,8 @@ enum {
     FKDE_OPT_MAX_CTAS = 4,    /* 0 = all SMs; >0 caps the persistent grid        */
     FKDE_OPT_FLUSH_TILES = 5, /* score pass: drain the TMEM accumulator to the
                                  extended-precision register sums every k column
-                                 tiles; k a power of two in [1, 2^20] (default 2) */
+                                 tiles; k a power of two in [1, 2^20], or 0 for
+                                 the default (~256 columns)                      */
     FKDE_OPT_TRACE_PTR = 6    /* debug: device pointer (11*8*256 int64) receiving
                                  clock64 stamps of the score kernel's block 0   */
 };

@@ -19,6 +19,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <numeric>
 #include <atomic>
 #include <cmath>
 #include <cstdarg>
@@ -152,7 +153,7 @@ struct Options {
     int splits = 0;
     int timing = 0;
     int max_ctas = 0;
-    int flush_tiles = 2;
+    int flush_tiles = 0;   // 0: ~256 columns (engine default)
     long long* trace = nullptr;   // debug: device buffer for pairwise_tc_kernel's clock trace
 };
 
@@ -268,8 +269,8 @@ Status compute_mean(Device& D, const double* dX, size_t n, int d, PassScalars* s
 }
 
 Status pack(Device& D, const double* x, size_t rows, int d, int format, bool center, double k,
-            const PassScalars* sc, DevBuf& out, size_t* rows_padded) {
-    const size_t rp = round_up(std::max<size_t>(rows, 1), kTileRows);
+            const PassScalars* sc, DevBuf& out, size_t* rows_padded, size_t align = kTileRows) {
+    const size_t rp = round_up(std::max<size_t>(rows, 1), align);
     STATUS_TRY(ensure(out, rp * kRowBytes));
     PackArgs a;
     a.x = x;
@@ -297,7 +298,10 @@ Status density_pass(Device& D, const Options& o, int mode, size_t rows_pad, size
                                               : choose_splits(o, rt, ct, o.max_ctas > 0
                                                                              ? std::min(o.max_ctas, D.num_sms)
                                                                              : D.num_sms);
-    const size_t nparts = static_cast<size_t>(splits) * 2;
+    // partial sums per (split, row): SIMT writes 2 (column halves), the tensor-core
+    // kernel one per epilogue tile phase
+    const size_t per = o.engine == FKDE_ENGINE_SIMT ? 2 : TcConfig<kModeGauss>::kNP;
+    const size_t nparts = static_cast<size_t>(splits) * per;
     STATUS_TRY(ensure(D.part0, nparts * rows_pad * sizeof(float)));
     if (mode == kModeLaplace) STATUS_TRY(ensure(D.part1, nparts * rows_pad * sizeof(float)));
     PairArgs a{};
@@ -311,7 +315,7 @@ Status density_pass(Device& D, const Options& o, int mode, size_t rows_pad, size
     a.part1 = mode == kModeLaplace ? D.part1.as<float>() : nullptr;
     a.flush_log2 = 0;
     a.rows_pad = rows_pad;
-    a.diag_tile0 = -1;
+    a.diag_row0 = -1;
     if (mode == kModeGauss)
         STATUS_TRY(launch_pairwise<kModeGauss>(D, o, a, n_cols));
     else
@@ -378,10 +382,15 @@ Status score_program(Device& D, const Options& o, const Job& J, const double* dX
     const Shard sh = shard_of(n, D.world, D.rank, kTileRows);
     size_t rows_pad = 0, cols_pad = 0;
     STATUS_TRY(pack(D, dX + sh.begin * d, sh.rows, d, 0, true, ks, sc, D.opA, &rows_pad));
-    STATUS_TRY(pack(D, dX, n, d, 1, true, ks, sc, D.opB, &cols_pad));
+    // score-pass column tiles are TcConfig<kModeScore>::kNCol points wide: pad the
+    // column operand to a whole number of those and of 128-point pack tiles
+    constexpr size_t kScoreNCol = TcConfig<kModeScore>::kNCol;
+    const size_t col_align = std::lcm<size_t>(kScoreNCol, kTileRows);
+    STATUS_TRY(pack(D, dX, n, d, 1, true, ks, sc, D.opB, &cols_pad, col_align));
     record(D, o, FKDE_T_SCORE);
 
-    const size_t rt = rows_pad / kTileRows, ct = cols_pad / kTileRows;
+    const size_t rt = rows_pad / kTileRows;
+    const size_t ct = cols_pad / (o.engine == FKDE_ENGINE_SIMT ? kTileRows : kScoreNCol);
     const int ctas = o.max_ctas > 0 ? std::min(o.max_ctas, D.num_sms) : D.num_sms;
     const int splits = o.engine == FKDE_ENGINE_SIMT ? 1 : choose_splits(o, rt, ct, ctas);
     // fp64 partials per split
@@ -396,10 +405,14 @@ Status score_program(Device& D, const Options& o, const Job& J, const double* dX
     a.sc = sc;
     a.dpart0 = D.part0.as<double>();
     a.dpart1 = D.part1.as<double>();
+    // drain interval: the option, or by default ~256 columns (the accumulation
+    // length that keeps the tensor core's truncation error near 2e-4)
+    const int flush = o.flush_tiles > 0 ? o.flush_tiles
+                                        : std::max<int>(1, 256 / static_cast<int>(kScoreNCol));
     a.flush_log2 = 0;
-    while ((2 << a.flush_log2) <= o.flush_tiles) ++a.flush_log2;
+    while ((2 << a.flush_log2) <= flush) ++a.flush_log2;
     a.rows_pad = rows_pad;
-    a.diag_tile0 = static_cast<int>(sh.begin / kTileRows);
+    a.diag_row0 = static_cast<long long>(sh.begin);
     a.trace = o.trace;
     STATUS_TRY(launch_pairwise<kModeScore>(D, o, a, n));
     record(D, o, FKDE_T_FINALIZE);
@@ -886,7 +899,7 @@ int fkde_gpu_set_option(fkde_gpu_ctx* ctx, int key, int64_t value) {
             ctx->opt.trace = reinterpret_cast<long long*>(value);
             return FKDE_OK;
         case FKDE_OPT_FLUSH_TILES:
-            if (value < 1 || value > 1 << 20 || (value & (value - 1))) return FKDE_INVALID_ARGUMENT;
+            if (value < 0 || value > 1 << 20 || (value & (value - 1))) return FKDE_INVALID_ARGUMENT;
             ctx->opt.flush_tiles = static_cast<int>(value);
             return FKDE_OK;
         default:

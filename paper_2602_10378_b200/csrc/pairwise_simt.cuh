@@ -34,9 +34,8 @@ __device__ __forceinline__ void unpack_y(const uint8_t* tiles, size_t row, bool 
 template <int MODE>
 __global__ void __launch_bounds__(128) pairwise_simt_kernel(PairArgs args, size_t n_cols) {
     // score pass: global column index of this row (self pair excluded, see PairArgs)
-    const long long diag_col = (MODE == kModeScore && args.diag_tile0 >= 0)
-                                   ? static_cast<long long>(args.diag_tile0) * 128 + blockIdx.x * 128ll +
-                                         threadIdx.x
+    const long long diag_col = (MODE == kModeScore && args.diag_row0 >= 0)
+                                   ? args.diag_row0 + blockIdx.x * 128ll + threadIdx.x
                                    : -1;
     __shared__ float cols[128][17];
     const size_t row = blockIdx.x * 128ull + threadIdx.x;

@@ -30,6 +30,7 @@
 // S/P buffer of tile t is ordered after GEMM2(t) reading P(t) from it.
 #pragma once
 #include <cuda_fp16.h>
+#include <climits>
 #include <cstdint>
 
 #include "layout.cuh"
@@ -57,10 +58,10 @@ struct PairArgs {
     int flush_log2;       // SCORE: O is drained every 2^flush_log2 column tiles (a sub-unit)
     size_t rows_pad;
     // SCORE: column tile holding row tile 0's diagonal (rows and columns are
-    // the same point set, row shard start = diag_tile0 * 128); the self pair
+    // the same point set, row shard starting at global point diag_row0); the self pair
     // phi_ii = 1 is excluded from the tensor-core sums and added back exactly
     // in finalize_score, so that T - x S never cancels against the self term.
-    int diag_tile0;       // -1: no diagonal
+    long long diag_row0;  // -1: no diagonal
     // debug (builds with -DFKDE_ENABLE_TRACE only): per-event clock64 trace of
     // block 0 (nullptr = off).  Layout [warp][event slot][tile] -> long long
     long long* trace;
@@ -81,33 +82,45 @@ template <int MODE>
 struct TcConfig {
     static constexpr bool kScore = MODE == kModeScore;
     static constexpr int kStages = 8;
-    // warps: 0 producer, 1 GEMM1 issuer (+ TMEM owner), 2..9 epilogue,
-    // 10 GEMM2 issuer (score only).  tcgen05.mma issue blocks while the
-    // tensor core is busy, so GEMM1 and GEMM2 get their own issuing warps and
-    // the tensor core never idles behind a GEMM2 that waits for P.
-    // score: GEMM2 issuer warp (10; 11 would put it on the sub-partition
-    // without another control warp -- measured no difference)
-#ifndef FKDE_G2_WARP
-#define FKDE_G2_WARP 10
+    // warps: 0 producer, 1 GEMM1 issuer (+ TMEM owner), 2 .. 2+4*kNP-1
+    // epilogue (kNP warps per TMEM lane quadrant, one per SM sub-partition
+    // each), then the GEMM2 issuer (score only).  tcgen05.mma issue blocks
+    // while the tensor core is busy, so GEMM1 and GEMM2 get their own issuing
+    // warps and the tensor core never idles behind a GEMM2 that waits for P.
+#ifndef FKDE_EPI_NP
+#define FKDE_EPI_NP 3
 #endif
-    static constexpr int kG2Warp = FKDE_G2_WARP;
-    static constexpr int kThreads = kScore ? (kG2Warp + 1) * 32 : 320;
+    static constexpr int kNP = FKDE_EPI_NP;          // epilogue warps per lane quadrant
+    static constexpr int kEpi0 = 2;
+    static constexpr int kEpiEnd = kEpi0 + 4 * kNP;
+    static constexpr int kG2Warp = kEpiEnd;
+    static constexpr int kThreads = kScore ? (kG2Warp + 1) * 32 : kEpiEnd * 32;
     static constexpr uint32_t kOffA = 0;
+    // column tile width: score 96 points (4 S/P buffers of 96 TMEM columns fit
+    // beside the two O buffers; 3 of 128 made the S ring the bottleneck), KDE 128
+#ifndef FKDE_SCORE_NCOL
+#define FKDE_SCORE_NCOL 96
+#endif
+    static constexpr int kNCol = kScore ? FKDE_SCORE_NCOL : 128;
+    static constexpr uint32_t kColBytes = kNCol * kRowBytes;   // one B column tile
+    static_assert(kNCol % 32 == 0 && kColBytes % 1024 == 0, "column tiles of whole SW128 atoms");
     static constexpr uint32_t kOffB = 2 * kTileBytes;
-    // score: fp64 drain accumulators, [2 halves][128 rows][kAccStride] doubles
+    // score: per-unit merge area for the kNP epilogue warps' drained sums,
+    // [kNP][128 rows][kAccStride] doubles
     static constexpr uint32_t kAccStride = 17;
     static constexpr uint32_t kOffAcc = kOffB + kStages * kTileBytes;
-    static constexpr uint32_t kAccBytes = kScore ? 2 * 128 * kAccStride * 8 : 0;
+    static constexpr uint32_t kAccBytes = kScore ? kNP * 128 * kAccStride * 8 : 0;
     static constexpr uint32_t kOffBar = kOffAcc + kAccBytes;
     // S accumulators in TMEM (128 columns each).  Score: 3 (S/P of tiles
     // t, t+1, t+2 in flight, GEMM2 lags GEMM1 by two tiles) + O[2] at 384.
     // KDE: 4.
-    static constexpr int kSBuf = kScore ? 3 : 4;
-    static constexpr int kLag = kSBuf - 1;   // score: GEMM2(t) issued after GEMM1(t + kLag)
-    static constexpr uint32_t kNumBars = 4 + 2 * kStages + 4 * 4 + 4;
-    static constexpr uint32_t kSmemBytes = kOffBar + kNumBars * 8 + 16 + 1024;  // + align slack
+    static constexpr int kSBuf = kScore ? 384 / kNCol : 4;
+    static constexpr uint32_t kNumBars = 4 + 2 * kStages + 4 * kSBuf + 4;
+    // + tmem slot, drain tokens, 1 KiB alignment slack
+    static constexpr uint32_t kSmemBytes = kOffBar + kNumBars * 8 + 64 + 1024;
     static constexpr uint32_t kTmemCols = 512;
     static constexpr uint32_t kTmemO = 384;   // score: O[2] (2 x 64 cols: T_hi, S, T_lo)
+    static_assert(!kScore || kSBuf * kNCol <= kTmemO, "S/P buffers overlap O");
     static constexpr uint32_t kN2 = 48;       // GEMM2 N
 };
 
@@ -134,13 +147,17 @@ __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kerne
     uint64_t* a_empty = bars + 2;         // [2]
     uint64_t* b_full = bars + 4;          // [kStages]
     uint64_t* b_empty = b_full + kStages; // [kStages]
-    uint64_t* s_full = b_empty + kStages; // [4]
-    uint64_t* s_empty = s_full + 4;       // [4]
-    uint64_t* p_full = s_empty + 4;       // [4]
-    uint64_t* s_free = p_full + 4;        // [4] score: GEMM2 done reading P (S buffer reusable)
-    uint64_t* o_full = s_free + 4;        // [2]
+    constexpr int kSB = Cfg::kSBuf;
+    uint64_t* s_full = b_empty + kStages; // [kSB]
+    uint64_t* s_empty = s_full + kSB;     // [kSB]
+    uint64_t* p_full = s_empty + kSB;     // [kSB]
+    uint64_t* s_free = p_full + kSB;      // [kSB] score: GEMM2 done reading P (S buffer reusable)
+    uint64_t* o_full = s_free + kSB;      // [2]
     uint64_t* o_empty = o_full + 2;       // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
+    // score: per (lane quadrant, O buffer) count of drains whose o_full wait
+    // has passed (see the epilogue's drain())
+    volatile uint32_t* drain_passed = tmem_slot + 1;   // [4][2]
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -150,7 +167,7 @@ __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kerne
             ptx::mbar_init(&a_full[i], 1);
             ptx::mbar_init(&a_empty[i], 1);
         }
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < kSB; ++i) {
             ptx::mbar_init(&s_full[i], 1);
             ptx::mbar_init(&s_empty[i], 4);
             ptx::mbar_init(&p_full[i], 4);
@@ -166,6 +183,7 @@ __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kerne
         }
 
 
+        for (int i = 0; i < 8; ++i) drain_passed[i] = 0;
         ptx::fence_barrier_init();
     }
     if (warp == 1) ptx::tmem_alloc<Cfg::kTmemCols>(tmem_slot);
@@ -201,22 +219,23 @@ __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kerne
                 const int st = it_b % kStages;
                 ptx::mbar_wait(&b_empty[st], ((it_b / kStages) & 1) ^ 1);
                 if (ptx::elect_one()) {
-                    ptx::mbar_arrive_expect_tx(&b_full[st], kTileBytes);
-                    ptx::bulk_g2s_hint(smB + st * kTileBytes, args.opB + (size_t)ct * kTileBytes,
-                                       kTileBytes, &b_full[st], pol_b);
+                    ptx::mbar_arrive_expect_tx(&b_full[st], Cfg::kColBytes);
+                    ptx::bulk_g2s_hint(smB + st * kTileBytes, args.opB + (size_t)ct * Cfg::kColBytes,
+                                       Cfg::kColBytes, &b_full[st], pol_b);
                 }
                 __syncwarp();
                 ++it_b;
             }
         }
     } else if (warp == 1 || (kScore && warp == Cfg::kG2Warp)) {
+        static_assert(Cfg::kNP <= Cfg::kSBuf, "each epilogue warp holds one S buffer");
         // ===================== MMA issuers =====================
         // Whole warp in the loop, one elected lane issues every tcgen05 op
         // (commits must come from the issuing thread; elect.sync on a
         // converged warp always picks the same lane).  Descriptors are built
         // once and advanced by adding (byte offset >> 4) to the start-address
         // field, so each MMA costs a uniform add + the instruction.
-        constexpr uint32_t idesc1 = ptx::idesc_f16_f32(128, 128, false, false);
+        constexpr uint32_t idesc1 = ptx::idesc_f16_f32(128, Cfg::kNCol, false, false);
         constexpr uint32_t idesc2 = ptx::idesc_f16_f32(128, Cfg::kN2, false, true);
         const uint64_t descA = ptx::smem_desc_sw128(ptx::smem_u32(smA), 16, 1024);
         const uint64_t descB = ptx::smem_desc_sw128(ptx::smem_u32(smB), 16, 1024);
@@ -264,7 +283,7 @@ __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kerne
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk) {
                             const int k = kk == 0 ? 1 : (kk == 1 ? 0 : kk);  // 1 (norms), 0, 2, 3
-                            ptx::umma_f16(tmem_base + sb * 128, da0 + ((k * 32) >> 4),
+                            ptx::umma_f16(tmem_base + sb * Cfg::kNCol, da0 + ((k * 32) >> 4),
                                           db0 + ((k * 32) >> 4), idesc1, kk > 0 ? 1u : 0u);
                         }
                         ptx::umma_commit(&s_full[sb]);
@@ -284,10 +303,10 @@ __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kerne
                     ptx::tc_fence_after();
                     if (ptx::elect_one()) {
                         const uint64_t db0 = descBmn + ((st * kTileBytes) >> 4);
-                        const uint32_t ta0 = tmem_base + sb * 128;
+                        const uint32_t ta0 = tmem_base + sb * Cfg::kNCol;
                         const uint32_t to = tmem_base + Cfg::kTmemO + ob * 64;
 #pragma unroll
-                        for (int k = 0; k < 8; ++k) {
+                        for (int k = 0; k < Cfg::kNCol / 16; ++k) {
 #pragma unroll
                             for (int part = 0; part < 2; ++part) {
                                 // one N=48 MMA per K step: columns 0-15 T_hi, 16 S, 32-47 T_lo
@@ -313,23 +332,26 @@ __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kerne
             }
             ++it_a;
         }
-    } else if (warp >= 2 && warp < 10) {
+    } else if (warp >= Cfg::kEpi0 && warp < Cfg::kEpiEnd) {
         // ===================== epilogue warps =====================
-        // Warp w reads TMEM lane quadrant w%4 and handles every other column
-        // tile (parity (w-2)/4), all 128 columns of it.  The two warps sharing
-        // an SM sub-partition (and a lane quadrant) therefore work on
-        // different tiles, out of phase: while one waits for its S tile or
-        // for tcgen05.ld the other keeps the MUFU pipe busy.  The loop visits
-        // only this warp's own tiles; all per-tile bookkeeping is a few
-        // integer ops (the two warps per sub-partition cannot hide long
-        // dependent scalar chains).
-        const int q = warp & 3;             // TMEM lane quadrant
-        const int par = (warp - 2) >> 2;    // tile parity handled by this warp
-        const int r = q * 32 + lane;        // row within the 128-row tile
+        // Warp w reads TMEM lane quadrant w%4 and handles every kNP-th column
+        // tile (phase par = (w-2)/4), all 128 columns of it, in four 32-column
+        // chunks.  The kNP warps sharing an SM sub-partition (and a lane
+        // quadrant) therefore work on different tiles, out of phase: while one
+        // waits for its next S tile (GEMM1 of tile t + kNP can only start
+        // once GEMM2 of tile t has released the buffer) the others keep the
+        // MUFU pipe busy.  The own-tile loop carries only a few integer ops of
+        // bookkeeping: with few warps per sub-partition, long dependent scalar
+        // chains between tiles would not be hidden.
+        constexpr int NP = Cfg::kNP;
+        const int q = warp & 3;                      // TMEM lane quadrant
+        const int par = (warp - Cfg::kEpi0) >> 2;    // tile phase handled by this warp
+        const int r = q * 32 + lane;                 // row within the 128-row tile
         const float dsc = args.sc->dscale;
         const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
         const int lf = args.flush_log2;
-        uint32_t it_s = 0, it_u = 0;        // global tile / O sub-unit counters (all parities)
+        const int fmask = (1 << lf) - 1;
+        uint32_t it_s = 0, it_u = 0;        // global tile / O sub-unit counters (all phases)
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
             const int sp = u / args.n_row_tiles, rt = u % args.n_row_tiles;
             const int ct0 = static_cast<int>((long long)sp * args.n_col_tiles / args.splits);
@@ -343,26 +365,31 @@ __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kerne
             float ahi[kMaxDim + 1], alo[kMaxDim + 1];
 #pragma unroll
             for (int c = 0; c <= kMaxDim; ++c) ahi[c] = alo[c] = 0.f;
-            // O sub-unit j (tiles [j << lf, (j+1) << lf) of this unit, global
-            // index it_u + j, TMEM buffer (it_u + j) & 1) is drained by the
-            // parity equal to its global index's, at this warp's first own tile
-            // at least two tiles after its last (its GEMM2 has then completed,
-            // so the o_full wait does not stall), or at the unit end.
-            const int nsub = (len + (1 << lf) - 1) >> lf;
-            int j = (par - static_cast<int>(it_u)) & 1;
-            int drain_at = j < nsub ? min((j + 1) << lf, len) + 1 : INT_MAX;
-            auto drain = [&](int jj) {
-                const uint32_t g = it_u + jj;
+            // O sub-unit j covers tiles [j << lf, (j+1) << lf) of this unit
+            // (global index it_u + j, TMEM buffer (it_u + j) & 1).  It is
+            // drained by the warp owning the tile two after its last one, right
+            // after that warp's P store (GEMM2 of the sub-unit has completed by
+            // then, so the o_full wait rarely stalls), or at the unit end.
+            auto drain = [&](int j) {
+                const uint32_t g = it_u + j;
                 uint32_t od[16], ol[16], os_;
                 const uint32_t to = lane_addr + Cfg::kTmemO + (g & 1) * 64;
+                // o_full[g & 1] is a parity wait: it is unambiguous only once the
+                // drain of sub-unit g - 2 (same buffer, possibly by another phase's
+                // warp of this quadrant) has passed its own wait.  Drains of one
+                // buffer pass in order (GEMM2 of g needs the drain of g - 2), so a
+                // per-(quadrant, buffer) count orders them; it almost never spins.
+                volatile uint32_t* tok = drain_passed + q * 2 + (g & 1);
+                while (*tok < (g >> 1)) {
+                }
                 ptx::mbar_wait(&o_full[g & 1], (g >> 1) & 1);
-                FKDE_TRACE(4, it_s);
+                __syncwarp();
+                if (lane == 0) *tok = (g >> 1) + 1;
                 ptx::tc_fence_after();
                 ptx::tmem_ld16(to, od);
                 ptx::tmem_ld1(to + 16, os_);
                 ptx::tmem_ld16(to + 32, ol);
                 ptx::tmem_ld_wait();
-                FKDE_TRACE(5, it_s);
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&o_empty[g & 1]);
@@ -378,64 +405,73 @@ __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kerne
                 }
             };
             // this warp's first own tile and its S buffer / phase
-            int rel = (par - static_cast<int>(it_s)) & 1;
-            uint32_t sidx = it_s + rel;
+            int rel = par - static_cast<int>(it_s % NP);
+            if (rel < 0) rel += NP;
+            const uint32_t sidx = it_s + rel;
             uint32_t sb = sidx % Cfg::kSBuf, ph = (sidx / Cfg::kSBuf) & 1;
-            const int diag_rel = args.diag_tile0 >= 0 ? args.diag_tile0 + rt - ct0 : -1;
-            for (; rel < len; rel += 2) {
+            // score: global index of this lane's row minus the unit's first
+            // column; the row's self pair sits at column jd - rel * kNCol of
+            // tile rel (masked where that lies in [0, kNCol))
+            const long long jd0 = args.diag_row0 >= 0
+                                      ? args.diag_row0 + (long long)rt * kTileRows + r - (long long)ct0 * Cfg::kNCol
+                                      : -(1ll << 40);
+            // tiles of this unit the row tile's diagonal crosses: [drel_lo, drel_hi]
+            // (floor division; empty when the pass has no diagonal)
+            const long long drow0 = jd0 - r;
+            auto fdiv = [](long long a) {
+                return a >= 0 ? a / Cfg::kNCol : -((-a + Cfg::kNCol - 1) / Cfg::kNCol);
+            };
+            const bool has_diag = args.diag_row0 >= 0;
+            const int drel_lo = has_diag ? static_cast<int>(fdiv(drow0)) : INT_MAX;
+            const int drel_hi = has_diag ? static_cast<int>(fdiv(drow0 + kTileRows - 1)) : -1;
+            for (; rel < len; rel += NP) {
                 FKDE_TRACE(0, it_s + rel);
                 ptx::mbar_wait(&s_full[sb], ph);
                 FKDE_TRACE(1, it_s + rel);
                 ptx::tc_fence_after();
-                const uint32_t ts = lane_addr + sb * 128;
+                const uint32_t ts = lane_addr + sb * Cfg::kNCol;
                 const float2 dsc2 = make_float2(dsc, dsc);
                 if constexpr (kScore) {
-                    const bool diag = rel == diag_rel;
+                    const int jdiag = (rel >= drel_lo && rel <= drel_hi)
+                                          ? static_cast<int>(jd0 - (long long)rel * Cfg::kNCol)
+                                          : -1;   // this row's diagonal column (if in this tile)
                     const float2 off2 = make_float2(kPScaleF, kPScaleF);
                     const float2 neg1 = make_float2(-1.f, -1.f);
 #pragma unroll 1
-                    for (int h2 = 0; h2 < 2; ++h2) {
-                        uint32_t v0[32], v1[32];
-                        ptx::tmem_ld32(ts + h2 * 64, v0);
-                        ptx::tmem_ld32(ts + h2 * 64 + 32, v1);
+                    for (int ch = 0; ch < Cfg::kNCol / 32; ++ch) {
+                        uint32_t v[32];
+                        ptx::tmem_ld32(ts + ch * 32, v);
                         ptx::tmem_ld_wait();
-                        if (diag) {
-                            const int jj = r - h2 * 64;   // this row's diagonal column
+                        if (__any_sync(0xffffffffu, jdiag >= 0)) {
 #pragma unroll
-                            for (int c = 0; c < 32; ++c) {   // -inf -> phi = 0
-                                v0[c] = ptx::sel_eq(v0[c], c, jj, 0xFF800000u);
-                                v1[c] = ptx::sel_eq(v1[c], c + 32, jj, 0xFF800000u);
-                            }
+                            for (int c = 0; c < 32; ++c)    // -inf -> phi = 0
+                                v[c] = ptx::sel_eq(v[c], c + ch * 32, jdiag, 0xFF800000u);
                         }
                         // phi' = phi * 2^15 split exactly into fp16 hi + lo: hi keeps
                         // the top 11 significant bits (mask), lo = phi' - hi (exact),
                         // both convert to fp16 exactly / to nearest.  (S may exceed 0
                         // by rounding for coincident points: phi' <= 2^15 (1 + 1e-5),
-                        // well inside fp16, so no clamp.)  Column chunk c (32 S
-                        // columns) is overwritten by its own P: hi words in its
-                        // first 16 columns, lo words in the next 16.
+                        // well inside fp16, so no clamp.)  The chunk's 32 S columns
+                        // are overwritten by its own P: hi words in the first 16
+                        // columns, lo words in the next 16.
+                        uint32_t hi_w[16], lo_w[16];
 #pragma unroll
-                        for (int cc = 0; cc < 2; ++cc) {
-                            uint32_t hi_w[16], lo_w[16];
-#pragma unroll
-                            for (int w = 0; w < 16; ++w) {
-                                const uint32_t ra = cc == 0 ? v0[2 * w] : v1[2 * w];
-                                const uint32_t rb = cc == 0 ? v0[2 * w + 1] : v1[2 * w + 1];
-                                const float2 t = ptx::ffma2(
-                                    make_float2(__uint_as_float(ra), __uint_as_float(rb)), dsc2, off2);
-                                const float2 p = ((kPolyMask >> w) & 1)
-                                                     ? ptx::ex2_poly2(t)
-                                                     : make_float2(ptx::ex2(t.x), ptx::ex2(t.y));
-                                const float2 h = make_float2(
-                                    __uint_as_float(__float_as_uint(p.x) & 0xFFFFE000u),
-                                    __uint_as_float(__float_as_uint(p.y) & 0xFFFFE000u));
-                                const float2 l = ptx::ffma2(h, neg1, p);
-                                hi_w[w] = ptx::cvt_f16x2(h.x, h.y);
-                                lo_w[w] = ptx::cvt_f16x2(l.x, l.y);
-                            }
-                            ptx::tmem_st16(ts + h2 * 64 + cc * 32, hi_w);
-                            ptx::tmem_st16(ts + h2 * 64 + cc * 32 + 16, lo_w);
+                        for (int w = 0; w < 16; ++w) {
+                            const float2 t = ptx::ffma2(
+                                make_float2(__uint_as_float(v[2 * w]), __uint_as_float(v[2 * w + 1])),
+                                dsc2, off2);
+                            const float2 p = ((kPolyMask >> w) & 1)
+                                                 ? ptx::ex2_poly2(t)
+                                                 : make_float2(ptx::ex2(t.x), ptx::ex2(t.y));
+                            const float2 h = make_float2(
+                                __uint_as_float(__float_as_uint(p.x) & 0xFFFFE000u),
+                                __uint_as_float(__float_as_uint(p.y) & 0xFFFFE000u));
+                            const float2 l = ptx::ffma2(h, neg1, p);
+                            hi_w[w] = ptx::cvt_f16x2(h.x, h.y);
+                            lo_w[w] = ptx::cvt_f16x2(l.x, l.y);
                         }
+                        ptx::tmem_st16(ts + ch * 32, hi_w);
+                        ptx::tmem_st16(ts + ch * 32 + 16, lo_w);
                     }
                     FKDE_TRACE(7, it_s + rel);
                     ptx::tmem_st_wait();
@@ -443,31 +479,27 @@ __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kerne
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(&p_full[sb]);
                     FKDE_TRACE(2, it_s + rel);
-                    if (rel >= drain_at) {
-                        drain(j);
-                        j += 2;
-                        drain_at = j < nsub ? min((j + 1) << lf, len) + 1 : INT_MAX;
+                    // drain the sub-unit whose last tile is rel - 2 (if any)
+                    if (rel >= 2 && ((rel - 2) & fmask) == fmask) {
+                        drain((rel - 2) >> lf);
                         FKDE_TRACE(3, it_s + rel);
                     }
                 } else {
                     // (phi <= 1 up to the expansion's rounding: no clamp needed)
 #pragma unroll 1
-                    for (int h2 = 0; h2 < 2; ++h2) {
-                        uint32_t v0[32], v1[32];
-                        ptx::tmem_ld32(ts + h2 * 64, v0);
-                        ptx::tmem_ld32(ts + h2 * 64 + 32, v1);
+                    for (int ch = 0; ch < 4; ++ch) {
+                        uint32_t v[32];
+                        ptx::tmem_ld32(ts + ch * 32, v);
                         ptx::tmem_ld_wait();
-                        if (h2 == 1) {
+                        if (ch == 3) {
                             ptx::tc_fence_before();
                             __syncwarp();
                             if (lane == 0) ptx::mbar_arrive(&s_empty[sb]);
                         }
 #pragma unroll
-                        for (int c = 0; c < 64; c += 2) {
-                            const uint32_t ra = c < 32 ? v0[c] : v1[c - 32];
-                            const uint32_t rb = c < 32 ? v0[c + 1] : v1[c + 1 - 32];
+                        for (int c = 0; c < 32; c += 2) {
                             const float2 dd = ptx::fmul2(
-                                make_float2(__uint_as_float(ra), __uint_as_float(rb)), dsc2);
+                                make_float2(__uint_as_float(v[c]), __uint_as_float(v[c + 1])), dsc2);
                             const float2 p = make_float2(ptx::ex2(dd.x), ptx::ex2(dd.y));
                             const int a = (c >> 1) & 1;
                             acc2[a] = ptx::fadd2(acc2[a], p);
@@ -475,8 +507,8 @@ __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kerne
                         }
                     }
                 }
-                // next own tile: buffer index advances by 2 (mod kSBuf)
-                sb += 2;
+                // next own tile: buffer index advances by NP (mod kSBuf)
+                sb += NP;
                 if (sb >= Cfg::kSBuf) {
                     sb -= Cfg::kSBuf;
                     ph ^= 1;
@@ -484,29 +516,46 @@ __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kerne
             }
             const size_t row = static_cast<size_t>(rt) * kTileRows + r;
             if constexpr (kScore) {
-                for (; j < nsub; j += 2) drain(j);
-                // the two parities drained disjoint sub-units: merge them through
-                // shared memory (named barrier over the 8 epilogue warps) and
+                // sub-units ending at the last two tiles have their drain tile
+                // beyond the unit: drained here, in order, by the owner of the
+                // unit's last tile
+                if ((it_s + len - 1) % NP == static_cast<uint32_t>(par)) {
+#pragma unroll 1
+                    for (int last = len - 2; last < len; ++last) {
+                        if (last < 0) continue;
+                        if ((last & fmask) == fmask || last == len - 1) drain(last >> lf);
+                    }
+                }
+                // the kNP phases drained disjoint sub-units: merge them through
+                // shared memory (named barrier over the epilogue warps) and
                 // write one fp64 partial per (split, row)
-                double* acc = reinterpret_cast<double*>(smem + Cfg::kOffAcc) +
-                              (par * 128 + r) * Cfg::kAccStride;
+                double* accs = reinterpret_cast<double*>(smem + Cfg::kOffAcc);
+                double* acc = accs + (par * 128 + r) * Cfg::kAccStride;
 #pragma unroll
                 for (int c = 0; c <= kMaxDim; ++c)
                     acc[c] = static_cast<double>(ahi[c]) + static_cast<double>(alo[c]);
-                asm volatile("bar.sync 1, 256;" ::: "memory");
+                ptx::named_bar_sync(1, NP * 128);
                 if (par == 0) {
-                    const double* other = acc + 128 * Cfg::kAccStride;
+                    double tot[kMaxDim + 1];
+#pragma unroll
+                    for (int c = 0; c <= kMaxDim; ++c) tot[c] = acc[c];
+#pragma unroll
+                    for (int o = 1; o < NP; ++o) {
+                        const double* other = accs + (o * 128 + r) * Cfg::kAccStride;
+#pragma unroll
+                        for (int c = 0; c <= kMaxDim; ++c) tot[c] += other[c];
+                    }
                     const size_t idx = static_cast<size_t>(sp) * args.rows_pad + row;
-                    args.dpart0[idx] = acc[kMaxDim] + other[kMaxDim];
+                    args.dpart0[idx] = tot[kMaxDim];
                     double2* t = reinterpret_cast<double2*>(args.dpart1 + idx * kMaxDim);
 #pragma unroll
-                    for (int w = 0; w < kMaxDim / 2; ++w)
-                        t[w] = make_double2(acc[2 * w] + other[2 * w], acc[2 * w + 1] + other[2 * w + 1]);
+                    for (int w = 0; w < kMaxDim / 2; ++w) t[w] = make_double2(tot[2 * w], tot[2 * w + 1]);
                 }
-                asm volatile("bar.sync 1, 256;" ::: "memory");   // acc is rewritten next unit
-                it_u += nsub;
+                ptx::named_bar_sync(1, NP * 128);   // the merge area is rewritten next unit
+                it_u += (len + fmask) >> lf;
             } else {
-                const size_t idx = static_cast<size_t>(sp * 2 + par) * args.rows_pad + row;
+                // the kNP phases hold disjoint column subsets of this unit
+                const size_t idx = static_cast<size_t>(sp * NP + par) * args.rows_pad + row;
                 args.part0[idx] = (acc2[0].x + acc2[0].y) + (acc2[1].x + acc2[1].y);
                 if constexpr (MODE == kModeLaplace)
                     args.part1[idx] = (accl2[0].x + accl2[0].y) + (accl2[1].x + accl2[1].y);

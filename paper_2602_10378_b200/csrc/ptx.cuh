@@ -42,11 +42,15 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
 // that would deadlock traps (a reported launch error) instead of hanging the
 // device until the watchdog.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    // bounded: a protocol bug traps after ~2^33 cycles (~4 s) instead of hanging
     uint32_t spins = 0;
+    long long t0 = 0;
     while (!mbar_try_wait(bar, parity)) {
-        if (++spins > (1u << 26)) {
-            printf("fkde_b200: mbarrier wait timeout (block %d thread %d)\n", blockIdx.x,
-                   threadIdx.x);
+        if (++spins == 1024) {
+            t0 = clock64();
+        } else if (spins > 1024 && (spins & 1023) == 0 && clock64() - t0 > (1ll << 33)) {
+            printf("fkde_b200: mbarrier wait timeout (block %d thread %d bar 0x%x parity %u)\n",
+                   blockIdx.x, threadIdx.x, smem_u32(bar), parity);
             __trap();
         }
     }
@@ -301,6 +305,11 @@ __device__ __forceinline__ float2 ex2_poly2(float2 t) {
     // (bits(rm) << 23) == rint(t) << 23 (the magic's own bits shift out)
     return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(rm.x) << 23)),
                        __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(rm.y) << 23)));
+}
+
+// named barrier over `count` threads (multiple of 32)
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
 // v = (a == b) ? x : v as a predicated select (keeps the compiler from

@@ -210,7 +210,7 @@ def test_flush_interval_and_ragged_units(port):
 
 
 def test_flush_interval_must_be_power_of_two(ctx):
-    for bad in (0, 3, 6, (1 << 20) + 1):
+    for bad in (-1, 3, 6, (1 << 20) + 1):
         with pytest.raises(fk.InvalidArgumentError):
             ctx.set_option(N.OPT_FLUSH_TILES, bad)
 
