@@ -124,12 +124,14 @@ struct TcConfig {
     static constexpr uint32_t kN2 = 48;       // GEMM2 N
 };
 
-// score epilogue: pairs w (of the 16 per 32-column chunk) whose exponentials
-// are evaluated on the FMA pipe (ptx::ex2_poly2) instead of MUFU
-#ifndef FKDE_POLY_MASK
-#define FKDE_POLY_MASK 0x0000
+// score epilogue: how phi' is split into fp16 hi + lo.  0: hi = phi' with the
+// low 13 mantissa bits masked (2 LOP3 per pair, ALU pipe); 1: Veltkamp split
+// (t = phi' (2^13 + 1), hi = t - (t - phi'), FMA pipe only; more accurate --
+// config-1 score error 1.6e-4 vs 2.2e-4 -- but 7 % slower: the epilogue is
+// sensitive to every added instruction, tools/ubench_pipe.cu)
+#ifndef FKDE_SPLIT
+#define FKDE_SPLIT 0
 #endif
-constexpr uint32_t kPolyMask = FKDE_POLY_MASK;
 
 template <int MODE>
 __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kernel(PairArgs args) {
@@ -370,7 +372,7 @@ __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kerne
             // drained by the warp owning the tile two after its last one, right
             // after that warp's P store (GEMM2 of the sub-unit has completed by
             // then, so the o_full wait rarely stalls), or at the unit end.
-            auto drain = [&](int j) {
+            auto drain = [&](int j, int tt) {
                 const uint32_t g = it_u + j;
                 uint32_t od[16], ol[16], os_;
                 const uint32_t to = lane_addr + Cfg::kTmemO + (g & 1) * 64;
@@ -383,6 +385,7 @@ __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kerne
                 while (*tok < (g >> 1)) {
                 }
                 ptx::mbar_wait(&o_full[g & 1], (g >> 1) & 1);
+                FKDE_TRACE(4, tt);
                 __syncwarp();
                 if (lane == 0) *tok = (g >> 1) + 1;
                 ptx::tc_fence_after();
@@ -390,6 +393,7 @@ __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kerne
                 ptx::tmem_ld1(to + 16, os_);
                 ptx::tmem_ld16(to + 32, ol);
                 ptx::tmem_ld_wait();
+                FKDE_TRACE(5, tt);
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&o_empty[g & 1]);
@@ -437,11 +441,13 @@ __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kerne
                                           : -1;   // this row's diagonal column (if in this tile)
                     const float2 off2 = make_float2(kPScaleF, kPScaleF);
                     const float2 neg1 = make_float2(-1.f, -1.f);
+                    const float2 vk2 = make_float2(8193.f, 8193.f);   // 2^13 + 1
 #pragma unroll 1
                     for (int ch = 0; ch < Cfg::kNCol / 32; ++ch) {
                         uint32_t v[32];
                         ptx::tmem_ld32(ts + ch * 32, v);
                         ptx::tmem_ld_wait();
+                        if (ch == 0) FKDE_TRACE(6, it_s + rel);
                         if (__any_sync(0xffffffffu, jdiag >= 0)) {
 #pragma unroll
                             for (int c = 0; c < 32; ++c)    // -inf -> phi = 0
@@ -460,12 +466,15 @@ __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kerne
                             const float2 t = ptx::ffma2(
                                 make_float2(__uint_as_float(v[2 * w]), __uint_as_float(v[2 * w + 1])),
                                 dsc2, off2);
-                            const float2 p = ((kPolyMask >> w) & 1)
-                                                 ? ptx::ex2_poly2(t)
-                                                 : make_float2(ptx::ex2(t.x), ptx::ex2(t.y));
+                            const float2 p = make_float2(ptx::ex2(t.x), ptx::ex2(t.y));
+#if FKDE_SPLIT == 1
+                            const float2 vt = ptx::fmul2(p, vk2);
+                            const float2 h = ptx::fadd2(vt, ptx::ffma2(vt, neg1, p));   // t + (p - t)
+#else
                             const float2 h = make_float2(
                                 __uint_as_float(__float_as_uint(p.x) & 0xFFFFE000u),
                                 __uint_as_float(__float_as_uint(p.y) & 0xFFFFE000u));
+#endif
                             const float2 l = ptx::ffma2(h, neg1, p);
                             hi_w[w] = ptx::cvt_f16x2(h.x, h.y);
                             lo_w[w] = ptx::cvt_f16x2(l.x, l.y);
@@ -481,7 +490,7 @@ __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kerne
                     FKDE_TRACE(2, it_s + rel);
                     // drain the sub-unit whose last tile is rel - 2 (if any)
                     if (rel >= 2 && ((rel - 2) & fmask) == fmask) {
-                        drain((rel - 2) >> lf);
+                        drain((rel - 2) >> lf, it_s + rel);
                         FKDE_TRACE(3, it_s + rel);
                     }
                 } else {
@@ -523,7 +532,7 @@ __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kerne
 #pragma unroll 1
                     for (int last = len - 2; last < len; ++last) {
                         if (last < 0) continue;
-                        if ((last & fmask) == fmask || last == len - 1) drain(last >> lf);
+                        if ((last & fmask) == fmask || last == len - 1) drain(last >> lf, 255);
                     }
                 }
                 // the kNP phases drained disjoint sub-units: merge them through
