@@ -11,6 +11,10 @@
 //   fkde::{gaussian_kernel, laplace_corrected_kernel, gaussian_norm_const} (kernels.hpp)
 //   fkde::Rng / mix64 (rng.hpp), fkde::bench::sample_mixture (mixture.hpp:25)
 //   fkde::{mean_stddev, silverman_bandwidth, sdkde_bandwidth, silverman_prefactor}
+//   fkde::io::{write_samples_bin, write_samples_csv, write_values} (io.hpp) and
+//   fkde::bench::{load_mixture, mixture_hash, mixture_pdf} (mixture.hpp),
+//   fkde::perfmodel::{flops_nd, flops_1d, bytes_nd, bytes_1d, bytes_linear,
+//   intensity_asymptotic} (perfmodel.hpp) -- the §8f rows' file formats and models
 #include <cstring>
 #include <exception>
 #include <thread>
@@ -18,6 +22,8 @@
 
 #include "fkde/bandwidth.hpp"
 #include "fkde/errors.hpp"
+#include "fkde/io.hpp"
+#include "fkde/perfmodel.hpp"
 #include "fkde/kernels.hpp"
 #include "fkde/mixture.hpp"
 #include "fkde/oracle.hpp"
@@ -193,5 +199,78 @@ int fkr_sdkde_naive(const double* train, std::size_t n, const double* queries, s
         return map_exception(err_index);
     }
 }
+
+// ---- §8f rows: file formats, mixture config, perf model ----------------------
+int fkr_write_samples_bin(const char* path, const double* v, std::size_t n, std::size_t d) {
+    try {
+        io::write_samples_bin(make_set(v, n, d), path);
+        return 0;
+    } catch (...) {
+        return map_exception(nullptr);
+    }
+}
+int fkr_write_samples_csv(const char* path, const double* v, std::size_t n, std::size_t d) {
+    try {
+        io::write_samples_csv(make_set(v, n, d), path);
+        return 0;
+    } catch (...) {
+        return map_exception(nullptr);
+    }
+}
+int fkr_write_values(const char* path, const double* v, std::size_t m, const char* format) {
+    try {
+        io::write_values(std::vector<double>(v, v + m), path, format);
+        return 0;
+    } catch (...) {
+        return map_exception(nullptr);
+    }
+}
+// n, d of a sample file (0 on error); values copied when out != nullptr
+int fkr_read_samples(const char* path, double* out, std::size_t cap, std::size_t* n, std::size_t* d) {
+    try {
+        const SampleSet s = io::read_samples(path);
+        *n = s.n;
+        *d = s.d;
+        if (out && cap >= s.values.size()) std::memcpy(out, s.values.data(), s.values.size() * 8);
+        return 0;
+    } catch (const IoError&) {
+        return 8;
+    } catch (...) {
+        return map_exception(nullptr);
+    }
+}
+int fkr_read_values(const char* path, double* out, std::size_t cap, std::size_t* m) {
+    try {
+        const std::vector<double> v = io::read_values(path);
+        *m = v.size();
+        if (out && cap >= v.size()) std::memcpy(out, v.data(), v.size() * 8);
+        return 0;
+    } catch (const IoError&) {
+        return 8;
+    } catch (...) {
+        return map_exception(nullptr);
+    }
+}
+std::uint64_t fkr_mixture_hash(const char* config_path) {
+    return bench::mixture_hash(bench::load_mixture(config_path));
+}
+int fkr_mixture_pdf(const char* config_path, const double* x, std::size_t n, double* out) {
+    try {
+        const auto mix = bench::load_mixture(config_path);
+        const auto v = bench::mixture_pdf(mix, make_set(x, n, mix.dim()));
+        std::memcpy(out, v.data(), n * 8);
+        return 0;
+    } catch (...) {
+        return map_exception(nullptr);
+    }
+}
+double fkr_flops_nd(std::size_t d, std::size_t k) { return perfmodel::flops_nd(d, k); }
+double fkr_flops_1d(std::size_t k) { return perfmodel::flops_1d(k); }
+double fkr_bytes_nd(std::size_t d, std::size_t k, std::size_t tm, std::size_t tn) {
+    return perfmodel::bytes_nd(d, k, tm, tn);
+}
+double fkr_bytes_1d(std::size_t k) { return perfmodel::bytes_1d(k); }
+double fkr_bytes_linear(std::size_t d, std::size_t k) { return perfmodel::bytes_linear(d, k); }
+double fkr_intensity_asymptotic(std::size_t d) { return perfmodel::intensity_asymptotic(d); }
 
 }  // extern "C"

@@ -17,6 +17,7 @@ from .types import (Bandwidth, DegenerateDataError, DensityResult, DeviceError,
                     ScoreUnderflowError, UnsupportedDimensionError, engine_from_string,
                     method_from_string, to_string)
 from . import engine
+from . import io
 from .engine import (Context, EngineOptions, ScoreAccumulator, TilePlan, default_context,
                      kde_flash, pairwise_sq_dists_block, score_accumulate, score_flash,
                      sdkde_flash)

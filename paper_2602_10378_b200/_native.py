@@ -47,6 +47,14 @@ HOST_SYMBOLS = (
     "fkde_host_sdkde_bandwidth",
 )
 
+IO_SYMBOLS = (
+    "fkde_io_read_samples", "fkde_io_free", "fkde_io_write_samples_bin",
+    "fkde_io_write_samples_csv", "fkde_io_write_values", "fkde_io_read_values",
+    "fkde_io_last_error",
+)
+# fkde_io_status
+IO_OK, IO_ERROR, IO_INVALID_ARGUMENT = 0, 1, 2
+
 _lib = None
 
 _dp = ctypes.POINTER(ctypes.c_double)
@@ -99,6 +107,16 @@ def _declare(lib):
     lib.fkde_host_silverman_prefactor.restype = ctypes.c_double
     lib.fkde_host_sdkde_bandwidth.argtypes = [_dp, _sz, _sz, ctypes.c_double]
     lib.fkde_host_sdkde_bandwidth.restype = ctypes.c_double
+    ip = ctypes.POINTER(ctypes.c_int)
+    lib.fkde_io_read_samples.argtypes = [ctypes.c_char_p, ctypes.POINTER(_dp), _szp, _szp, ip]
+    lib.fkde_io_free.argtypes = [_dp, ctypes.c_int]
+    lib.fkde_io_free.restype = None
+    lib.fkde_io_write_samples_bin.argtypes = [ctypes.c_char_p, _dp, _sz, _sz]
+    lib.fkde_io_write_samples_csv.argtypes = [ctypes.c_char_p, _dp, _sz, _sz]
+    lib.fkde_io_write_values.argtypes = [ctypes.c_char_p, _dp, _sz, ctypes.c_char_p]
+    lib.fkde_io_read_values.argtypes = [ctypes.c_char_p, ctypes.POINTER(_dp), _szp]
+    lib.fkde_io_last_error.argtypes = []
+    lib.fkde_io_last_error.restype = ctypes.c_char_p
     return lib
 
 

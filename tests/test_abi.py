@@ -16,9 +16,9 @@ import paper_2602_10378_b200 as fk
 from paper_2602_10378_b200 import _native as N
 
 
-def header_symbols():
-    src = open(os.path.join(ROOT, "include", "fkde_gpu.h")).read()
-    return sorted(set(re.findall(r"\b(fkde_(?:gpu|host)_\w+)\s*\(", src)))
+def header_symbols(name="fkde_gpu.h"):
+    src = open(os.path.join(ROOT, "include", name)).read()
+    return sorted(set(re.findall(r"\b(fkde_(?:gpu|host|io)_\w+)\s*\(", src)))
 
 
 def test_library_exports_every_declared_symbol():
@@ -28,6 +28,22 @@ def test_library_exports_every_declared_symbol():
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) == set(N.EXPORTED_SYMBOLS) | set(N.HOST_SYMBOLS)
+
+
+def test_library_exports_every_io_symbol():
+    lib = N.load()
+    syms = header_symbols("fkde_io.h")
+    assert set(syms) == set(N.IO_SYMBOLS)
+    for s in syms:
+        assert hasattr(lib, s), s
+
+
+def test_every_header_is_covered():
+    # every include/*.h entry point is in one of the checked symbol lists
+    listed = set(N.EXPORTED_SYMBOLS) | set(N.HOST_SYMBOLS) | set(N.IO_SYMBOLS)
+    for name in os.listdir(os.path.join(ROOT, "include")):
+        if name.endswith(".h"):
+            assert set(header_symbols(name)) <= listed, name
 
 
 def test_library_is_sm100a_only():
