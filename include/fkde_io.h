@@ -46,6 +46,9 @@ typedef enum fkde_io_status {
  * without a CUDA driver); release with fkde_io_free(*out, *pinned). */
 int fkde_io_read_samples(const char* path, double** out, size_t* n, size_t* d, int* pinned);
 void fkde_io_free(double* p, int pinned);
+/* count doubles of host memory, page-locked when *pinned (in: requested,
+ * out: granted); NULL when out of memory.  Release with fkde_io_free. */
+double* fkde_io_alloc(size_t count, int* pinned);
 
 int fkde_io_write_samples_bin(const char* path, const double* values, size_t n, size_t d);
 int fkde_io_write_samples_csv(const char* path, const double* values, size_t n, size_t d);

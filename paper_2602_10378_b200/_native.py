@@ -48,7 +48,7 @@ HOST_SYMBOLS = (
 )
 
 IO_SYMBOLS = (
-    "fkde_io_read_samples", "fkde_io_free", "fkde_io_write_samples_bin",
+    "fkde_io_read_samples", "fkde_io_free", "fkde_io_alloc", "fkde_io_write_samples_bin",
     "fkde_io_write_samples_csv", "fkde_io_write_values", "fkde_io_read_values",
     "fkde_io_last_error",
 )
@@ -111,6 +111,8 @@ def _declare(lib):
     lib.fkde_io_read_samples.argtypes = [ctypes.c_char_p, ctypes.POINTER(_dp), _szp, _szp, ip]
     lib.fkde_io_free.argtypes = [_dp, ctypes.c_int]
     lib.fkde_io_free.restype = None
+    lib.fkde_io_alloc.argtypes = [_sz, ip]
+    lib.fkde_io_alloc.restype = _dp
     lib.fkde_io_write_samples_bin.argtypes = [ctypes.c_char_p, _dp, _sz, _sz]
     lib.fkde_io_write_samples_csv.argtypes = [ctypes.c_char_p, _dp, _sz, _sz]
     lib.fkde_io_write_values.argtypes = [ctypes.c_char_p, _dp, _sz, ctypes.c_char_p]

@@ -145,10 +145,9 @@ void member(const std::string& v, const std::vector<std::string>& allowed, const
 }
 
 // ---------------------------------------------------------------- samples
-struct Samples {  // pinned host buffer from fkde_io_read_samples, or owned vector
+struct Samples {  // host buffer from fkde_io_read_samples / fkde_io_alloc (pinned when possible)
     double* p = nullptr;
     bool pinned = false;
-    std::vector<double> own;
     size_t n = 0, d = 0;
     Samples() = default;
     Samples(const Samples&) = delete;
@@ -157,15 +156,11 @@ struct Samples {  // pinned host buffer from fkde_io_read_samples, or owned vect
     Samples& operator=(Samples&& o) noexcept {
         std::swap(p, o.p);
         std::swap(pinned, o.pinned);
-        std::swap(own, o.own);
         std::swap(n, o.n);
         std::swap(d, o.d);
-        if (!p && !own.empty()) p = own.data();
         return *this;
     }
-    ~Samples() {
-        if (own.empty()) fkde_io_free(p, pinned ? 1 : 0);
-    }
+    ~Samples() { fkde_io_free(p, pinned ? 1 : 0); }
     const double* data() const { return p; }
 };
 
@@ -178,15 +173,6 @@ Samples read_samples(const std::string& path) {
     if (rc != FKDE_IO_OK) throw IoError(fkde_io_last_error());
     s.p = p;
     s.pinned = pinned != 0;
-    return s;
-}
-
-Samples owned(std::vector<double> v, size_t n, size_t d) {
-    Samples s;
-    s.own = std::move(v);
-    s.p = s.own.data();
-    s.n = n;
-    s.d = d;
     return s;
 }
 
@@ -242,12 +228,18 @@ struct Mixture {
         }
         return h;
     }
+    // draws into page-locked memory (the engine's H2D copy is then one DMA)
     Samples sample(size_t n, uint64_t seed) const {
-        std::vector<double> v(n * d);
-        if (fkde_host_sample_mixture(weights.data(), means.data(), sigmas.data(), k(), d, n, seed,
-                                     v.data()) != 0)
+        Samples s;
+        int pinned = 1;
+        s.p = fkde_io_alloc(n * d, &pinned);
+        if (!s.p) throw std::bad_alloc();
+        s.pinned = pinned != 0;
+        s.n = n;
+        s.d = d;
+        if (fkde_host_sample_mixture(weights.data(), means.data(), sigmas.data(), k(), d, n, seed, s.p) != 0)
             throw NumericError("sample_mixture: invalid mixture");
-        return owned(std::move(v), n, d);
+        return s;
     }
     std::vector<double> pdf(const double* x, size_t n) const {  // mixture.cpp:68-95
         std::vector<double> out(n, 0.0), norm(k());

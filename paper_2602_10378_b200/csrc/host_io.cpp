@@ -203,6 +203,16 @@ int fkde_io_read_samples(const char* path, double** out, size_t* n, size_t* d, i
     });
 }
 
+double* fkde_io_alloc(size_t count, int* pinned) {
+    if (!pinned) return nullptr;
+    *pinned = *pinned ? 1 : 0;
+    try {
+        return alloc_values(count, pinned);
+    } catch (...) {
+        return nullptr;
+    }
+}
+
 void fkde_io_free(double* p, int pinned) {
     if (!p) return;
     if (pinned) cudaFreeHost(p);
