@@ -33,7 +33,12 @@ METRICS = [
     ("launch__grid_size", "grid"),
     ("launch__block_size", "block"),
     ("smsp__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue slots busy %"),
+    ("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", "ALU inst %"),
+    ("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "FMA inst %"),
 ]
+STALL_PREFIX = "smsp__average_warps_issue_stalled_"
+STALL_SUFFIX = "_per_issue_active.ratio"
 
 
 def raw(rep):
@@ -105,6 +110,14 @@ def main():
                 if key in k:
                     md.append(f"| {label} (`{key}`) | {k[key]} {k['_units'].get(key, '')} |")
             md.append("")
+            st = sorted(((fnum(v) or 0.0, key[len(STALL_PREFIX):-len(STALL_SUFFIX)])
+                         for key, v in k.items()
+                         if key.startswith(STALL_PREFIX) and key.endswith(STALL_SUFFIX)), reverse=True)
+            if st:
+                md.append("Warp stall reasons (warps stalled per issued instruction):")
+                md.append("")
+                md.append(", ".join(f"{nm} {v:.2f}" for v, nm in st[:9] if v > 0.005))
+                md.append("")
             samples = sp.get(norm(name), [])
             tot = sum(s for s, _ in samples) or 1
             top = sorted(samples, reverse=True)[:8]
@@ -115,13 +128,14 @@ def main():
                     md.append(f"- {100.0 * s / tot:5.1f}%  `{ins}`")
                 md.append("")
             if "pairwise_tc_kernel<0>" in norm(name) and "1m" in os.path.basename(rep):
+                scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
                 rd = fnum(k.get("dram__bytes_read.sum"))
                 wr = fnum(k.get("dram__bytes_write.sum"))
-                unit = k["_units"].get("dram__bytes_read.sum", "byte")
-                scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
                 if rd is not None and wr is not None:
+                    rd *= scale.get(k["_units"].get("dram__bytes_read.sum", "byte"), 1)
+                    wr *= scale.get(k["_units"].get("dram__bytes_write.sum", "byte"), 1)
                     score_json = {"kernel": name, "report": os.path.basename(rep),
-                                  "dram_bytes_per_launch": (rd + wr) * scale,
+                                  "dram_bytes_per_launch": rd + wr,
                                   "duration": k.get("gpu__time_duration.sum"),
                                   "duration_unit": k["_units"].get("gpu__time_duration.sum")}
     if a.launches and os.path.exists(a.launches):
