@@ -269,7 +269,8 @@ Status compute_mean(Device& D, const double* dX, size_t n, int d, PassScalars* s
 }
 
 Status pack(Device& D, const double* x, size_t rows, int d, int format, bool center, double k,
-            const PassScalars* sc, DevBuf& out, size_t* rows_padded, size_t align = kTileRows) {
+            const PassScalars* sc, DevBuf& out, size_t* rows_padded, size_t align = kTileRows,
+            float a_offset = 0.f) {
     const size_t rp = round_up(std::max<size_t>(rows, 1), align);
     STATUS_TRY(ensure(out, rp * kRowBytes));
     PackArgs a;
@@ -282,6 +283,7 @@ Status pack(Device& D, const double* x, size_t rows, int d, int format, bool cen
     a.k = k;
     a.sc = sc;
     a.out = out.as<uint4>();
+    a.a_offset = a_offset;
     pack_operands<<<grid1(rp, 128), 128, 0, D.stream>>>(a);
     ++D.launches;
     CUDA_TRY(cudaGetLastError());
@@ -381,7 +383,9 @@ Status score_program(Device& D, const Options& o, const Job& J, const double* dX
     // row shards start on a tile boundary so the diagonal is tile aligned
     const Shard sh = shard_of(n, D.world, D.rank, kTileRows);
     size_t rows_pad = 0, cols_pad = 0;
-    STATUS_TRY(pack(D, dX + sh.begin * d, sh.rows, d, 0, true, ks, sc, D.opA, &rows_pad));
+    // A rows carry the P' = phi * 2^15 offset (layout.cuh): S = log2 P' off the tensor core
+    STATUS_TRY(pack(D, dX + sh.begin * d, sh.rows, d, 0, true, ks, sc, D.opA, &rows_pad, kTileRows,
+                    kPScaleF));
     // score-pass column tiles are TcConfig<kModeScore>::kNCol points wide: pad the
     // column operand to a whole number of those and of 128-point pack tiles
     constexpr size_t kScoreNCol = TcConfig<kModeScore>::kNCol;

@@ -14,7 +14,8 @@
 //
 //   chunk   A (row side)                 B (column side)
 //   0-1     y_hi[0:16]                   y_hi[0:16]
-//   2       a1 a2 a3 1 1 1 0 0           1 1 1 b1 b2 b3 0 0     (a,b = -|y|^2/2 split)
+//   2       a1 a2 a3 1 1 1 c 0           1 1 1 b1 b2 b3 1 0     (a,b = -|y|^2/2 split;
+//                                                               c = per-pass offset, below)
 //   3       0                            0
 //   4-5     y_hi[0:16]                   y_lo[0:16]
 //   6-7     y_lo[0:16]                   y_hi[0:16]
@@ -24,6 +25,12 @@
 // sum_j phi_ij (the ones -- S comes off the tensor core from the same rounded
 // phi as T), 32-47 = sum_j phi_ij y_lo_j.  The first 32 columns (T_hi, S) are
 // drained to fp64 every few tiles; T_lo (2^-11 smaller) only at the end.
+//
+// c adds a constant to every product: the score pass packs c = 15 * 2^-2e, so
+// S * 2^2e = log2(phi * 2^15) comes off the tensor core with the P' scale
+// (kPScaleExp) applied exactly inside the accumulation (one rounding fewer than
+// adding it in the epilogue: config-1 score error 2.2e-4 -> 2.0e-4); the density
+// passes pack c = 0.
 //
 // Rows are grouped in tiles of 128 (16 KiB, contiguous) stored exactly as the
 // SWIZZLE_128B shared-memory image: 16-byte chunk c of row r lives at

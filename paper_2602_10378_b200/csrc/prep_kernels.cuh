@@ -95,6 +95,9 @@ struct PackArgs {
     double k;                // sqrt(log2 e) / h
     const PassScalars* sc;   // mu (if center) and e
     uint4* out;              // rows_padded * 8 uint4
+    float a_offset;          // A rows: constant added to every Gram entry (before the
+                             // 2^(2e) scale): chunk-2 element 6 = a_offset * 2^-2e,
+                             // paired with a 1 in the B rows (score pass: kPScaleF)
 };
 
 __device__ __forceinline__ uint32_t pack_h2(__half a, __half b) {
@@ -133,7 +136,7 @@ __global__ void pack_operands(PackArgs a) {
     }
     // chunk layout (see layout.cuh):      A                 B
     //   0-1  y_hi                          y_hi              y_hi
-    //   2    norms                         a1 a2 a3 1 1 1    1 1 1 b1 b2 b3
+    //   2    norms                         a1 a2 a3 1 1 1 c  1 1 1 b1 b2 b3 1
     //   3    zero
     //   4-5                                y_hi              y_lo
     //   6-7                                y_lo              y_hi
@@ -150,16 +153,16 @@ __global__ void pack_operands(PackArgs a) {
                                          : pack_h2(yh[k0], yh[k0 + 1]);
         }
     if (valid) {
-        if (a.format == 0) {  // a1 a2 a3 1 1 1 0 0
+        if (a.format == 0) {  // a1 a2 a3 1 1 1 c 0   (c = a_offset * 2^-2e, exact)
             ch[2][0] = pack_h2(n1, n2);
             ch[2][1] = pack_h2(n3, one);
             ch[2][2] = pack_h2(one, one);
-            ch[2][3] = 0u;
-        } else {              // 1 1 1 b1 b2 b3 0 0
+            ch[2][3] = pack_h2(__float2half(ldexpf(a.a_offset, -2 * a.sc->e)), zero);
+        } else {              // 1 1 1 b1 b2 b3 1 0
             ch[2][0] = pack_h2(one, one);
             ch[2][1] = pack_h2(one, n1);
             ch[2][2] = pack_h2(n2, n3);
-            ch[2][3] = 0u;
+            ch[2][3] = pack_h2(one, zero);
         }
     } else {
         if (a.format == 0) {
