@@ -115,7 +115,7 @@ def make_inputs(n, m):
 
 
 # ---- CPU baseline (the reference oracle, bounded sample) ------------------------------
-def cpu_oracle_sample(X, Y, h, rows_score=128, rows_query=128):
+def cpu_oracle_sample(X, Y, h, rows_score=2048, rows_query=1024):
     """Times the reference's naive oracle on a row sample; returns (extrapolated
     full-workload seconds, details).  Cost is exactly linear in evaluated rows."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
