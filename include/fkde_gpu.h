@@ -72,7 +72,7 @@ enum {
                                  extended-precision register sums every k column
                                  tiles; k a power of two in [1, 2^20], or 0 for
                                  the default (~256 columns)                      */
-    FKDE_OPT_TRACE_PTR = 6    /* debug: device pointer (11*8*256 int64) receiving
+    FKDE_OPT_TRACE_PTR = 6    /* debug: device pointer (32*8*256 int64) receiving
                                  clock64 stamps of the score kernel's block 0   */
 };
 enum { FKDE_ENGINE_TC = 0, FKDE_ENGINE_SIMT = 1 };

@@ -22,12 +22,12 @@
 // The n x n kernel matrix never leaves the SM; per column tile the SMEM
 // traffic is the 16 KiB B tile read by both GEMMs and the 16 KiB A tile.
 //
-// Warp roles (320/352 threads): warp 0 = bulk-copy producer, warp 1 = TMEM
-// owner + GEMM1 issuer, warp 10 (score) = GEMM2 issuer, warps 2..9 = epilogue
-// (warp w reads TMEM lane quadrant w%4 of every other tile, parity (w-2)/4).  Pipelines (mbarriers): A tiles x2,
-// B tiles x kStages, S/P accumulators x2 (TMEM), O x1 (TMEM).  The MMA
-// thread's tcgen05 ops execute in issue order, so GEMM1(t+2) overwriting the
-// S/P buffer of tile t is ordered after GEMM2(t) reading P(t) from it.
+// Warp roles: warp 0 = bulk-copy producer, warp 1 = TMEM owner + GEMM1 issuer;
+// score pass: warp 2 = GEMM2 issuer, warps 4..7 = O drain warps (one per TMEM
+// lane quadrant), warps 8.. = epilogue; KDE: warps 2.. = epilogue.  Epilogue
+// warp w reads TMEM lane quadrant w%4 of every kNP-th tile.  Pipelines
+// (mbarriers): A tiles x2, B tiles x kStages, S/P accumulators x kSBuf (TMEM),
+// O x2 (TMEM, score).
 #pragma once
 #include <cuda_fp16.h>
 #include <climits>
@@ -81,20 +81,40 @@ struct PairArgs {
 template <int MODE>
 struct TcConfig {
     static constexpr bool kScore = MODE == kModeScore;
-    static constexpr int kStages = 8;
-    // warps: 0 producer, 1 GEMM1 issuer (+ TMEM owner), 2 .. 2+4*kNP-1
-    // epilogue (kNP warps per TMEM lane quadrant, one per SM sub-partition
-    // each), then the GEMM2 issuer (score only).  tcgen05.mma issue blocks
-    // while the tensor core is busy, so GEMM1 and GEMM2 get their own issuing
-    // warps and the tensor core never idles behind a GEMM2 that waits for P.
+    // KDE: warps 0 producer, 1 GEMM1 issuer (+ TMEM owner), 2 .. 2+4*kNP-1
+    // epilogue (kNP warps per TMEM lane quadrant, one per SM sub-partition each).
+    // SCORE: warpgroup 0 = control (0 producer, 1 GEMM1 issuer + TMEM owner,
+    // 2 GEMM2 issuer, 3 idle), warpgroups 1..kNP = epilogue.  tcgen05.mma issue
+    // blocks while the tensor core is busy, so GEMM1 and GEMM2 get their own
+    // issuing warps and the tensor core never idles behind a GEMM2 that waits for
+    // P.  The control warpgroup gives its registers to the epilogue warpgroups
+    // (setmaxnreg), which is what makes four epilogue warps per sub-partition fit.
 #ifndef FKDE_EPI_NP
 #define FKDE_EPI_NP 3
 #endif
-    static constexpr int kNP = FKDE_EPI_NP;          // epilogue warps per lane quadrant
-    static constexpr int kEpi0 = 2;
+#ifndef FKDE_SCORE_NP
+#define FKDE_SCORE_NP 3
+#endif
+#ifndef FKDE_CTRL_REGS
+#define FKDE_CTRL_REGS 56
+#endif
+    static constexpr int kNP = kScore ? FKDE_SCORE_NP : FKDE_EPI_NP;   // epilogue warps per lane quadrant
+    // score: warpgroup 1 (warps 4..7) = the O drain warps, one per lane quadrant
+    static constexpr int kCtrlEnd = kScore ? 4 : 2;
+    static constexpr int kEpi0 = kScore ? 8 : 2;
     static constexpr int kEpiEnd = kEpi0 + 4 * kNP;
-    static constexpr int kG2Warp = kEpiEnd;
-    static constexpr int kThreads = kScore ? (kG2Warp + 1) * 32 : kEpiEnd * 32;
+    static constexpr int kG2Warp = kScore ? 2 : -1;
+    static constexpr int kThreads = kEpiEnd * 32;
+    // score register split: launch at kLaunchRegs (x kThreads <= 64K, multiple of 8),
+    // control warpgroup down to kCtrlRegs, drain warpgroup stays at kLaunchRegs,
+    // epilogue warpgroups up to kEpiRegs (the pool is what the launch allocated)
+    static constexpr int kLaunchRegs = kScore ? (65536 / kThreads) / 8 * 8 : 128;
+    static constexpr int kCtrlRegs = FKDE_CTRL_REGS;
+    static constexpr int kEpiRegs =
+        kScore ? (kLaunchRegs * kThreads - 128 * kCtrlRegs - 128 * kLaunchRegs) / (128 * kNP) / 8 * 8
+               : 0;
+    static_assert(!kScore || (kEpiRegs >= kLaunchRegs && kEpiRegs <= 256), "setmaxnreg split");
+    static constexpr int kStages = 8;
     static constexpr uint32_t kOffA = 0;
     // column tile width: score 96 points (4 S/P buffers of 96 TMEM columns fit
     // beside the two O buffers; 3 of 128 made the S ring the bottleneck), KDE 128
@@ -105,18 +125,15 @@ struct TcConfig {
     static constexpr uint32_t kColBytes = kNCol * kRowBytes;   // one B column tile
     static_assert(kNCol % 32 == 0 && kColBytes % 1024 == 0, "column tiles of whole SW128 atoms");
     static constexpr uint32_t kOffB = 2 * kTileBytes;
-    // score: per-unit merge area for the kNP epilogue warps' drained sums,
-    // [kNP][128 rows][kAccStride] doubles
-    static constexpr uint32_t kAccStride = 17;
     static constexpr uint32_t kOffAcc = kOffB + kStages * kTileBytes;
-    static constexpr uint32_t kAccBytes = kScore ? kNP * 128 * kAccStride * 8 : 0;
+    static constexpr uint32_t kAccBytes = 0;
     static constexpr uint32_t kOffBar = kOffAcc + kAccBytes;
     // S accumulators in TMEM (128 columns each).  Score: 3 (S/P of tiles
     // t, t+1, t+2 in flight, GEMM2 lags GEMM1 by two tiles) + O[2] at 384.
     // KDE: 4.
     static constexpr int kSBuf = kScore ? 384 / kNCol : 4;
     static constexpr uint32_t kNumBars = 4 + 2 * kStages + 4 * kSBuf + 4;
-    // + tmem slot, drain tokens, 1 KiB alignment slack
+    // + tmem slot, 1 KiB alignment slack
     static constexpr uint32_t kSmemBytes = kOffBar + kNumBars * 8 + 64 + 1024;
     static constexpr uint32_t kTmemCols = 512;
     static constexpr uint32_t kTmemO = 384;   // score: O[2] (2 x 64 cols: T_hi, S, T_lo)
@@ -134,7 +151,8 @@ struct TcConfig {
 #endif
 
 template <int MODE>
-__global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kernel(PairArgs args) {
+__global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1)
+pairwise_tc_kernel(PairArgs args) {
     using Cfg = TcConfig<MODE>;
     constexpr bool kScore = Cfg::kScore;
     constexpr int kStages = Cfg::kStages;
@@ -157,9 +175,6 @@ __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kerne
     uint64_t* o_full = s_free + kSB;      // [2]
     uint64_t* o_empty = o_full + 2;       // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
-    // score: per (lane quadrant, O buffer) count of drains whose o_full wait
-    // has passed (see the epilogue's drain())
-    volatile uint32_t* drain_passed = tmem_slot + 1;   // [4][2]
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -184,8 +199,6 @@ __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kerne
             ptx::mbar_init(&o_empty[i], 4);
         }
 
-
-        for (int i = 0; i < 8; ++i) drain_passed[i] = 0;
         ptx::fence_barrier_init();
     }
     if (warp == 1) ptx::tmem_alloc<Cfg::kTmemCols>(tmem_slot);
@@ -196,6 +209,12 @@ __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kerne
 
     const int n_units = args.n_row_tiles * args.splits;
 
+    // Control warps (producer, MMA issuers) and epilogue warps live in separate
+    // warpgroups in the score pass; each side resizes its register file at the
+    // top of its own branch so that ptxas can allocate the epilogue's code for
+    // kEpiRegs registers (the resize dominates every epilogue instruction).
+    if (warp < Cfg::kCtrlEnd) {
+    if constexpr (kScore) ptx::setmaxnreg_dec<Cfg::kCtrlRegs>();
     if (warp == 0) {
         // ===================== producer: bulk async copies =====================
         // The whole warp runs the loop (all values warp-uniform, no waterfall
@@ -334,26 +353,83 @@ __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kerne
             }
             ++it_a;
         }
-    } else if (warp >= Cfg::kEpi0 && warp < Cfg::kEpiEnd) {
+    }
+    } else if (warp < Cfg::kEpi0) {
+        if constexpr (kScore) {
+            // ===================== O drain warps (score) =====================
+            // Warp 4+q drains lane quadrant q of every O sub-unit (2^flush_log2
+            // column tiles) in order: wait for GEMM2's commit, read T_hi, S, T_lo,
+            // release the buffer, fold into float-float sums (2Sum, ~48-bit
+            // significand) and write one fp64 partial per (split, row) at the
+            // unit's end.  Keeping this off the epilogue warps leaves them a
+            // uniform ld -> ex2 -> st stream with no waits on GEMM2.
+            const int q = warp & 3;
+            const int r = q * 32 + lane;
+            const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
+            const int lf = args.flush_log2;
+            const int fmask = (1 << lf) - 1;
+            uint32_t it_u = 0;
+            for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+                const int sp = u / args.n_row_tiles, rt = u % args.n_row_tiles;
+                const int ct0 = static_cast<int>((long long)sp * args.n_col_tiles / args.splits);
+                const int ct1 = static_cast<int>((long long)(sp + 1) * args.n_col_tiles / args.splits);
+                const int nsub = (ct1 - ct0 + fmask) >> lf;
+                float ahi[kMaxDim + 1], alo[kMaxDim + 1];
+#pragma unroll
+                for (int c = 0; c <= kMaxDim; ++c) ahi[c] = alo[c] = 0.f;
+#pragma unroll 1
+                for (int j = 0; j < nsub; ++j, ++it_u) {
+                    const uint32_t g = it_u;
+                    const uint32_t to = lane_addr + Cfg::kTmemO + (g & 1) * 64;
+                    uint32_t od[16], ol[16], os_;
+                    FKDE_TRACE(4, g);
+                    ptx::mbar_wait(&o_full[g & 1], (g >> 1) & 1);
+                    FKDE_TRACE(5, g);
+                    ptx::tc_fence_after();
+                    ptx::tmem_ld16(to, od);
+                    ptx::tmem_ld1(to + 16, os_);
+                    ptx::tmem_ld16(to + 32, ol);
+                    ptx::tmem_ld_wait();
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&o_empty[g & 1]);
+#pragma unroll
+                    for (int c = 0; c <= kMaxDim; ++c) {
+                        const float x = c < kMaxDim ? __uint_as_float(od[c]) + __uint_as_float(ol[c])
+                                                    : __uint_as_float(os_);
+                        const float s2 = ahi[c] + x;           // 2Sum(ahi, x)
+                        const float bb = s2 - ahi[c];
+                        const float e = (ahi[c] - (s2 - bb)) + (x - bb);
+                        ahi[c] = s2;
+                        alo[c] += e;
+                    }
+                }
+                const size_t idx = static_cast<size_t>(sp) * args.rows_pad + static_cast<size_t>(rt) * kTileRows + r;
+                args.dpart0[idx] = static_cast<double>(ahi[kMaxDim]) + static_cast<double>(alo[kMaxDim]);
+                double2* t = reinterpret_cast<double2*>(args.dpart1 + idx * kMaxDim);
+#pragma unroll
+                for (int w = 0; w < kMaxDim / 2; ++w)
+                    t[w] = make_double2(static_cast<double>(ahi[2 * w]) + static_cast<double>(alo[2 * w]),
+                                        static_cast<double>(ahi[2 * w + 1]) + static_cast<double>(alo[2 * w + 1]));
+            }
+        }
+    } else if (warp < Cfg::kEpiEnd) {
+        if constexpr (kScore) ptx::setmaxnreg_inc<Cfg::kEpiRegs>();
         // ===================== epilogue warps =====================
         // Warp w reads TMEM lane quadrant w%4 and handles every kNP-th column
-        // tile (phase par = (w-2)/4), all 128 columns of it, in four 32-column
-        // chunks.  The kNP warps sharing an SM sub-partition (and a lane
-        // quadrant) therefore work on different tiles, out of phase: while one
-        // waits for its next S tile (GEMM1 of tile t + kNP can only start
-        // once GEMM2 of tile t has released the buffer) the others keep the
-        // MUFU pipe busy.  The own-tile loop carries only a few integer ops of
-        // bookkeeping: with few warps per sub-partition, long dependent scalar
-        // chains between tiles would not be hidden.
+        // tile (phase par = (w-kEpi0)/4), all its columns, in 32-column chunks.
+        // The kNP warps sharing an SM sub-partition (and a lane quadrant)
+        // therefore work on different tiles, out of phase: while one waits for
+        // its next S tile (GEMM1 of tile t + kNP can only start once GEMM2 of
+        // tile t has released the buffer) the others keep the MUFU pipe busy.
+        // The own-tile loop carries only a few integer ops of bookkeeping.
         constexpr int NP = Cfg::kNP;
         const int q = warp & 3;                      // TMEM lane quadrant
         const int par = (warp - Cfg::kEpi0) >> 2;    // tile phase handled by this warp
         const int r = q * 32 + lane;                 // row within the 128-row tile
         const float dsc = args.sc->dscale;
         const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
-        const int lf = args.flush_log2;
-        const int fmask = (1 << lf) - 1;
-        uint32_t it_s = 0, it_u = 0;        // global tile / O sub-unit counters (all phases)
+        uint32_t it_s = 0;                           // global tile counter (all phases)
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
             const int sp = u / args.n_row_tiles, rt = u % args.n_row_tiles;
             const int ct0 = static_cast<int>((long long)sp * args.n_col_tiles / args.splits);
@@ -361,53 +437,6 @@ __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kerne
             const int len = ct1 - ct0;
             float2 acc2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
             float2 accl2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-            // score: running sums of the drained O sub-unit accumulators as
-            // unevaluated float pairs (hi + lo, ~48-bit significand): 2Sum on
-            // the FMA pipe instead of fp64 conversions + adds
-            float ahi[kMaxDim + 1], alo[kMaxDim + 1];
-#pragma unroll
-            for (int c = 0; c <= kMaxDim; ++c) ahi[c] = alo[c] = 0.f;
-            // O sub-unit j covers tiles [j << lf, (j+1) << lf) of this unit
-            // (global index it_u + j, TMEM buffer (it_u + j) & 1).  It is
-            // drained by the warp owning the tile two after its last one, right
-            // after that warp's P store (GEMM2 of the sub-unit has completed by
-            // then, so the o_full wait rarely stalls), or at the unit end.
-            auto drain = [&](int j, int tt) {
-                const uint32_t g = it_u + j;
-                uint32_t od[16], ol[16], os_;
-                const uint32_t to = lane_addr + Cfg::kTmemO + (g & 1) * 64;
-                // o_full[g & 1] is a parity wait: it is unambiguous only once the
-                // drain of sub-unit g - 2 (same buffer, possibly by another phase's
-                // warp of this quadrant) has passed its own wait.  Drains of one
-                // buffer pass in order (GEMM2 of g needs the drain of g - 2), so a
-                // per-(quadrant, buffer) count orders them; it almost never spins.
-                volatile uint32_t* tok = drain_passed + q * 2 + (g & 1);
-                while (*tok < (g >> 1)) {
-                }
-                ptx::mbar_wait(&o_full[g & 1], (g >> 1) & 1);
-                FKDE_TRACE(4, tt);
-                __syncwarp();
-                if (lane == 0) *tok = (g >> 1) + 1;
-                ptx::tc_fence_after();
-                ptx::tmem_ld16(to, od);
-                ptx::tmem_ld1(to + 16, os_);
-                ptx::tmem_ld16(to + 32, ol);
-                ptx::tmem_ld_wait();
-                FKDE_TRACE(5, tt);
-                ptx::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&o_empty[g & 1]);
-#pragma unroll
-                for (int c = 0; c <= kMaxDim; ++c) {
-                    const float x = c < kMaxDim ? __uint_as_float(od[c]) + __uint_as_float(ol[c])
-                                                : __uint_as_float(os_);
-                    const float s2 = ahi[c] + x;           // 2Sum(ahi, x)
-                    const float bb = s2 - ahi[c];
-                    const float e = (ahi[c] - (s2 - bb)) + (x - bb);
-                    ahi[c] = s2;
-                    alo[c] += e;
-                }
-            };
             // this warp's first own tile and its S buffer / phase
             int rel = par - static_cast<int>(it_s % NP);
             if (rel < 0) rel += NP;
@@ -490,11 +519,6 @@ __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kerne
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(&p_full[sb]);
                     FKDE_TRACE(2, it_s + rel);
-                    // drain the sub-unit whose last tile is rel - 2 (if any)
-                    if (rel >= 2 && ((rel - 2) & fmask) == fmask) {
-                        drain((rel - 2) >> lf, it_s + rel);
-                        FKDE_TRACE(3, it_s + rel);
-                    }
                 } else {
                     // (phi <= 1 up to the expansion's rounding: no clamp needed)
 #pragma unroll 1
@@ -525,47 +549,9 @@ __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1) pairwise_tc_kerne
                     ph ^= 1;
                 }
             }
-            const size_t row = static_cast<size_t>(rt) * kTileRows + r;
-            if constexpr (kScore) {
-                // sub-units ending at the last two tiles have their drain tile
-                // beyond the unit: drained here, in order, by the owner of the
-                // unit's last tile
-                if ((it_s + len - 1) % NP == static_cast<uint32_t>(par)) {
-#pragma unroll 1
-                    for (int last = len - 2; last < len; ++last) {
-                        if (last < 0) continue;
-                        if ((last & fmask) == fmask || last == len - 1) drain(last >> lf, 255);
-                    }
-                }
-                // the kNP phases drained disjoint sub-units: merge them through
-                // shared memory (named barrier over the epilogue warps) and
-                // write one fp64 partial per (split, row)
-                double* accs = reinterpret_cast<double*>(smem + Cfg::kOffAcc);
-                double* acc = accs + (par * 128 + r) * Cfg::kAccStride;
-#pragma unroll
-                for (int c = 0; c <= kMaxDim; ++c)
-                    acc[c] = static_cast<double>(ahi[c]) + static_cast<double>(alo[c]);
-                ptx::named_bar_sync(1, NP * 128);
-                if (par == 0) {
-                    double tot[kMaxDim + 1];
-#pragma unroll
-                    for (int c = 0; c <= kMaxDim; ++c) tot[c] = acc[c];
-#pragma unroll
-                    for (int o = 1; o < NP; ++o) {
-                        const double* other = accs + (o * 128 + r) * Cfg::kAccStride;
-#pragma unroll
-                        for (int c = 0; c <= kMaxDim; ++c) tot[c] += other[c];
-                    }
-                    const size_t idx = static_cast<size_t>(sp) * args.rows_pad + row;
-                    args.dpart0[idx] = tot[kMaxDim];
-                    double2* t = reinterpret_cast<double2*>(args.dpart1 + idx * kMaxDim);
-#pragma unroll
-                    for (int w = 0; w < kMaxDim / 2; ++w) t[w] = make_double2(tot[2 * w], tot[2 * w + 1]);
-                }
-                ptx::named_bar_sync(1, NP * 128);   // the merge area is rewritten next unit
-                it_u += (len + fmask) >> lf;
-            } else {
+            if constexpr (!kScore) {
                 // the kNP phases hold disjoint column subsets of this unit
+                const size_t row = static_cast<size_t>(rt) * kTileRows + r;
                 const size_t idx = static_cast<size_t>(sp * NP + par) * args.rows_pad + row;
                 args.part0[idx] = (acc2[0].x + acc2[0].y) + (acc2[1].x + acc2[1].y);
                 if constexpr (MODE == kModeLaplace)

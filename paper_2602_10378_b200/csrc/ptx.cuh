@@ -326,6 +326,16 @@ __device__ __forceinline__ float2 ex2_poly2(float2 t) {
                        __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(rm.y) << 23)));
 }
 
+// warpgroup-wide register reallocation (all four warps of a warpgroup execute it)
+template <int N>
+__device__ __forceinline__ void setmaxnreg_inc() {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <int N>
+__device__ __forceinline__ void setmaxnreg_dec() {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+
 // named barrier over `count` threads (multiple of 32)
 __device__ __forceinline__ void named_bar_sync(int id, int count) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");

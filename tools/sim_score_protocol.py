@@ -1,7 +1,8 @@
 """Model check of the score kernel's mbarrier protocol (csrc/pairwise_tc.cuh,
 pairwise_tc_kernel<kModeScore>) for one CTA.
 
-Actors: the GEMM1 issuer, the GEMM2 issuer and the 4*NP epilogue warps, each a
+Actors: the GEMM1 issuer, the GEMM2 issuer, the 4 O-drain warps (one per TMEM
+lane quadrant) and the 4*NP epilogue warps, each a
 generator yielding the waits of the kernel in program order; arrivals and
 tensor-core commits are applied when the actor resumes (the tensor core is
 in-order, so a commit after an MMA completes when the actor issues it).  A
@@ -33,20 +34,11 @@ class _Bar:
         return ok
 
 
-class _Cond:
-    def __init__(self, f):
-        self.f = f
-
-    def done(self, parity, need):
-        return self.f()
-
-
 def run(NP, F, lens, seed=0, SB=4):
     """SB: S/P TMEM buffers (384 / column-tile width)."""
     lf = F.bit_length() - 1
     fmask = F - 1
     bars = {}
-    tok = {(q, b): 0 for q in range(4) for b in range(2)}
 
     def B(name, i, count):
         if (name, i) not in bars:
@@ -85,37 +77,34 @@ def run(NP, F, lens, seed=0, SB=4):
                     itu += 1
                 it += 1
 
-    def epi(par, q):
-        its = itu = 0
+    def drainer(q):
+        itu = 0
         for L in lens:
-            def drain(j):
-                g = itu + j
-                yield (_Cond(lambda: tok[(q, g & 1)] >= (g >> 1)), 0, None)
+            for _ in range((L + fmask) >> lf):
+                g = itu
                 yield (ofull(g & 1), (g >> 1) & 1, (g >> 1) + 1)
-                tok[(q, g & 1)] = (g >> 1) + 1
                 oempty(g & 1).arrive()
+                itu += 1
+
+    def epi(par, q):
+        its = 0
+        for L in lens:
             rel = (par - its % NP) % NP
             sidx = its + rel
             sb, ph = sidx % SB, (sidx // SB) & 1
             while rel < L:
                 yield (sfull(sb), ph, (its + rel) // SB + 1)
                 pfull(sb).arrive()
-                if rel >= 2 and ((rel - 2) & fmask) == fmask:
-                    yield from drain((rel - 2) >> lf)
                 sb += NP
                 if sb >= SB:
                     sb -= SB
                     ph ^= 1
                 rel += NP
-            if (its + L - 1) % NP == par:
-                for last in (L - 2, L - 1):
-                    if last >= 0 and ((last & fmask) == fmask or last == L - 1):
-                        yield from drain(last >> lf)
-            itu += (L + fmask) >> lf
             its += L
 
     rng = random.Random(seed)
-    actors = [g1(), g2()] + [epi(p, q) for p in range(NP) for q in range(4)]
+    actors = [g1(), g2()] + [drainer(q) for q in range(4)] + \
+        [epi(p, q) for p in range(NP) for q in range(4)]
     cur = [None] * len(actors)
     done = [False] * len(actors)
     try:

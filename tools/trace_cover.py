@@ -13,7 +13,8 @@ sys.path.insert(0, ROOT)
 import paper_2602_10378_b200 as fk  # noqa: E402
 from paper_2602_10378_b200 import _native as N, fixtures as F  # noqa: E402
 
-NP = int(os.environ.get("FKDE_EPI_NP", "3"))
+NP = int(os.environ.get("FKDE_SCORE_NP", "3"))
+E0 = 8          # first epilogue warp (0-3 control, 4-7 O drain warps)
 
 
 def main():
@@ -28,13 +29,13 @@ def main():
     torch.cuda.synchronize()
     t = buf.view(32, 8, 256).cpu().numpy().astype(np.float64)
     lo, hi = 16, 200
-    t0 = np.nanmin(np.where(t[2:2 + 4 * NP, 1, lo:hi] > 0, t[2:2 + 4 * NP, 1, lo:hi], np.nan))
-    t1 = np.nanmax(np.where(t[2:2 + 4 * NP, 7, lo:hi] > 0, t[2:2 + 4 * NP, 7, lo:hi], np.nan))
+    t0 = np.nanmin(np.where(t[E0:E0 + 4 * NP, 1, lo:hi] > 0, t[E0:E0 + 4 * NP, 1, lo:hi], np.nan))
+    t1 = np.nanmax(np.where(t[E0:E0 + 4 * NP, 7, lo:hi] > 0, t[E0:E0 + 4 * NP, 7, lo:hi], np.nan))
     span = t1 - t0
     ntiles = hi - lo
     print(f"n={n}: window {span:.0f} cycles for ~{ntiles} tiles = {span / ntiles:.0f}/tile")
     for s in range(4):
-        warps = [w for w in range(2, 2 + 4 * NP) if w % 4 == s]
+        warps = [w for w in range(E0, E0 + 4 * NP) if w % 4 == s]
         cov = np.zeros(int(span) + 1, dtype=np.int8)
         for w in warps:
             for k in range(lo, hi):
@@ -43,13 +44,11 @@ def main():
                     cov[int(a - t0):int(b - t0)] += 1
         frac = [(cov >= j).mean() for j in (1, 2, 3)]
         print(f"  SMSP {s} (warps {warps}): >=1 warp computing {frac[0]*100:.1f}%  >=2 {frac[1]*100:.1f}%  3 {frac[2]*100:.1f}%")
-    E = range(2, 2 + 4 * NP)
+    E = range(E0, E0 + 4 * NP)
     ldl = np.concatenate([(t[w, 6, lo:hi] - t[w, 1, lo:hi])[t[w, 6, lo:hi] > 0] for w in E])
     print(f"  first-chunk ld latency (s_full pass -> ld done): mean {ldl.mean():.0f} median {np.median(ldl):.0f}")
-    ow = np.concatenate([(t[w, 4, lo:hi] - t[w, 2, lo:hi])[t[w, 4, lo:hi] > 0] for w in E])
-    lw = np.concatenate([(t[w, 5, lo:hi] - t[w, 4, lo:hi])[t[w, 4, lo:hi] > 0] for w in E])
-    aw = np.concatenate([(t[w, 3, lo:hi] - t[w, 5, lo:hi])[t[w, 4, lo:hi] > 0] for w in E])
-    print(f"  drain: o_full wait {ow.mean():.0f}  ld {lw.mean():.0f}  2Sum+rest {aw.mean():.0f}")
+    dw = np.concatenate([(t[w, 5, :] - t[w, 4, :])[(t[w, 4, :] > 0) & (t[w, 5, :] > 0)] for w in range(4, 8)])
+    print(f"  drain warps: o_full wait per sub-unit mean {dw.mean():.0f} (includes idle time)")
     comp = np.concatenate([(t[w, 7, lo:hi] - t[w, 6, lo:hi])[t[w, 6, lo:hi] > 0] for w in E])
     print(f"  compute after first ld (3 chunks): mean {comp.mean():.0f}")
 

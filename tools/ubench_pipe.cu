@@ -257,7 +257,135 @@ void run_tmem_pipe(const char* name, int warps) {
     cudaFree(cyc);
 }
 
+// tmem_mix with a concurrent tensor-core stream: warp 0 issues, per "tile",
+// 4 SS MMAs M=128 N=96 (GEMM1-like, into TMEM cols 288..383) then 12 TS MMAs
+// N=48 reading A from those columns (GEMM2-like, into cols 384..431), commits,
+// waits, idles `gap` cycles; warps 4..15 run the score epilogue's TMEM
+// ld -> math -> st pattern on cols 0..287.  Does tensor traffic slow the epilogue?
+__global__ void __launch_bounds__(512, 1) tmem_mix_mma(int iters, int mma_on, int gap, uint32_t* sink,
+                                                      unsigned long long* cyc) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tslot;
+    __shared__ int done;     // epilogue warps finished
+    const int warp = threadIdx.x / 32;
+    for (int i = threadIdx.x; i < 65536 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
+    if (threadIdx.x == 0) {
+        ptx::mbar_init(&bar, 1);
+        ptx::fence_barrier_init();
+        done = 0;
+    }
+    if (warp == 0) ptx::tmem_alloc<512>(&tslot);
+    ptx::fence_proxy_async_smem();
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tb0 = tslot;
+    if (warp == 0) {
+        if (mma_on) {
+            const uint32_t sA = ptx::smem_u32(smem), sB = sA + 32768;
+            constexpr uint32_t id1 = ptx::idesc_f16_f32(128, 96, false, false);
+            constexpr uint32_t id2 = ptx::idesc_f16_f32(128, 48, false, true);
+            uint32_t ph = 0;
+            while (*(volatile int*)&done < 12) {
+                if (ptx::elect_one()) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        ptx::umma_f16(tb0 + 288, ptx::smem_desc_sw128(sA + k * 32, 16, 1024),
+                                      ptx::smem_desc_sw128(sB + k * 32, 16, 1024), id1, k ? 1u : 0u);
+#pragma unroll
+                    for (int k = 0; k < 12; ++k)
+                        ptx::umma_f16_ts(tb0 + 384, tb0 + 288 + k * 8, ptx::smem_desc_sw128(sB + (k & 3) * 2048, 16384, 1024),
+                                         id2, 1u);
+                    ptx::umma_commit(&bar);
+                }
+                __syncwarp();
+                ptx::mbar_wait(&bar, ph);
+                ph ^= 1;
+                const long long t = clock64();
+                while (clock64() - t < gap) {
+                }
+            }
+        }
+    } else if (warp >= 4) {
+        const uint32_t tb = tb0 + ((uint32_t)((warp & 3) * 32) << 16) + ((warp - 4) >> 2) * 96;
+        const float2 off2 = make_float2(15.f, 15.f), neg1 = make_float2(-1.f, -1.f);
+        const float2 dsc2 = make_float2(1.0001f, 1.0001f);
+        {
+            uint32_t z[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) z[i] = __float_as_uint(-0.01f * (i + 1));
+            for (int c = 0; c < 96; c += 16) ptx::tmem_st16(tb + c, z);
+            ptx::tmem_st_wait();
+        }
+        const unsigned long long t0 = clock64();
+        for (int it = 0; it < iters; ++it) {
+#pragma unroll 1
+            for (int ch = 0; ch < 3; ++ch) {
+                uint32_t v[32];
+                ptx::tmem_ld32(tb + ch * 32, v);
+                ptx::tmem_ld_wait();
+                uint32_t hi_w[16], lo_w[16];
+#pragma unroll
+                for (int w = 0; w < 16; ++w) {
+                    const float2 t = ptx::ffma2(make_float2(__uint_as_float(v[2 * w]), __uint_as_float(v[2 * w + 1])), dsc2, off2);
+                    const float2 p = make_float2(ptx::ex2(t.x), ptx::ex2(t.y));
+                    const float2 h = make_float2(__uint_as_float(__float_as_uint(p.x) & 0xFFFFE000u),
+                                                 __uint_as_float(__float_as_uint(p.y) & 0xFFFFE000u));
+                    const float2 l = ptx::ffma2(h, neg1, p);
+                    hi_w[w] = ptx::cvt_f16x2(h.x, h.y) & 0xBFFFBFFFu;
+                    lo_w[w] = ptx::cvt_f16x2(l.x, l.y);
+                }
+                ptx::tmem_st16(tb + ch * 32, hi_w);
+                ptx::tmem_st16(tb + ch * 32 + 16, lo_w);
+            }
+            ptx::tmem_st_wait();
+        }
+        const unsigned long long t1 = clock64();
+        if ((threadIdx.x & 31) == 0) {
+            cyc[blockIdx.x * 16 + warp] = t1 - t0;
+            atomicAdd(&done, 1);
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<512>(tb0);
+    }
+    if (threadIdx.x == 1000) sink[0] = 0;
+}
+
+void run_tmem_mma(int mma_on, int gap) {
+    const int iters = 600;
+    uint32_t* sink;
+    unsigned long long* cyc;
+    cudaMalloc(&sink, 4096 * 4);
+    cudaMalloc(&cyc, 148 * 16 * 8);
+    cudaFuncSetAttribute(tmem_mix_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+    tmem_mix_mma<<<148, 512, 65536>>>(5, mma_on, gap, sink, cyc);
+    tmem_mix_mma<<<148, 512, 65536>>>(iters, mma_on, gap, sink, cyc);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) { printf("tmem_mma: %s\n", cudaGetErrorString(e)); exit(1); }
+    unsigned long long h[148 * 16];
+    cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
+    double mx = 0;
+    for (int b = 0; b < 148; ++b)
+        for (int w = 4; w < 16; ++w) mx = h[b * 16 + w] > mx ? h[b * 16 + w] : mx;
+    const double elems = (double)iters * 96 * 32 * 12;
+    printf("tmem ld+math+st, 12 warps, MMA stream %s (gap %4d): %6.2f elem/clk/SM (%.1f%% of 16/clk)\n",
+           mma_on ? "on " : "off", gap, elems / mx, elems / mx / 16 * 100);
+    fflush(stdout);
+    cudaFree(sink);
+    cudaFree(cyc);
+}
+
 int main() {
+    run_tmem_mma(0, 0);
+    run_tmem_mma(1, 0);
+    run_tmem_mma(1, 300);
+    run_tmem_mma(1, 800);
+    return 0;
     for (int w : {8, 12, 16}) {
         run_tmem<0>("tmem ld+math+st", w);
         run_tmem<1>("tmem ld+math", w);
