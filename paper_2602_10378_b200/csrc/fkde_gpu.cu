@@ -163,6 +163,8 @@ struct Device {
     int world = 1;
     int num_sms = 148;
     cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr;       // host copies that overlap the next pass
+    cudaEvent_t ev_side_in = nullptr, ev_side_out = nullptr;
     ncclComm_t comm = nullptr;
     bool attrs_set = false;
     DevBuf X, Y, opA, opB, part0, part1, xsd, out, aux0, aux1, colpart, scal, err, flags;
@@ -644,6 +646,20 @@ Status run_job(Device& D, const Options& o, const Job& J) {
             break;
         case Job::kSdkde: {
             STATUS_TRY(score_program(D, o, J, dX, sc_s, true));
+            if (J.out2) {
+                // debiased samples to the host on the side stream, overlapping the
+                // density pass (it only reads D.xsd)
+                STATUS_TRY(ensure(D.aux1, J.n * d * sizeof(double)));
+                add_mean<<<grid1(J.n * d, 256), 256, 0, D.stream>>>(D.xsd.as<double>(), J.n, d, sc_s,
+                                                                    D.aux1.as<double>());
+                ++D.launches;
+                CUDA_TRY(cudaGetLastError());
+                CUDA_TRY(cudaEventRecord(D.ev_side_in, D.stream));
+                CUDA_TRY(cudaStreamWaitEvent(D.side, D.ev_side_in, 0));
+                CUDA_TRY(cudaMemcpyAsync(J.out2, D.aux1.p, J.n * d * sizeof(double),
+                                         cudaMemcpyDeviceToHost, D.side));
+                CUDA_TRY(cudaEventRecord(D.ev_side_out, D.side));
+            }
             // sc_q: same centring mean, fresh scale (x_sd is already centred)
             CUDA_TRY(cudaMemcpyAsync(sc_q, sc_s, sizeof(PassScalars), cudaMemcpyDeviceToDevice,
                                      D.stream));
@@ -675,14 +691,8 @@ Status run_job(Device& D, const Options& o, const Job& J) {
             CUDA_TRY(cudaMemcpyAsync(J.out, D.out.p, J.m * sizeof(double), cudaMemcpyDeviceToHost,
                                      D.stream));
         }
-        if (J.kind == Job::kSdkde && J.out2) {
-            STATUS_TRY(ensure(D.aux1, nd * sizeof(double)));
-            add_mean<<<grid1(nd, 256), 256, 0, D.stream>>>(D.xsd.as<double>(), J.n, d, sc_s,
-                                                          D.aux1.as<double>());
-            ++D.launches;
-            CUDA_TRY(cudaMemcpyAsync(J.out2, D.aux1.p, nd * sizeof(double),
-                                     cudaMemcpyDeviceToHost, D.stream));
-        }
+        if (J.kind == Job::kSdkde && J.out2)   // the side-stream copy joins the main stream
+            CUDA_TRY(cudaStreamWaitEvent(D.stream, D.ev_side_out, 0));
     } else if (J.kind == Job::kScore) {
         CUDA_TRY(cudaMemcpyAsync(J.out, D.aux0.p, nd * sizeof(double), cudaMemcpyDeviceToHost,
                                  D.stream));
@@ -765,6 +775,9 @@ Status init_device(Device& D, int dev, int rank, int world) {
                            prop.major, prop.minor);
     D.num_sms = prop.multiProcessorCount;
     CUDA_TRY(cudaStreamCreateWithFlags(&D.stream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&D.side, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&D.ev_side_in, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&D.ev_side_out, cudaEventDisableTiming));
     return {};
 }
 
@@ -875,6 +888,9 @@ void fkde_gpu_destroy(fkde_gpu_ctx* ctx) {
         for (auto& e : D.ev)
             if (e) cudaEventDestroy(e);
         if (D.stream) cudaStreamDestroy(D.stream);
+        if (D.side) cudaStreamDestroy(D.side);
+        if (D.ev_side_in) cudaEventDestroy(D.ev_side_in);
+        if (D.ev_side_out) cudaEventDestroy(D.ev_side_out);
     }
     delete ctx;
 }
