@@ -149,6 +149,10 @@ struct TcConfig {
 #ifndef FKDE_SPLIT
 #define FKDE_SPLIT 0
 #endif
+// GEMM2 N for the P_lo half: 32 (y_hi + the ones block; P_lo . y_lo dropped) or 48
+#ifndef FKDE_G2_LO_N
+#define FKDE_G2_LO_N 32
+#endif
 
 template <int MODE>
 __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1)
@@ -258,6 +262,9 @@ pairwise_tc_kernel(PairArgs args) {
         // field, so each MMA costs a uniform add + the instruction.
         constexpr uint32_t idesc1 = ptx::idesc_f16_f32(128, Cfg::kNCol, false, false);
         constexpr uint32_t idesc2 = ptx::idesc_f16_f32(128, Cfg::kN2, false, true);
+        // P_lo rows only need the y_hi and ones columns: P_lo . y_lo is 2^-22 of the
+        // sum and is dropped, which takes 1/6 of GEMM2's MACs (and power) away
+        constexpr uint32_t idesc2_lo = ptx::idesc_f16_f32(128, FKDE_G2_LO_N, false, true);
         const uint64_t descA = ptx::smem_desc_sw128(ptx::smem_u32(smA), 16, 1024);
         const uint64_t descB = ptx::smem_desc_sw128(ptx::smem_u32(smB), 16, 1024);
         const uint64_t descBmn = ptx::smem_desc_sw128(ptx::smem_u32(smB), kTileBytes, 1024);
@@ -332,7 +339,7 @@ pairwise_tc_kernel(PairArgs args) {
                             for (int part = 0; part < 2; ++part) {
                                 // one N=48 MMA per K step: columns 0-15 T_hi, 16 S, 32-47 T_lo
                                 ptx::umma_f16_ts(to, ta0 + (k >> 1) * 32 + part * 16 + (k & 1) * 8,
-                                                 db0 + ((k * 2048) >> 4), idesc2,
+                                                 db0 + ((k * 2048) >> 4), part ? idesc2_lo : idesc2,
                                                  (first && part == 0 && k == 0) ? 0u : 1u);
                             }
                         }
