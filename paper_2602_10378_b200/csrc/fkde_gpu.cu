@@ -456,7 +456,7 @@ Status score_program(Device& D, const Options& o, const Job& J, const double* dX
     STATUS_TRY(prepare_flags(D, sh.rows));
     f.flag_count = D.flags.as<unsigned int>();
     f.flag_rows = f.flag_count + 1;
-    finalize_score<<<grid1(std::max<size_t>(sh.rows, 1), 128), 128, 0, D.stream>>>(f);
+    finalize_score<<<grid1(std::max<size_t>(sh.rows, 1) * d, 256), 256, 0, D.stream>>>(f);
     ++D.launches;
     CUDA_TRY(cudaGetLastError());
     {

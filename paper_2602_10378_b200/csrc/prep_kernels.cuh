@@ -212,8 +212,13 @@ struct FinalizeArgs {
     unsigned int* flag_rows;            // (local indices)
 };
 
+// One thread per (row, coordinate): consecutive threads read consecutive
+// doubles of the [split][row][16] partials and write consecutive score /
+// x^SD entries (a thread per row strided every access by 128 B).
 __global__ void finalize_score(FinalizeArgs a) {
-    const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    const size_t i = t / static_cast<size_t>(a.d);
+    const int c = static_cast<int>(t % static_cast<size_t>(a.d));
     if (i >= a.rows) return;
     // S' and T' exclude the self pair (phi_ii = exp(0) = 1, engine.cpp:43-50
     // snaps r_ii^2 to 0): S = 1 + S', and T - x_i S = T' - x_i S'.
@@ -221,30 +226,27 @@ __global__ void finalize_score(FinalizeArgs a) {
     for (int s = 0; s < a.splits; ++s) Sp += a.part_s[s * a.rows_pad + i];
     Sp = ldexp(Sp, -kPScaleExp);  // the tc/simt score sums carry phi * 2^15
     if (Sp < kScoreFlagMass && a.flag_rows) {  // too little neighbour mass for fp16 P
-        a.flag_rows[atomicAdd(a.flag_count, 1u)] = static_cast<unsigned int>(i);
+        if (c == 0) a.flag_rows[atomicAdd(a.flag_count, 1u)] = static_cast<unsigned int>(i);
         return;
     }
     const double S = 1.0 + Sp;
     const double ys = ldexp(a.k, -a.sc->e);
     const size_t g = a.row0 + i;
-    if (a.phi_sum) a.phi_sum[g] = S;
+    if (a.phi_sum && c == 0) a.phi_sum[g] = S;
     if (!(S > 0.0) || !isfinite(S)) {
-        atomicMin(a.underflow_row, static_cast<unsigned long long>(g));
+        if (c == 0) atomicMin(a.underflow_row, static_cast<unsigned long long>(g));
         return;
     }
     const double inv = 1.0 / (a.h_score * a.h_score * S);
-    for (int c = 0; c < a.d; ++c) {
-        double Tp = 0.0;
-        for (int s = 0; s < a.splits; ++s)
-            Tp += a.part_t[(s * a.rows_pad + i) * kMaxDim + c];
-        const double tc = ldexp(Tp, -kPScaleExp) / ys;  // sum_{j != i} phi_ij xc_j
-        const double x = a.x[g * a.d + c];
-        const double xc = x - a.sc->mu[c];
-        const double s = (tc - xc * Sp) * inv;         // (T - x S) / (h^2 S)
-        if (a.score) a.score[g * a.d + c] = s;
-        if (a.xsd_c) a.xsd_c[g * a.d + c] = xc + a.shift * s;
-        if (a.weighted) a.weighted[g * a.d + c] = (tc + xc) + S * a.sc->mu[c];
-    }
+    double Tp = 0.0;
+    for (int s = 0; s < a.splits; ++s) Tp += a.part_t[(s * a.rows_pad + i) * kMaxDim + c];
+    const double tc = ldexp(Tp, -kPScaleExp) / ys;  // sum_{j != i} phi_ij xc_j
+    const double x = a.x[g * a.d + c];
+    const double xc = x - a.sc->mu[c];
+    const double sc = (tc - xc * Sp) * inv;         // (T - x S) / (h^2 S)
+    if (a.score) a.score[g * a.d + c] = sc;
+    if (a.xsd_c) a.xsd_c[g * a.d + c] = xc + a.shift * sc;
+    if (a.weighted) a.weighted[g * a.d + c] = (tc + xc) + S * a.sc->mu[c];
 }
 
 // debiased samples in original coordinates: x_sd = x_sd_c + mu
