@@ -24,6 +24,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -59,7 +60,11 @@ NcclApi& nccl() {
     static NcclApi api;
     static std::once_flag once;
     std::call_once(once, [] {
-        const char* names[] = {"libnccl.so.2", "libnccl.so"};
+        // FKDE_NCCL_LIB: explicit NCCL (or NCCL-API-compatible) library path,
+        // e.g. a specific NCCL build; tests use it for an in-process transport
+        // that lets the multi-rank code path run on a single GPU
+        const char* env = std::getenv("FKDE_NCCL_LIB");
+        const char* names[] = {env && *env ? env : "libnccl.so.2", "libnccl.so.2", "libnccl.so"};
         void* h = nullptr;
         for (const char* nm : names) {
             h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
@@ -693,14 +698,17 @@ Status run_job(Device& D, const Options& o, const Job& J) {
         }
         if (J.kind == Job::kSdkde && J.out2)   // the side-stream copy joins the main stream
             CUDA_TRY(cudaStreamWaitEvent(D.stream, D.ev_side_out, 0));
-    } else if (J.kind == Job::kScore) {
-        CUDA_TRY(cudaMemcpyAsync(J.out, D.aux0.p, nd * sizeof(double), cudaMemcpyDeviceToHost,
-                                 D.stream));
+    } else if (J.kind == Job::kScore) {   // (host outputs only on the first device)
+        if (J.out)
+            CUDA_TRY(cudaMemcpyAsync(J.out, D.aux0.p, nd * sizeof(double), cudaMemcpyDeviceToHost,
+                                     D.stream));
     } else if (J.kind == Job::kScoreAcc) {
-        CUDA_TRY(cudaMemcpyAsync(J.out, D.aux0.p, J.n * sizeof(double), cudaMemcpyDeviceToHost,
-                                 D.stream));
-        CUDA_TRY(cudaMemcpyAsync(J.out2, D.aux1.p, nd * sizeof(double), cudaMemcpyDeviceToHost,
-                                 D.stream));
+        if (J.out)
+            CUDA_TRY(cudaMemcpyAsync(J.out, D.aux0.p, J.n * sizeof(double), cudaMemcpyDeviceToHost,
+                                     D.stream));
+        if (J.out2)
+            CUDA_TRY(cudaMemcpyAsync(J.out2, D.aux1.p, nd * sizeof(double), cudaMemcpyDeviceToHost,
+                                     D.stream));
     }
     record(D, o, FKDE_T_TOTAL);
     if (!J.sync) return {};
