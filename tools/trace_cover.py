@@ -43,7 +43,12 @@ def main():
                 if a > 0 and b > 0 and a >= t0 and b <= t1:
                     cov[int(a - t0):int(b - t0)] += 1
         frac = [(cov >= j).mean() for j in (1, 2, 3)]
-        print(f"  SMSP {s} (warps {warps}): >=1 warp computing {frac[0]*100:.1f}%  >=2 {frac[1]*100:.1f}%  3 {frac[2]*100:.1f}%")
+        comp_s = np.concatenate([(t[w, 7, lo:hi] - t[w, 1, lo:hi])[(t[w, 7, lo:hi] > 0) & (t[w, 1, lo:hi] > 0)]
+                                 for w in warps])
+        wait_s = np.concatenate([(t[w, 1, lo:hi] - t[w, 0, lo:hi])[(t[w, 1, lo:hi] > 0) & (t[w, 0, lo:hi] > 0)]
+                                 for w in warps])
+        print(f"  SMSP {s} (warps {warps}): >=1 warp computing {frac[0]*100:.1f}%  >=2 {frac[1]*100:.1f}%  3 {frac[2]*100:.1f}%"
+              f" | per tile: s_full wait {wait_s.mean():5.0f}, ld..st {comp_s.mean():5.0f} cycles")
     E = range(E0, E0 + 4 * NP)
     ldl = np.concatenate([(t[w, 6, lo:hi] - t[w, 1, lo:hi])[t[w, 6, lo:hi] > 0] for w in E])
     print(f"  first-chunk ld latency (s_full pass -> ld done): mean {ldl.mean():.0f} median {np.median(ldl):.0f}")
