@@ -8,17 +8,17 @@
 // applies exp (engine.cpp:83-97/197) and reduces row sums (engine.cpp:128,198)
 // and, for the score, the second product Phi_tile * X_j (engine.cpp:199).
 //
-// Here one work unit = (128-row tile, contiguous range of 128-column tiles).
-// Per column tile:
-//   GEMM1  S[128x128] = A_rows(128x64 fp16) . B_cols(128x64 fp16)^T  -> TMEM
+// Here one work unit = (128-row tile, contiguous range of column tiles: 96
+// points in the score pass, 128 in the density passes).  Per column tile:
+//   GEMM1  S[128xN] = A_rows(128x64 fp16) . B_cols(Nx64 fp16)^T  -> TMEM
 //          (S is log2(phi) directly; see layout.cuh)
 //   epilogue warps: tcgen05.ld S -> phi = ex2(S*dscale) in registers;
 //          KDE: row sums (Gaussian) or (sum phi, sum phi*log2 phi) (Laplace);
 //          SCORE: phi -> fp16 hi/lo -> tcgen05.st back into S's own TMEM
 //          columns (P aliases S, flash-attention-4 style: no SMEM round trip)
-//   GEMM2 (SCORE only, A from TMEM)  O[128x48] += [P_hi | P_lo](128x256) . [B;B]
+//   GEMM2 (SCORE only, A from TMEM)  O[128x48] += P_hi . B[:, 0:48] + P_lo . B[:, 0:32]
 //          (B = the same column tile, MN-major) -> sum_j phi y_hi_j,
-//          sum_j phi y_lo_j, sum_j phi  (TMEM, fp32)
+//          sum_j phi y_lo_j, sum_j phi  (TMEM, fp32; drained by the drain warps)
 // The n x n kernel matrix never leaves the SM; per column tile the SMEM
 // traffic is the 16 KiB B tile read by both GEMMs and the 16 KiB A tile.
 //
@@ -128,9 +128,9 @@ struct TcConfig {
     static constexpr uint32_t kOffAcc = kOffB + kStages * kTileBytes;
     static constexpr uint32_t kAccBytes = 0;
     static constexpr uint32_t kOffBar = kOffAcc + kAccBytes;
-    // S accumulators in TMEM (128 columns each).  Score: 3 (S/P of tiles
-    // t, t+1, t+2 in flight, GEMM2 lags GEMM1 by two tiles) + O[2] at 384.
-    // KDE: 4.
+    // S accumulators in TMEM.  Score: 4 S/P buffers of 96 columns (a tile's S is
+    // overwritten by its P; the buffer is free again once GEMM2 has read P) +
+    // O[2] at column 384.  KDE: 4 of 128 (freed as soon as S is loaded).
     static constexpr int kSBuf = kScore ? 384 / kNCol : 4;
     static constexpr uint32_t kNumBars = 4 + 2 * kStages + 4 * kSBuf + 4;
     // + tmem slot, 1 KiB alignment slack
