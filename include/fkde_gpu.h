@@ -31,7 +31,10 @@
  * Multi-GPU: fkde_gpu_create(devices, n) drives n devices from one process
  * (one host thread per device, ncclCommInitAll); fkde_gpu_create_rank() is the
  * one-process-per-GPU form (torchrun), with the ncclUniqueId produced by
- * fkde_gpu_nccl_unique_id() on rank 0 and broadcast by the caller.  Sample
+ * fkde_gpu_nccl_unique_id() on rank 0 and broadcast by the caller.  NCCL is
+ * dlopen'ed on first multi-rank use: libnccl.so.2, or the library named by the
+ * FKDE_NCCL_LIB environment variable (a specific NCCL build, or the tests'
+ * in-process transport, tests/cpp/nccl_emu.cpp).  Sample
  * rows are sharded for the score pass, the debiased samples are gathered with
  * one ncclAllGather, and queries are sharded for the density pass.
  */
