@@ -90,7 +90,7 @@ struct TcConfig {
     // P.  The control warpgroup gives its registers to the epilogue warpgroups
     // (setmaxnreg), which is what makes four epilogue warps per sub-partition fit.
 #ifndef FKDE_EPI_NP
-#define FKDE_EPI_NP 3
+#define FKDE_EPI_NP 4
 #endif
 #ifndef FKDE_SCORE_NP
 #define FKDE_SCORE_NP 3
