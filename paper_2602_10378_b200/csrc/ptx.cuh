@@ -77,12 +77,6 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
-__device__ __forceinline__ uint64_t policy_evict_first() {
-    uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-
 // ---- fences -----------------------------------------------------------------
 // generic-proxy smem writes -> visible to the async proxy (tensor core reads)
 __device__ __forceinline__ void fence_proxy_async_smem() {
@@ -301,31 +295,6 @@ __device__ __forceinline__ uint32_t elect_one() {
     return pred;
 }
 
-// 2^t for a pair on the FMA pipe (no MUFU): t = j + f, j = rint(t) via the
-// 1.5*2^23 magic-number add, f in [-1/2, 1/2], 2^f by a degree-5 polynomial
-// (relative-error minimax fit, max rel. error 2^-22.0 in fp32 Horner -- the
-// same order as ex2.approx), 2^j added into the exponent field.  t is clamped
-// at -127 (result then < 2^-126, which the fp16 conversion flushes to 0).
-// Used for a fraction of the columns so the FMA pipe takes part of the
-// exponential load off the MUFU pipe (flash-attention-4's trick).
-__device__ __forceinline__ float2 ex2_poly2(float2 t) {
-    t.x = fmaxf(t.x, -127.f);
-    t.y = fmaxf(t.y, -127.f);
-    const float2 magic = make_float2(12582912.f, 12582912.f);
-    const float2 rm = fadd2(t, magic);                         // low bits hold rint(t)
-    const float2 r = fadd2(rm, make_float2(-12582912.f, -12582912.f));
-    const float2 f = fadd2(t, make_float2(-r.x, -r.y));
-    float2 p = ffma2(make_float2(1.327647129073739e-3f, 1.327647129073739e-3f), f,
-                     make_float2(9.675541892647743e-3f, 9.675541892647743e-3f));
-    p = ffma2(p, f, make_float2(5.550713092088699e-2f, 5.550713092088699e-2f));
-    p = ffma2(p, f, make_float2(2.4022120237350464e-1f, 2.4022120237350464e-1f));
-    p = ffma2(p, f, make_float2(6.931469440460205e-1f, 6.931469440460205e-1f));
-    p = ffma2(p, f, make_float2(1.0000001192092896f, 1.0000001192092896f));
-    // (bits(rm) << 23) == rint(t) << 23 (the magic's own bits shift out)
-    return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(rm.x) << 23)),
-                       __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(rm.y) << 23)));
-}
-
 // warpgroup-wide register reallocation (all four warps of a warpgroup execute it)
 template <int N>
 __device__ __forceinline__ void setmaxnreg_inc() {
@@ -336,11 +305,6 @@ __device__ __forceinline__ void setmaxnreg_dec() {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
 }
 
-// named barrier over `count` threads (multiple of 32)
-__device__ __forceinline__ void named_bar_sync(int id, int count) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
-
 // v = (a == b) ? x : v as a predicated select (keeps the compiler from
 // turning a per-lane dynamic index into a branch tree)
 __device__ __forceinline__ uint32_t sel_eq(uint32_t v, int a, int b, uint32_t x) {
@@ -349,13 +313,6 @@ __device__ __forceinline__ uint32_t sel_eq(uint32_t v, int a, int b, uint32_t x)
         : "=r"(r)
         : "r"(v), "r"(a), "r"(b), "r"(x));
     return r;
-}
-
-__device__ __forceinline__ void st_shared_v4(uint32_t saddr, uint32_t a, uint32_t b, uint32_t c,
-                                             uint32_t d) {
-    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(saddr), "r"(a), "r"(b), "r"(c),
-                 "r"(d)
-                 : "memory");
 }
 
 }  // namespace ptx
