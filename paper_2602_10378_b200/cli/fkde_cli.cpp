@@ -350,13 +350,18 @@ struct BandwidthPolicy {
 // ---------------------------------------------------------------- engine
 struct Engine {
     fkde_gpu_ctx* ctx = nullptr;
-    Engine() {
+    // --threads maps onto devices (the reference's worker cap, engine.hpp:33-38):
+    // 0 = every visible GPU (row / query shards + NCCL allgathers), k = the first k
+    explicit Engine(size_t threads = 0) {
         int devs = 0;
         if (fkde_gpu_device_count(&devs) != 0 || devs < 1)
             throw std::runtime_error("no CUDA device for the B200 engine");
-        const int dev0 = 0;
-        const int rc = fkde_gpu_create(&dev0, 1, &ctx);
-        if (rc != FKDE_OK) throw std::runtime_error("fkde_gpu_create failed (status " + std::to_string(rc) + ")");
+        const int use = threads == 0 ? devs : static_cast<int>(std::min<size_t>(threads, devs));
+        std::vector<int> ids(use);
+        for (int i = 0; i < use; ++i) ids[i] = i;
+        const int rc = fkde_gpu_create(ids.data(), use, &ctx);
+        if (rc != FKDE_OK) throw std::runtime_error("fkde_gpu_create on " + std::to_string(use) +
+                                                    " device(s) failed (status " + std::to_string(rc) + ")");
     }
     ~Engine() { fkde_gpu_destroy(ctx); }
     void check(int rc) const {
@@ -514,7 +519,7 @@ int run_estimate(const Args& a) {
     const size_t tile_m = a.has("--tile-m") ? positive(a.str("--tile-m"), "--tile-m") : 64;
     const size_t tile_n = a.has("--tile-n") ? positive(a.str("--tile-n"), "--tile-n") : 1024;
     const bool no_fuse = a.flag("--no-fuse");
-    if (a.has("--threads")) to_u64(a.str("--threads"), "--threads");   // engine: device count is the context's
+    const size_t threads = a.has("--threads") ? to_u64(a.str("--threads"), "--threads") : 0;
     const std::string out = a.req("--out"), format = a.str("--format", "csv");
     member(format, {"csv", "bin", "json"}, "--format");
 
@@ -523,7 +528,7 @@ int run_estimate(const Args& a) {
     const Method method = MethodSpec::parse(method_s).method;
     if (train.d != queries.d) throw NumericError("estimate: train and query dimensions differ");
     const auto h = bw.resolve(train, method);
-    Engine eng;
+    Engine eng(threads);
     const auto t0 = std::chrono::steady_clock::now();
     std::optional<double> neg;
     const std::vector<double> vals = eng.estimate(train, queries.data(), queries.n, train.d, method, h,
@@ -657,6 +662,7 @@ int run_bench(const Args& a) {
         for (const auto& t : split_list(a.str("--tile-n"))) tn_grid.push_back(positive(t, "--tile-n"));
     }
     const size_t repeats = a.has("--repeats") ? positive(a.str("--repeats"), "--repeats") : 5;
+    const size_t threads = a.has("--threads") ? to_u64(a.str("--threads"), "--threads") : 0;
     const std::string out = a.req("--out"), format = a.str("--format", "csv");
     member(format, {"csv", "json"}, "--format");
     const bool strict = a.flag("--strict");
@@ -693,7 +699,7 @@ int run_bench(const Args& a) {
                             r.mflops = model_flops(spec, mix.d, n, m);
                             r.exps = exp_count(spec, n, m);
                             try {
-                                if (!eng) eng = std::make_unique<Engine>();
+                                if (!eng) eng = std::make_unique<Engine>(threads);
                                 auto once = [&] {
                                     const auto h = bw.resolve(train, spec.method);
                                     eng->estimate(train, q.data(), m, mix.d, spec.method, h, tm, tn, spec.fused,
@@ -778,7 +784,7 @@ int run_bench(const Args& a) {
                         r.h = h.first;
                         r.hs = h.second;
                         if (n_eval < 2) throw NumericError("error_metrics: n_eval must be >= 2");
-                        if (!eng) eng = std::make_unique<Engine>();
+                        if (!eng) eng = std::make_unique<Engine>(threads);
                         if (grid) {   // trapezoid on [min(mu - 6 sigma), max(mu + 6 sigma)]
                             if (mix.d != 1) throw NumericError("error_metrics: Grid1D requires d == 1");
                             double lo = mix.means[0] - 6.0 * mix.sigmas[0], hi = mix.means[0] + 6.0 * mix.sigmas[0];
@@ -893,6 +899,7 @@ const char* kUsage =
     "  bench --mode runtime|error --config MIX.json --n-grid N1,N2 --out FILE [--methods ...]\n"
     "        [--seed S] [--seeds S1,S2] [--engines gpu] [--tile-m ...] [--tile-n ...]\n"
     "        [--repeats R] [--metric auto|grid|mc] [--n-eval E] [--hw SPEC] [--format csv|json] [--strict]\n"
+    "        [--threads K]   (estimate / bench: K GPUs, 0 = all visible)\n"
     "  model --d D --k K --hw SPEC [--tile-m M] [--tile-n N]\n";
 
 }  // namespace
