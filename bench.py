@@ -302,6 +302,16 @@ def run_ours(args):
                                       f"debiased samples, queries sharded",
                        "l2": "inputs larger than L2 (X fp64 128 MiB; B-operand tiles 128 MiB)"},
             "phases_ms": {"score_pass": score_avg, "density_pass": query_avg},
+            # the reference's own performance model of this run:
+            # paper-model pipeline FLOPs (4d+12+d/4+3/2) k^2 (perfmodel.cpp:62-67) and
+            # the runtime sweep's model_flops (sweep.cpp:74-90), with the utilization
+            # the reference's sweep would print against the B200 FP32 preset
+            "perf_model": {
+                "paper_flops": (4 * d + 12 + d / 4 + 1.5) * n * n,
+                "model_flops": (4 * d + 12) * n * n + (2 * d + 12) * n * m,
+                "utilization_vs_b200_fp32": ((4 * d + 12) * n * n + (2 * d + 12) * n * m)
+                / wall / 74.4e12,
+                "exp_count": float(n) * n + float(n) * m},
             "clocks": clocks,
             "e2e": {"value": m / e2e_s, "unit": "queries/s", "wall_s": e2e_s,
                     "h2d_bytes_per_step": (n + m) * d * 8,
