@@ -175,6 +175,12 @@ struct Device {
     DevBuf X, Y, opA, opB, part0, part1, xsd, out, aux0, aux1, colpart, scal, err, flags;
     cudaEvent_t ev[FKDE_T_COUNT + 1] = {};
     int64_t launches = 0;
+    // device-resident API: the call's whole device program as a CUDA graph,
+    // replayed while the arguments and options repeat (small problems are
+    // launch-bound: ~20 kernels per SD-KDE)
+    std::string graph_key, graph_seen;
+    cudaGraphExec_t graph = nullptr;
+    int64_t graph_launches = 0;
     float timing[FKDE_T_COUNT] = {};
     Status last;
 };
@@ -895,6 +901,7 @@ void fkde_gpu_destroy(fkde_gpu_ctx* ctx) {
             if (b->p) cudaFree(b->p);
         for (auto& e : D.ev)
             if (e) cudaEventDestroy(e);
+        if (D.graph) cudaGraphExecDestroy(D.graph);
         if (D.stream) cudaStreamDestroy(D.stream);
         if (D.side) cudaStreamDestroy(D.side);
         if (D.ev_side_in) cudaEventDestroy(D.ev_side_in);
@@ -1123,6 +1130,58 @@ int fkde_gpu_pairwise_sq_dists(fkde_gpu_ctx* ctx, const double* A, size_t na, co
     return finish(ctx, run_job(ctx->devs[0], ctx->opt, J));
 }
 
+namespace {
+// Device-resident jobs (J.sync == false, single rank): the first call with a
+// given argument/option set runs eagerly (and makes every allocation), the
+// second is captured into a CUDA graph, later ones replay it.
+Status run_device_job(fkde_gpu_ctx* ctx, const Job& J) {
+    Device& D = ctx->devs[0];
+    const Options& o = ctx->opt;
+    // (per-phase event timing and the debug trace run eagerly)
+    if (D.world != 1 || o.trace || o.timing) return run_job(D, o, J);
+    char buf[512];
+    std::snprintf(buf, sizeof(buf), "%d|%p|%p|%p|%zu|%zu|%d|%a|%a|%d|%d|%d|%d|%d|%d|%d", J.kind,
+                  (const void*)J.dX, (const void*)J.dY, (void*)J.d_out, J.n, J.m, J.d, J.h,
+                  J.h_score, J.kernel, J.fused, o.engine, o.splits, o.timing, o.max_ctas,
+                  o.flush_tiles);
+    const std::string key(buf);
+    CUDA_TRY(cudaSetDevice(D.dev));
+    if (D.graph && key == D.graph_key) {
+        CUDA_TRY(cudaGraphLaunch(D.graph, D.stream));
+        D.launches = D.graph_launches;
+        return {};
+    }
+    if (key != D.graph_seen) {   // first sighting: eager
+        D.graph_seen = key;
+        return run_job(D, o, J);
+    }
+    if (D.graph) {
+        cudaGraphExecDestroy(D.graph);
+        D.graph = nullptr;
+        D.graph_key.clear();
+    }
+    cudaGraph_t g = nullptr;
+    CUDA_TRY(cudaStreamBeginCapture(D.stream, cudaStreamCaptureModeThreadLocal));
+    Status s = run_job(D, o, J);
+    const cudaError_t ce = cudaStreamEndCapture(D.stream, &g);
+    if (!s.ok()) {
+        if (g) cudaGraphDestroy(g);
+        return s;
+    }
+    if (ce != cudaSuccess) return make_status(FKDE_CUDA_ERROR, "stream capture: %s", cudaGetErrorString(ce));
+    const cudaError_t ie = cudaGraphInstantiate(&D.graph, g, 0);
+    cudaGraphDestroy(g);
+    if (ie != cudaSuccess) {
+        D.graph = nullptr;
+        return make_status(FKDE_CUDA_ERROR, "graph instantiate: %s", cudaGetErrorString(ie));
+    }
+    D.graph_key = key;
+    D.graph_launches = D.launches;
+    CUDA_TRY(cudaGraphLaunch(D.graph, D.stream));
+    return {};
+}
+}  // namespace
+
 int fkde_gpu_sdkde_device(fkde_gpu_ctx* ctx, const double* dX, size_t n, const double* dY,
                           size_t m, size_t d, double h, double h_score, double* d_out) {
     if (!ctx) return FKDE_INVALID_ARGUMENT;
@@ -1144,7 +1203,7 @@ int fkde_gpu_sdkde_device(fkde_gpu_ctx* ctx, const double* dX, size_t n, const d
     J.d_out = d_out;
     J.sync = false;
     std::lock_guard<std::mutex> lock(ctx->mu);
-    return finish(ctx, run_job(ctx->devs[0], ctx->opt, J));
+    return finish(ctx, run_device_job(ctx, J));
 }
 
 int fkde_gpu_kde_device(fkde_gpu_ctx* ctx, const double* dX, size_t n, const double* dY,
@@ -1167,7 +1226,7 @@ int fkde_gpu_kde_device(fkde_gpu_ctx* ctx, const double* dX, size_t n, const dou
     J.d_out = d_out;
     J.sync = false;
     std::lock_guard<std::mutex> lock(ctx->mu);
-    return finish(ctx, run_job(ctx->devs[0], ctx->opt, J));
+    return finish(ctx, run_device_job(ctx, J));
 }
 
 }  // extern "C"

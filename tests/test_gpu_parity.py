@@ -452,3 +452,38 @@ def test_config3_plain_kde_32k_subsample(ctx, port):
     ref = port.kde_naive(tr, q[qs], h, threads=os.cpu_count())
     assert max_component_rel(v[qs], ref) < TOL_DENS
     assert max_log_rel(v[qs], ref) < 1e-3
+
+
+def test_device_api_graph_replay_is_bitwise(ctx, port):
+    # the device-resident API runs a call eagerly, captures the repeat into a CUDA
+    # graph and replays it afterwards: all three must give the same bits, and a
+    # changed argument must fall back to eager execution
+    import torch
+    tr, q = _mixture_inputs(port, 3000, 700)
+    dX = torch.from_numpy(tr).cuda()
+    dY = torch.from_numpy(q).cuda()
+    lib = N.load()
+    stream = torch.cuda.ExternalStream(ctx.stream())
+    outs = []
+    for h in (1.3, 1.3, 1.3, 1.3, 1.1, 1.3):
+        dO = torch.zeros(700, dtype=torch.float64, device="cuda") if not outs else outs_buf
+        outs_buf = dO
+        rc = lib.fkde_gpu_sdkde_device(ctx.handle, dX.data_ptr(), 3000, dY.data_ptr(), 700, 16, h, h,
+                                       dO.data_ptr())
+        assert rc == 0, ctx.last_error()
+        stream.synchronize()
+        outs.append(dO.cpu().numpy().copy())
+    assert all(np.array_equal(outs[0], o) for o in (outs[1], outs[2], outs[3], outs[5]))
+    assert not np.array_equal(outs[0], outs[4])
+    host = fk.sdkde_flash(tr, q, fk.Bandwidth.uniform(1.3), ctx=ctx).values
+    assert np.array_equal(outs[0], host)
+    for kind in (0, 1):   # KDE / Laplace through the graph path too
+        dO2 = torch.zeros(700, dtype=torch.float64, device="cuda")
+        res = []
+        for _ in range(3):
+            rc = lib.fkde_gpu_kde_device(ctx.handle, dX.data_ptr(), 3000, dY.data_ptr(), 700, 16, 1.2,
+                                         kind, 1, dO2.data_ptr())
+            assert rc == 0, ctx.last_error()
+            stream.synchronize()
+            res.append(dO2.cpu().numpy().copy())
+        assert np.array_equal(res[0], res[1]) and np.array_equal(res[0], res[2])
