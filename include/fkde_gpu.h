@@ -145,9 +145,15 @@ int fkde_gpu_pairwise_sq_dists(fkde_gpu_ctx* ctx, const double* A, size_t na, co
 
 /* ---- device-resident variants (single-device contexts) -------------------
  * Pointers are device memory on the context's device; work is enqueued on
- * fkde_gpu_stream(ctx) and the call returns without synchronising. */
+ * fkde_gpu_stream(ctx) and the call returns without synchronising.  A call
+ * repeated with identical arguments and options is captured into a CUDA
+ * graph on its second occurrence and replayed from the third on. */
 int fkde_gpu_sdkde_device(fkde_gpu_ctx* ctx, const double* dX, size_t n, const double* dY,
                           size_t m, size_t d, double h, double h_score, double* d_out);
+/* scores (n x d) of device-resident samples; rows whose score denominator
+ * underflows are not reported here (use fkde_gpu_score for the error index) */
+int fkde_gpu_score_device(fkde_gpu_ctx* ctx, const double* dX, size_t n, size_t d, double h_score,
+                          double* d_scores);
 int fkde_gpu_kde_device(fkde_gpu_ctx* ctx, const double* dX, size_t n, const double* dY,
                         size_t m, size_t d, double h, int kernel, int fused, double* d_out);
 

@@ -39,7 +39,7 @@ EXPORTED_SYMBOLS = (
     "fkde_gpu_world", "fkde_gpu_stream", "fkde_gpu_last_timing", "fkde_gpu_last_launch_count",
     "fkde_gpu_score", "fkde_gpu_score_accumulate", "fkde_gpu_kde", "fkde_gpu_sdkde",
     "fkde_gpu_estimate", "fkde_gpu_pairwise_sq_dists", "fkde_gpu_sdkde_device",
-    "fkde_gpu_kde_device", "fkde_gpu_shard_range",
+    "fkde_gpu_kde_device", "fkde_gpu_score_device", "fkde_gpu_shard_range",
 )
 HOST_SYMBOLS = (
     "fkde_host_mix64", "fkde_host_random_gaussian", "fkde_host_sample_mixture",
@@ -92,6 +92,7 @@ def _declare(lib):
     lib.fkde_gpu_pairwise_sq_dists.argtypes = [_vp, _dp, _sz, _dp, _sz, _sz, _dp]
     lib.fkde_gpu_sdkde_device.argtypes = [_vp, _vp, _sz, _vp, _sz, _sz, ctypes.c_double,
                                           ctypes.c_double, _vp]
+    lib.fkde_gpu_score_device.argtypes = [_vp, _vp, _sz, _sz, ctypes.c_double, _vp]
     lib.fkde_gpu_kde_device.argtypes = [_vp, _vp, _sz, _vp, _sz, _sz, ctypes.c_double,
                                         ctypes.c_int, ctypes.c_int, _vp]
     lib.fkde_gpu_shard_range.argtypes = [_sz, ctypes.c_int, ctypes.c_int, _sz, _szp, _szp, _szp]

@@ -705,6 +705,9 @@ Status run_job(Device& D, const Options& o, const Job& J) {
         if (J.kind == Job::kSdkde && J.out2)   // the side-stream copy joins the main stream
             CUDA_TRY(cudaStreamWaitEvent(D.stream, D.ev_side_out, 0));
     } else if (J.kind == Job::kScore) {   // (host outputs only on the first device)
+        if (J.d_out)
+            CUDA_TRY(cudaMemcpyAsync(J.d_out, D.aux0.p, nd * sizeof(double),
+                                     cudaMemcpyDeviceToDevice, D.stream));
         if (J.out)
             CUDA_TRY(cudaMemcpyAsync(J.out, D.aux0.p, nd * sizeof(double), cudaMemcpyDeviceToHost,
                                      D.stream));
@@ -1201,6 +1204,29 @@ int fkde_gpu_sdkde_device(fkde_gpu_ctx* ctx, const double* dX, size_t n, const d
     J.h = h;
     J.h_score = h_score;
     J.d_out = d_out;
+    J.sync = false;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    return finish(ctx, run_device_job(ctx, J));
+}
+
+int fkde_gpu_score_device(fkde_gpu_ctx* ctx, const double* dX, size_t n, size_t d, double h_score,
+                          double* d_scores) {
+    if (!ctx) return FKDE_INVALID_ARGUMENT;
+    if (ctx->devs.size() != 1)
+        return finish(ctx, make_status(FKDE_INVALID_ARGUMENT, "device API needs a 1-device context"));
+    Status s = validate_set(dX, n, d, "score train");
+    if (s.ok() && !finite_h(h_score))
+        s = make_status(FKDE_INVALID_ARGUMENT, "score_flash: h_score must be positive and finite");
+    if (s.ok() && !d_scores) s = make_status(FKDE_INVALID_ARGUMENT, "score_flash: null output");
+    if (!s.ok()) return finish(ctx, s);
+    Job J;
+    J.kind = Job::kScore;
+    J.dX = dX;
+    J.n = n;
+    J.d = static_cast<int>(d);
+    J.h = h_score;
+    J.h_score = h_score;
+    J.d_out = d_scores;
     J.sync = false;
     std::lock_guard<std::mutex> lock(ctx->mu);
     return finish(ctx, run_device_job(ctx, J));

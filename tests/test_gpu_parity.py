@@ -487,3 +487,20 @@ def test_device_api_graph_replay_is_bitwise(ctx, port):
             stream.synchronize()
             res.append(dO2.cpu().numpy().copy())
         assert np.array_equal(res[0], res[1]) and np.array_equal(res[0], res[2])
+
+
+def test_score_device_api_matches_host_api(ctx, port):
+    import torch
+    tr, _ = _mixture_inputs(port, 2500, 8)
+    host = fk.score_flash(tr, 1.4, ctx=ctx).values
+    dX = torch.from_numpy(tr).cuda()
+    dS = torch.zeros((2500, 16), dtype=torch.float64, device="cuda")
+    lib = N.load()
+    stream = torch.cuda.ExternalStream(ctx.stream())
+    for _ in range(3):   # eager, captured, replayed
+        dS.zero_()
+        torch.cuda.synchronize()
+        rc = lib.fkde_gpu_score_device(ctx.handle, dX.data_ptr(), 2500, 16, 1.4, dS.data_ptr())
+        assert rc == 0, ctx.last_error()
+        stream.synchronize()
+        assert np.array_equal(dS.cpu().numpy(), host)
