@@ -4,7 +4,7 @@
 // call sites:
 //
 //   fkde::gpu::score_accumulate / score_flash / kde_flash / sdkde_flash /
-//   pairwise_sq_dists_block / estimate
+//   pairwise_sq_dists_block / estimate, and fkde::gpu::io (the io.hpp file formats)
 //
 // Same argument meaning, same validation order, same exception types
 // (errors.hpp:10-56): the facade validates on the host exactly like the
@@ -29,6 +29,7 @@
 #include <vector>
 
 #include "../fkde_gpu.h"
+#include "../fkde_io.h"
 
 #ifdef FKDE_B200_USE_REFERENCE_TYPES
 #include "fkde/engine.hpp"
@@ -44,6 +45,10 @@ public:
 class DimensionMismatchError : public InvalidArgumentError {
 public:
     using InvalidArgumentError::InvalidArgumentError;
+};
+class IoError : public std::runtime_error {  // errors.hpp:53
+public:
+    using std::runtime_error::runtime_error;
 };
 class ScoreUnderflowError : public std::runtime_error {
 public:
@@ -319,6 +324,47 @@ inline DensityResult estimate(const SampleSet& train, const SampleSet& queries,
     }
     throw InvalidArgumentError("estimate: unknown method");
 }
+
+// fkde::io (io.hpp:11-38) over fkde_io.h: same formats byte for byte, same
+// exceptions; read_samples can stage the file through page-locked memory.
+namespace io {
+namespace detail {
+inline void check(int rc) {
+    if (rc == FKDE_IO_OK) return;
+    const std::string msg = fkde_io_last_error();
+    if (rc == FKDE_IO_INVALID_ARGUMENT) throw InvalidArgumentError(msg);
+    throw IoError(msg);
+}
+}  // namespace detail
+
+inline SampleSet read_samples(const std::string& path, bool pinned = false) {  // io.cpp:177-190
+    double* p = nullptr;
+    std::size_t n = 0, d = 0;
+    int pin = pinned ? 1 : 0;
+    detail::check(fkde_io_read_samples(path.c_str(), &p, &n, &d, &pin));
+    std::vector<double> v(p, p + n * d);
+    fkde_io_free(p, pin);
+    return SampleSet(std::move(v), n, d);
+}
+inline void write_samples_bin(const SampleSet& s, const std::string& path) {
+    detail::check(fkde_io_write_samples_bin(path.c_str(), s.values.data(), s.n, s.d));
+}
+inline void write_samples_csv(const SampleSet& s, const std::string& path) {
+    detail::check(fkde_io_write_samples_csv(path.c_str(), s.values.data(), s.n, s.d));
+}
+inline void write_values(const std::vector<double>& values, const std::string& path,
+                         const std::string& format) {
+    detail::check(fkde_io_write_values(path.c_str(), values.data(), values.size(), format.c_str()));
+}
+inline std::vector<double> read_values(const std::string& path) {
+    double* p = nullptr;
+    std::size_t m = 0;
+    detail::check(fkde_io_read_values(path.c_str(), &p, &m));
+    std::vector<double> v(p, p + m);
+    fkde_io_free(p, 0);
+    return v;
+}
+}  // namespace io
 
 }  // namespace gpu
 }  // namespace fkde

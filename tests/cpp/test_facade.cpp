@@ -45,6 +45,24 @@ static SampleSet random_set(std::size_t n, std::size_t d, unsigned seed, double 
 
 int main(int argc, char** argv) {
     const bool gpu = argc > 1 && std::strcmp(argv[1], "gpu") == 0;
+    // ---- fkde::gpu::io: reference file formats (test_io.cpp:31-102) ----
+    {
+        const auto s = random_set(33, 4, 9, 1e3);
+        const std::string bin = "/tmp/fkde_facade_io.bin", csv = "/tmp/fkde_facade_io.csv",
+                          val = "/tmp/fkde_facade_io_v.json";
+        gpu::io::write_samples_bin(s, bin);
+        gpu::io::write_samples_csv(s, csv);
+        const auto r1 = gpu::io::read_samples(bin), r2 = gpu::io::read_samples(csv, true);
+        EXPECT(r1.n == 33 && r1.d == 4 && r1.values == s.values);
+        EXPECT(r2.values == s.values);
+        gpu::io::write_values(s.values, val, "json");
+        EXPECT(gpu::io::read_values(val) == s.values);
+        EXPECT(throws<IoError>([&] { gpu::io::read_samples("/tmp/definitely_missing_fkde.bin"); }));
+        EXPECT(throws<InvalidArgumentError>([&] { gpu::io::write_values({1.0}, val, "xml"); }));
+        std::remove(bin.c_str());
+        std::remove(csv.c_str());
+        std::remove(val.c_str());
+    }
     // ---- validation (types.cpp / engine.cpp semantics), no device touched ----
     const auto a = random_set(10, 2, 1), b = random_set(10, 3, 2);
     const engine::TilePlan plan{64, 1024, 1, 1};
