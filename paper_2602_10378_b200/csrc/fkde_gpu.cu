@@ -141,9 +141,14 @@ struct DevBuf {
     T* as() const { return static_cast<T*>(p); }
 };
 
+// bumped on every workspace (re)allocation: a captured CUDA graph holds raw
+// workspace pointers and is only replayed while this is unchanged
+std::atomic<uint64_t> g_alloc_epoch{0};
+
 Status ensure(DevBuf& b, size_t bytes) {
     if (bytes == 0) bytes = 16;
     if (b.bytes >= bytes) return {};
+    g_alloc_epoch.fetch_add(1);
     if (b.p) cudaFree(b.p);
     b.p = nullptr;
     b.bytes = 0;
@@ -181,6 +186,7 @@ struct Device {
     std::string graph_key, graph_seen;
     cudaGraphExec_t graph = nullptr;
     int64_t graph_launches = 0;
+    uint64_t graph_epoch = 0;   // g_alloc_epoch when the graph was captured
     float timing[FKDE_T_COUNT] = {};
     Status last;
 };
@@ -1149,7 +1155,7 @@ Status run_device_job(fkde_gpu_ctx* ctx, const Job& J) {
                   o.flush_tiles);
     const std::string key(buf);
     CUDA_TRY(cudaSetDevice(D.dev));
-    if (D.graph && key == D.graph_key) {
+    if (D.graph && key == D.graph_key && D.graph_epoch == g_alloc_epoch.load()) {
         CUDA_TRY(cudaGraphLaunch(D.graph, D.stream));
         D.launches = D.graph_launches;
         return {};
@@ -1180,6 +1186,7 @@ Status run_device_job(fkde_gpu_ctx* ctx, const Job& J) {
     }
     D.graph_key = key;
     D.graph_launches = D.launches;
+    D.graph_epoch = g_alloc_epoch.load();
     CUDA_TRY(cudaGraphLaunch(D.graph, D.stream));
     return {};
 }

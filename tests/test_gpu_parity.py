@@ -477,6 +477,16 @@ def test_device_api_graph_replay_is_bitwise(ctx, port):
     assert not np.array_equal(outs[0], outs[4])
     host = fk.sdkde_flash(tr, q, fk.Bandwidth.uniform(1.3), ctx=ctx).values
     assert np.array_equal(outs[0], host)
+    # a bigger problem in between grows (reallocates) the context's workspaces: the
+    # graph captured for the first call must not be replayed with stale pointers
+    big, bq = _mixture_inputs(port, 9000, 1500)
+    fk.sdkde_flash(big, bq, fk.Bandwidth.uniform(1.3), ctx=ctx)
+    for _ in range(3):
+        rc = lib.fkde_gpu_sdkde_device(ctx.handle, dX.data_ptr(), 3000, dY.data_ptr(), 700, 16, 1.3, 1.3,
+                                       outs_buf.data_ptr())
+        assert rc == 0, ctx.last_error()
+        stream.synchronize()
+        assert np.array_equal(outs_buf.cpu().numpy(), outs[0])
     for kind in (0, 1):   # KDE / Laplace through the graph path too
         dO2 = torch.zeros(700, dtype=torch.float64, device="cuda")
         res = []
