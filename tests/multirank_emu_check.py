@@ -49,6 +49,40 @@ def main():
     multi.close()
     out["multi_device"] = {k: float(np.max(np.abs(got[k] - ref[k]))) for k in ref}
 
+    # device-resident API per rank (what bench.py drives under torchrun)
+    import torch
+    dX = torch.from_numpy(X).cuda()
+    dY = torch.from_numpy(Y).cuda()
+    lib = N.load()
+    uid_d = fk.engine.nccl_unique_id()
+    dev_res, dev_errs = [None] * world, []
+
+    def rank_dev(r):
+        try:
+            c = fk.Context(rank=r, world=world, device=0, nccl_id=uid_d)
+            c.set_option(N.OPT_SPLITS, splits)
+            dO = torch.zeros(m, dtype=torch.float64, device="cuda")
+            for _ in range(2):
+                rc = lib.fkde_gpu_sdkde_device(c.handle, dX.data_ptr(), n, dY.data_ptr(), m, 16, h, h,
+                                               dO.data_ptr())
+                if rc != 0:
+                    raise RuntimeError(c.last_error())
+                torch.cuda.ExternalStream(c.stream()).synchronize()
+            dev_res[r] = dO.cpu().numpy()
+            c.close()
+        except Exception as e:  # noqa: BLE001
+            dev_errs.append(repr(e))
+
+    th = [threading.Thread(target=rank_dev, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if dev_errs:
+        out["device_api_error"] = dev_errs
+    else:
+        out["device_api"] = [float(np.max(np.abs(dev_res[r] - ref["sdkde"]))) for r in range(world)]
+
     uid = fk.engine.nccl_unique_id()          # one context per rank, one thread each
     res, errs = [None] * world, []
 

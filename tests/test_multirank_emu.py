@@ -42,6 +42,8 @@ def test_multirank_path_is_bitwise_single_device(emu_lib, n, m, world, splits):
     res = json.loads(r.stdout.strip().splitlines()[-1])
     print(res)
     assert "per_rank_error" not in res, res
+    assert "device_api_error" not in res, res
+    assert all(v == 0.0 for v in res["device_api"]), res
     for form in [res["multi_device"]] + res["per_rank"]:
         for k, v in form.items():
             assert v == 0.0, (k, v, res)
