@@ -399,11 +399,11 @@ def test_config5_headline_subsample(ctx, port):
     r = fk.sdkde_flash(tr, q, fk.Bandwidth.uniform(h), ctx=ctx)
     v, deb = r.values, r.debiased_samples.values
     assert np.isfinite(v).all() and (v > 0).all()
-    rows = np.linspace(0, n - 1, 24).astype(int)
+    rows = np.linspace(0, n - 1, 4096).astype(int)
     sc = port.score_naive(tr, tr[rows], h, threads=os.cpu_count())
     ref_deb = tr[rows] + 0.5 * h * h * sc
     assert max_rowwise_rel(deb[rows], ref_deb) < TOL_DEB
-    qs = np.linspace(0, m - 1, 48).astype(int)
+    qs = np.linspace(0, m - 1, 4096).astype(int)
     ref_v = port.kde_naive(deb, q[qs], h, threads=os.cpu_count())
     assert max_component_rel(v[qs], ref_v) < TOL_DENS
     assert max_log_rel(v[qs], ref_v) < 1e-3
@@ -415,7 +415,7 @@ def test_config4_laplace_subsample(ctx, port):
     tr, q = _mixture_inputs(port, n, m)
     h = port.silverman_bandwidth(tr)
     v = fk.kde_flash(tr, q, h, fk.KernelKind.LaplaceCorrected, True, ctx=ctx).values
-    qs = np.linspace(0, m - 1, 64).astype(int)
+    qs = np.linspace(0, m - 1, 2048).astype(int)
     ref = port.laplace_naive(tr, q[qs], h, threads=os.cpu_count())
     assert max_rel_vs_peak(v[qs], ref) < TOL_LAP
 
