@@ -67,7 +67,8 @@ enum { FKDE_METHOD_KDE = 0, FKDE_METHOD_SDKDE = 1, FKDE_METHOD_LAPLACE = 2 };
 
 /* options (fkde_gpu_set_option) */
 enum {
-    FKDE_OPT_ENGINE = 1,      /* FKDE_ENGINE_TC (default) | FKDE_ENGINE_SIMT     */
+    FKDE_OPT_ENGINE = 1,      /* FKDE_ENGINE_TC (the only engine; kept for ABI
+                                 stability, any other value is rejected)         */
     FKDE_OPT_SPLITS = 2,      /* 0 = auto; >0 forces column splits per row tile  */
     FKDE_OPT_TIMING = 3,      /* 1 = record per-phase CUDA-event times            */
     FKDE_OPT_MAX_CTAS = 4,    /* 0 = all SMs; >0 caps the persistent grid        */
@@ -78,7 +79,7 @@ enum {
     FKDE_OPT_TRACE_PTR = 6    /* debug: device pointer (32*8*256 int64) receiving
                                  clock64 stamps of the score kernel's block 0   */
 };
-enum { FKDE_ENGINE_TC = 0, FKDE_ENGINE_SIMT = 1 };
+enum { FKDE_ENGINE_TC = 0 };
 
 /* per-phase timings (fkde_gpu_last_timing), milliseconds, rank-local */
 enum {
@@ -96,11 +97,15 @@ typedef struct fkde_gpu_ctx fkde_gpu_ctx;
 
 /* ---- lifecycle ---------------------------------------------------------- */
 int fkde_gpu_device_count(int* count);
+/* devices: distinct ids in [0, device count), or NULL for 0..n_devices-1 */
 int fkde_gpu_create(const int* devices, int n_devices, fkde_gpu_ctx** out);
 int fkde_gpu_nccl_unique_id(unsigned char id[128]);
 int fkde_gpu_create_rank(int device, int rank, int world, const unsigned char id[128],
                          fkde_gpu_ctx** out);
 void fkde_gpu_destroy(fkde_gpu_ctx* ctx);
+/* message of the calling thread's last call on ctx (or, if this thread made
+ * none, a private copy of the context's most recent message); the pointer
+ * stays valid until this thread's next call on ctx */
 const char* fkde_gpu_last_error(const fkde_gpu_ctx* ctx);
 int fkde_gpu_set_option(fkde_gpu_ctx* ctx, int key, int64_t value);
 int fkde_gpu_world(const fkde_gpu_ctx* ctx, int* rank, int* world);
@@ -147,7 +152,12 @@ int fkde_gpu_pairwise_sq_dists(fkde_gpu_ctx* ctx, const double* A, size_t na, co
  * Pointers are device memory on the context's device; work is enqueued on
  * fkde_gpu_stream(ctx) and the call returns without synchronising.  A call
  * repeated with identical arguments and options is captured into a CUDA
- * graph on its second occurrence and replayed from the third on. */
+ * graph on its second occurrence and replayed from the third on.
+ * Host-side argument checks are the same as the host entry points (null
+ * pointers, sizes, d, h, kernel kind); because nothing is read back, these
+ * calls NEVER report FKDE_NON_FINITE (NaN/Inf inputs) or
+ * FKDE_SCORE_UNDERFLOW -- use the host entry points when those diagnostics
+ * matter. */
 int fkde_gpu_sdkde_device(fkde_gpu_ctx* ctx, const double* dX, size_t n, const double* dY,
                           size_t m, size_t d, double h, double h_score, double* d_out);
 /* scores (n x d) of device-resident samples; rows whose score denominator

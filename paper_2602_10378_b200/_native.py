@@ -29,7 +29,7 @@ KERNEL_LAPLACE_CORRECTED = 1
 METHOD_KDE, METHOD_SDKDE, METHOD_LAPLACE = 0, 1, 2
 
 OPT_ENGINE, OPT_SPLITS, OPT_TIMING, OPT_MAX_CTAS, OPT_FLUSH_TILES = 1, 2, 3, 4, 5
-ENGINE_TC, ENGINE_SIMT = 0, 1
+ENGINE_TC = 0
 
 T_PREP, T_SCORE, T_FINALIZE, T_GATHER, T_QUERY, T_REDUCE, T_TOTAL, T_COUNT = range(8)
 

@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libfkde_b200.so")
 SOURCES = ["fkde_gpu.cu", "host_fixtures.cpp", "host_io.cpp"]
-HEADERS = ["ptx.cuh", "layout.cuh", "pairwise_tc.cuh", "pairwise_simt.cuh", "prep_kernels.cuh"]
+HEADERS = ["ptx.cuh", "layout.cuh", "pairwise_tc.cuh", "prep_kernels.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -49,7 +49,7 @@ def build(force: bool = False, verbose: bool = False, out: str = OUT, defines=()
     if out == OUT and not defines and not force and not _stale():
         return OUT
     cmd = [nvcc()] + NVCC_FLAGS + (["-Xptxas", "-v"] if verbose else []) + \
-        ["-D" + d for d in defines] + \
+        ["-D" + d for d in defines] + ["-I", json_include()] + \
         ["-o", out] + [os.path.join(CSRC, s) for s in SOURCES] + ["-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

@@ -33,7 +33,6 @@
 
 #include "../../include/fkde_gpu.h"
 #include "layout.cuh"
-#include "pairwise_simt.cuh"
 #include "pairwise_tc.cuh"
 #include "prep_kernels.cuh"
 
@@ -198,16 +197,31 @@ struct fkde_gpu_ctx {
     int world = 1;
     bool per_rank = false;  // one process per GPU
     Options opt;
-    std::string err;
-    std::mutex mu;
+    std::mutex mu;          // serialises calls (device state, workspaces, graphs)
+    std::mutex err_mu;      // guards err (written by every call's finish())
+    std::string err;        // message of the most recent call on this context
 };
 
 namespace {
 
-Status set_error(fkde_gpu_ctx* ctx, Status s) {
-    if (ctx) ctx->err = s.msg;
-    return s;
+// Per-thread copy of the last message a thread produced (or read) for a
+// context: fkde_gpu_last_error hands out a pointer that no other thread can
+// invalidate, and a thread sees the outcome of its own last call even when
+// other threads share the context.
+struct ErrSlot {
+    const fkde_gpu_ctx* ctx;
+    std::string msg;
+};
+thread_local std::vector<ErrSlot> t_errors;
+
+std::string& thread_error_slot(const fkde_gpu_ctx* ctx) {
+    for (auto& e : t_errors)
+        if (e.ctx == ctx) return e.msg;
+    if (t_errors.size() >= 16) t_errors.erase(t_errors.begin());
+    t_errors.push_back({ctx, std::string()});
+    return t_errors.back().msg;
 }
+
 
 // shard [r*chunk, min(n,(r+1)*chunk)) with chunk = ceil(n/world): equal-size
 // allgather slices (the tail slice is padding).
@@ -247,9 +261,7 @@ int choose_splits(const Options& o, size_t row_tiles, size_t col_tiles, int ctas
 
 template <int MODE>
 Status launch_pairwise(Device& D, const Options& o, const PairArgs& a, size_t n_cols) {
-    if (o.engine == FKDE_ENGINE_SIMT) {
-        pairwise_simt_kernel<MODE><<<a.n_row_tiles, 128, 0, D.stream>>>(a, n_cols);
-    } else {
+    {
         using Cfg = TcConfig<MODE>;
         static thread_local int attr_done_dev[64] = {};
         if (!(attr_done_dev[D.dev & 63] & (1 << MODE))) {
@@ -315,13 +327,10 @@ Status density_pass(Device& D, const Options& o, int mode, size_t rows_pad, size
                     const PassScalars* sc, int* nparts_out) {
     const size_t rt = rows_pad / kTileRows;
     const size_t ct = round_up(n_cols, kTileRows) / kTileRows;
-    int splits = o.engine == FKDE_ENGINE_SIMT ? 1
-                                              : choose_splits(o, rt, ct, o.max_ctas > 0
-                                                                             ? std::min(o.max_ctas, D.num_sms)
-                                                                             : D.num_sms);
-    // partial sums per (split, row): SIMT writes 2 (column halves), the tensor-core
-    // kernel one per epilogue tile phase
-    const size_t per = o.engine == FKDE_ENGINE_SIMT ? 2 : TcConfig<kModeGauss>::kNP;
+    const int splits =
+        choose_splits(o, rt, ct, o.max_ctas > 0 ? std::min(o.max_ctas, D.num_sms) : D.num_sms);
+    // partial sums per (split, row): one per epilogue tile phase
+    const size_t per = TcConfig<kModeGauss>::kNP;
     const size_t nparts = static_cast<size_t>(splits) * per;
     STATUS_TRY(ensure(D.part0, nparts * rows_pad * sizeof(float)));
     if (mode == kModeLaplace) STATUS_TRY(ensure(D.part1, nparts * rows_pad * sizeof(float)));
@@ -413,9 +422,9 @@ Status score_program(Device& D, const Options& o, const Job& J, const double* dX
     record(D, o, FKDE_T_SCORE);
 
     const size_t rt = rows_pad / kTileRows;
-    const size_t ct = cols_pad / (o.engine == FKDE_ENGINE_SIMT ? kTileRows : kScoreNCol);
+    const size_t ct = cols_pad / kScoreNCol;
     const int ctas = o.max_ctas > 0 ? std::min(o.max_ctas, D.num_sms) : D.num_sms;
-    const int splits = o.engine == FKDE_ENGINE_SIMT ? 1 : choose_splits(o, rt, ct, ctas);
+    const int splits = choose_splits(o, rt, ct, ctas);
     // fp64 partials per split
     STATUS_TRY(ensure(D.part0, static_cast<size_t>(splits) * rows_pad * sizeof(double)));
     STATUS_TRY(ensure(D.part1, static_cast<size_t>(splits) * rows_pad * kMaxDim * sizeof(double)));
@@ -651,6 +660,9 @@ Status run_job(Device& D, const Options& o, const Job& J) {
         dY = D.Y.as<double>();
     }
     STATUS_TRY(ensure(D.scal, 2 * sizeof(PassScalars)));
+    // both slots start clean on every call: the non-finite flags read back below
+    // must describe this call's inputs only, whichever slots the job writes
+    CUDA_TRY(cudaMemsetAsync(D.scal.p, 0, 2 * sizeof(PassScalars), D.stream));
     PassScalars* sc_s = D.scal.as<PassScalars>();
     PassScalars* sc_q = sc_s + 1;
 
@@ -752,7 +764,7 @@ Status run_job(Device& D, const Options& o, const Job& J) {
 // the single-process multi-device case).  Host outputs are written by device 0.
 Status run_all(fkde_gpu_ctx* ctx, const Job& J) {
     std::lock_guard<std::mutex> lock(ctx->mu);
-    if (ctx->devs.size() == 1) return set_error(ctx, run_job(ctx->devs[0], ctx->opt, J));
+    if (ctx->devs.size() == 1) return run_job(ctx->devs[0], ctx->opt, J);
     std::vector<Status> st(ctx->devs.size());
     std::vector<std::thread> th;
     for (size_t i = 0; i < ctx->devs.size(); ++i) {
@@ -765,8 +777,8 @@ Status run_all(fkde_gpu_ctx* ctx, const Job& J) {
     }
     for (auto& t : th) t.join();
     for (auto& s : st)
-        if (!s.ok()) return set_error(ctx, s);
-    return set_error(ctx, {});
+        if (!s.ok()) return s;
+    return {};
 }
 
 bool finite_h(double h) { return h > 0.0 && std::isfinite(h); }
@@ -781,7 +793,11 @@ Status validate_set(const void* p, size_t n, size_t d, const char* what) {
 }
 
 int finish(fkde_gpu_ctx* ctx, const Status& s, size_t* err_index = nullptr) {
-    if (ctx) ctx->err = s.msg;
+    if (ctx) {
+        std::lock_guard<std::mutex> lock(ctx->err_mu);
+        ctx->err = s.msg;
+        thread_error_slot(ctx) = s.msg;
+    }
     if (err_index && s.code == FKDE_SCORE_UNDERFLOW) *err_index = s.index;
     return s.code;
 }
@@ -833,12 +849,17 @@ int fkde_gpu_create(const int* devices, int n_devices, fkde_gpu_ctx** out) {
     *out = nullptr;
     int count = 0;
     if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) return FKDE_NO_DEVICE;
-    auto* ctx = new fkde_gpu_ctx();
-    ctx->devs.resize(n_devices);
-    ctx->world = n_devices;
     std::vector<int> ids(n_devices);
     for (int i = 0; i < n_devices; ++i) {
         ids[i] = devices ? devices[i] : i;
+        if (ids[i] < 0 || ids[i] >= count) return FKDE_INVALID_ARGUMENT;
+        for (int j = 0; j < i; ++j)
+            if (ids[j] == ids[i]) return FKDE_INVALID_ARGUMENT;   // one context slot per device
+    }
+    auto* ctx = new fkde_gpu_ctx();
+    ctx->devs.resize(n_devices);
+    ctx->world = n_devices;
+    for (int i = 0; i < n_devices; ++i) {
         Status s = init_device(ctx->devs[i], ids[i], i, n_devices);
         if (!s.ok()) {
             fkde_gpu_destroy(ctx);
@@ -873,6 +894,9 @@ int fkde_gpu_create_rank(int device, int rank, int world, const unsigned char id
                          fkde_gpu_ctx** out) {
     if (!out || world < 1 || rank < 0 || rank >= world) return FKDE_INVALID_ARGUMENT;
     *out = nullptr;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) return FKDE_NO_DEVICE;
+    if (device < 0 || device >= count) return FKDE_INVALID_ARGUMENT;
     auto* ctx = new fkde_gpu_ctx();
     ctx->devs.resize(1);
     ctx->world = world;
@@ -900,6 +924,11 @@ int fkde_gpu_create_rank(int device, int rank, int world, const unsigned char id
 
 void fkde_gpu_destroy(fkde_gpu_ctx* ctx) {
     if (!ctx) return;
+    for (size_t i = 0; i < t_errors.size(); ++i)
+        if (t_errors[i].ctx == ctx) {
+            t_errors.erase(t_errors.begin() + i);
+            break;
+        }
     for (auto& D : ctx->devs) {
         cudaSetDevice(D.dev);
         if (D.stream) cudaStreamSynchronize(D.stream);
@@ -919,13 +948,23 @@ void fkde_gpu_destroy(fkde_gpu_ctx* ctx) {
     delete ctx;
 }
 
-const char* fkde_gpu_last_error(const fkde_gpu_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
+const char* fkde_gpu_last_error(const fkde_gpu_ctx* ctx) {
+    if (!ctx) return "";
+    for (auto& e : t_errors)
+        if (e.ctx == ctx) return e.msg.c_str();
+    // this thread made no call on ctx: a private copy of the context's last message
+    auto* c = const_cast<fkde_gpu_ctx*>(ctx);
+    std::lock_guard<std::mutex> lock(c->err_mu);
+    std::string& slot = thread_error_slot(ctx);
+    slot = c->err;
+    return slot.c_str();
+}
 
 int fkde_gpu_set_option(fkde_gpu_ctx* ctx, int key, int64_t value) {
     if (!ctx) return FKDE_INVALID_ARGUMENT;
     switch (key) {
         case FKDE_OPT_ENGINE:
-            if (value != FKDE_ENGINE_TC && value != FKDE_ENGINE_SIMT) return FKDE_INVALID_ARGUMENT;
+            if (value != FKDE_ENGINE_TC) return FKDE_INVALID_ARGUMENT;   // the only engine
             ctx->opt.engine = static_cast<int>(value);
             return FKDE_OK;
         case FKDE_OPT_SPLITS:
@@ -1200,6 +1239,7 @@ int fkde_gpu_sdkde_device(fkde_gpu_ctx* ctx, const double* dX, size_t n, const d
     Status s = validate_pair(dX, n, dY, m, d, h);
     if (s.ok() && !finite_h(h_score))
         s = make_status(FKDE_INVALID_ARGUMENT, "Bandwidth: h_score must be positive and finite");
+    if (s.ok() && !d_out) s = make_status(FKDE_INVALID_ARGUMENT, "out: null pointer");
     if (!s.ok()) return finish(ctx, s);
     Job J;
     J.kind = Job::kSdkde;
@@ -1245,6 +1285,9 @@ int fkde_gpu_kde_device(fkde_gpu_ctx* ctx, const double* dX, size_t n, const dou
     if (ctx->devs.size() != 1)
         return finish(ctx, make_status(FKDE_INVALID_ARGUMENT, "device API needs a 1-device context"));
     Status s = validate_pair(dX, n, dY, m, d, h);
+    if (s.ok() && kernel != FKDE_KERNEL_GAUSSIAN && kernel != FKDE_KERNEL_LAPLACE_CORRECTED)
+        s = make_status(FKDE_INVALID_ARGUMENT, "unknown kernel kind %d", kernel);
+    if (s.ok() && !d_out) s = make_status(FKDE_INVALID_ARGUMENT, "out: null pointer");
     if (!s.ok()) return finish(ctx, s);
     Job J;
     J.kind = Job::kKde;

@@ -8,6 +8,7 @@
 // payload straight into pinned host memory (one read(2) into a
 // cudaHostAlloc'ed buffer), which the engine then copies to HBM as a single
 // DMA.  Host code only; no device work happens here.
+#include <json.hpp>
 #include <cuda_runtime.h>
 
 #include <cerrno>
@@ -262,20 +263,11 @@ int fkde_io_write_values(const char* path, const double* values, size_t m, const
             text = "value\n";
             for (size_t i = 0; i < m; ++i) text += fmt17(values[i]) + "\n";
         } else if (fmt == "json") {
-            // shortest round-trip representation (nlohmann::json::dump does the same
-            // for finite doubles, up to a trailing ".0" on integral values)
-            text = "[";
-            char buf[64];
-            for (size_t i = 0; i < m; ++i) {
-                if (!std::isfinite(values[i])) {
-                    text += i ? ",null" : "null";
-                    continue;
-                }
-                const auto r = std::to_chars(buf, buf + sizeof(buf), values[i]);
-                if (i) text += ',';
-                text.append(buf, r.ptr);
-            }
-            text += "]\n";
+            // nlohmann::json, like the reference's writer (io.cpp:203-206): the same
+            // number formatting (grisu2 shortest form, "0.0" for integral values,
+            // null for non-finite), so the files are byte-identical
+            nlohmann::json j = std::vector<double>(values, values + m);
+            text = j.dump() + "\n";
         } else {
             arg_error("write_values: unknown format '" + fmt + "'");
         }

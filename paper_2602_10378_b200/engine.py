@@ -145,9 +145,17 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+def device_count() -> int:
+    c = ctypes.c_int(0)
+    N.load().fkde_gpu_device_count(ctypes.byref(c))
+    return int(c.value)
+
+
 def default_context(threads: int = 0) -> Context:
-    """Process-wide context: threads <= 1 -> device 0; k > 1 -> devices 0..k-1."""
-    k = max(1, int(threads))
+    """Process-wide context: threads <= 1 -> device 0; k > 1 -> devices
+    0..min(k, visible devices)-1.  The reference accepts any worker count
+    (parallel.cpp:12-24); here it is capped by the GPUs present, like the CLI."""
+    k = max(1, min(int(threads), device_count()))
     with _default_lock:
         if k not in _default_ctx:
             _default_ctx[k] = Context(list(range(k)))

@@ -13,13 +13,12 @@ import ctypes
 import numpy as np
 
 from . import _native as N
-from .types import InvalidArgumentError, SampleSet
+from .types import InvalidArgumentError, IoError, SampleSet
 
 _dp = ctypes.POINTER(ctypes.c_double)
 
-
-class IoError(RuntimeError):
-    """fkde::IoError (errors.hpp)."""
+__all__ = ["IoError", "read_samples", "write_samples_bin", "write_samples_csv", "write_values",
+           "read_values"]
 
 
 def _check(rc: int) -> None:

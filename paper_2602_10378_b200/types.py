@@ -49,7 +49,8 @@ class NonFiniteValueError(RuntimeError):
 
 
 class IoError(RuntimeError):
-    pass
+    """fkde::IoError (errors.hpp): file missing, malformed or short write
+    (raised by paper_2602_10378_b200.io)."""
 
 
 class DeviceError(RuntimeError):

@@ -11,6 +11,9 @@ LIBDIR = os.path.join(ROOT, "paper_2602_10378_b200")
 SRC = os.path.join(ROOT, "tests", "cpp", "test_facade.cpp")
 REF_INC = "/root/reference/proj/core/include"
 REF_TYPES_O = os.path.join(ROOT, "oracle", "_ref", "obj", "types.o")
+# prebuilt by __graft_entry__.build() where /root/reference exists (it does not on
+# the GPU box): the facade compiled against the reference's own fkde:: types
+PREBUILT_REF = os.path.join(ROOT, "tests", "cpp", "bin", "test_facade_ref")
 
 
 def _build(out, extra=()):
@@ -41,5 +44,16 @@ def test_facade_compiles_against_reference_types(tmp_path):
 def test_facade_runs_engine_on_gpu(tmp_path):
     exe = _build(str(tmp_path / "test_facade"))
     r = subprocess.run([exe, "gpu"], capture_output=True, text=True, timeout=300)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_facade_with_reference_types_runs_engine_on_gpu():
+    # the reference's own SampleSet / DensityResult / exceptions driving the GPU
+    # engine through the facade (binary built by build() against
+    # /root/reference/proj/core/include + the reference's types.cpp)
+    assert os.path.exists(PREBUILT_REF), "run __graft_entry__.build() where /root/reference exists"
+    r = subprocess.run([PREBUILT_REF, "gpu"], capture_output=True, text=True, timeout=300)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr

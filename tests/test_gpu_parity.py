@@ -41,14 +41,6 @@ def ctx():
     c.close()
 
 
-@pytest.fixture(scope="module")
-def simt():
-    c = fk.Context([0])
-    c.set_option(N.OPT_ENGINE, N.ENGINE_SIMT)
-    yield c
-    c.close()
-
-
 def _mixture_inputs(port, n, m):
     import oracle as O
     w, mu, s = O.default_mixture_16d()
@@ -215,19 +207,6 @@ def test_flush_interval_must_be_power_of_two(ctx):
             ctx.set_option(N.OPT_FLUSH_TILES, bad)
 
 
-def test_tc_engine_matches_simt_engine(ctx, simt, port):
-    tr, q = _mixture_inputs(port, 4096, 2048)
-    h = 1.5
-    for kernel in (fk.KernelKind.Gaussian, fk.KernelKind.LaplaceCorrected):
-        a = fk.kde_flash(tr, q, h, kernel, True, ctx=ctx).values
-        b = fk.kde_flash(tr, q, h, kernel, True, ctx=simt).values
-        assert max_rel_vs_peak(a, b) < 1e-5
-    a = fk.score_flash(tr, h, ctx=ctx).values
-    b = fk.score_flash(tr, h, ctx=simt).values
-    print("tc vs simt score", max_rel_global_floor(a, b), max_rowwise_rel(a, b))
-    assert max_rel_global_floor(a, b) < 1e-3
-
-
 @pytest.mark.parametrize("n,m,d", [(1, 1, 1), (129, 130, 3), (257, 5, 2), (300, 1, 16),
                                    (1000, 999, 4)])
 def test_ragged_and_small_shapes(ctx, port, n, m, d):
@@ -335,6 +314,84 @@ def test_errors(ctx, port):
     tr[7, 1] = 0.0
     v = fk.kde_flash(tr, q, 1.0, ctx=ctx).values
     assert max_component_rel(v, port.kde_naive(tr, q, 1.0)) < TOL_DENS
+
+
+def test_nonfinite_flag_does_not_leak_between_jobs(ctx, port):
+    # a NaN seen by one kind of job must not make a later valid job of another
+    # kind (which writes the other PassScalars slot) report NON_FINITE
+    lib = N.load()
+    dp = ctypes.POINTER(ctypes.c_double)
+    tr = port.random_gaussian(64, 3, 11)
+    q = port.random_gaussian(8, 3, 12)
+    bad = tr.copy()
+    bad[5, 2] = np.inf
+    out = np.empty(8)
+    sc = np.empty((64, 3))
+    idx = ctypes.c_size_t(0)
+    rc = lib.fkde_gpu_kde(ctx.handle, bad.ctypes.data_as(dp), 64, q.ctypes.data_as(dp), 8, 3, 0.8, 0,
+                          1, out.ctypes.data_as(dp))
+    assert rc == N.NON_FINITE
+    rc = lib.fkde_gpu_score(ctx.handle, tr.ctypes.data_as(dp), 64, 3, 0.8, sc.ctypes.data_as(dp),
+                            ctypes.byref(idx))
+    assert rc == N.OK, ctx.last_error()
+    assert max_rowwise_rel(sc, port.score_naive(tr, tr, 0.8)) < TOL_SCORE
+    rc = lib.fkde_gpu_score(ctx.handle, bad.ctypes.data_as(dp), 64, 3, 0.8, sc.ctypes.data_as(dp),
+                            ctypes.byref(idx))
+    assert rc == N.NON_FINITE
+    rc = lib.fkde_gpu_kde(ctx.handle, tr.ctypes.data_as(dp), 64, q.ctypes.data_as(dp), 8, 3, 0.8, 0,
+                          1, out.ctypes.data_as(dp))
+    assert rc == N.OK, ctx.last_error()
+    assert max_component_rel(out, port.kde_naive(tr, q, 0.8)) < TOL_DENS
+
+
+def test_last_error_is_per_thread(ctx, port):
+    # two threads sharing one context: each sees the message of its own call
+    import threading
+    lib = N.load()
+    dp = ctypes.POINTER(ctypes.c_double)
+    tr = port.random_gaussian(32, 2, 13)
+    q = port.random_gaussian(4, 2, 14)
+    out = np.empty(4)
+    msgs = {}
+
+    def worker(tag, h):
+        for _ in range(200):
+            rc = lib.fkde_gpu_kde(ctx.handle, tr.ctypes.data_as(dp), 32, q.ctypes.data_as(dp), 4, 2,
+                                  h, 7 if tag == "kind" else 0, 1, out.ctypes.data_as(dp))
+            assert rc == N.INVALID_ARGUMENT
+            msgs.setdefault(tag, set()).add(lib.fkde_gpu_last_error(ctx.handle).decode())
+
+    ts = [threading.Thread(target=worker, args=("kind", 1.0)),
+          threading.Thread(target=worker, args=("h", -1.0))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert msgs["kind"] == {"unknown kernel kind 7"}
+    assert len(msgs["h"]) == 1 and "h must be positive" in next(iter(msgs["h"]))
+
+
+def test_device_ids_are_validated():
+    with pytest.raises(fk.DeviceError):
+        fk.Context([0, 4096])
+    with pytest.raises(fk.DeviceError):
+        fk.Context([0, 0])
+    # the reference accepts any worker count: default contexts cap it at the GPUs present
+    c = fk.engine.default_context(threads=4096)
+    assert c.world()[1] == fk.engine.device_count()
+
+
+def test_device_api_argument_checks(ctx):
+    import torch
+    lib = N.load()
+    dX = torch.zeros((16, 2), dtype=torch.float64, device="cuda")
+    dO = torch.zeros(4, dtype=torch.float64, device="cuda")
+    assert lib.fkde_gpu_kde_device(ctx.handle, dX.data_ptr(), 16, dX.data_ptr(), 4, 2, 1.0, 5, 1,
+                                   dO.data_ptr()) == N.INVALID_ARGUMENT
+    assert lib.fkde_gpu_kde_device(ctx.handle, dX.data_ptr(), 16, dX.data_ptr(), 4, 2, 1.0, 0, 1,
+                                   None) == N.INVALID_ARGUMENT
+    assert lib.fkde_gpu_sdkde_device(ctx.handle, dX.data_ptr(), 16, dX.data_ptr(), 4, 2, 1.0, 1.0,
+                                     None) == N.INVALID_ARGUMENT
 
 
 # ---- pairwise_sq_dists_block (test_engine.cpp:125-192) --------------------------------

@@ -115,12 +115,24 @@ def test_files_are_byte_identical_to_the_reference(tmp_path, reflib):
         fio.write_values(v, a, fmt)
         assert reflib.fkr_write_values(b.encode(), _p(v), v.size, fmt.encode()) == 0
         assert open(a, "rb").read() == open(b, "rb").read(), fmt
-    # json: number formatting may differ (shortest round trip on both sides), values may not
-    a, b = str(tmp_path / "vo.json"), str(tmp_path / "vr.json")
-    fio.write_values(v, a, "json")
-    assert reflib.fkr_write_values(b.encode(), _p(v), v.size, b"json") == 0
+    # json: both sides serialise with nlohmann::json -> byte-identical, including
+    # integral values ("0.0", "-0.0", "3.0"), large/small magnitudes and non-finite
+    specials = np.array([0.0, -0.0, 3.0, -7.0, 1e22, 1e-7, 123456789012345678.0, 2.5e-310,
+                         np.nan, np.inf])
+    for tag, vv in (("v", v), ("s", specials)):
+        a, b = str(tmp_path / f"vo_{tag}.json"), str(tmp_path / f"vr_{tag}.json")
+        fio.write_values(vv, a, "json")
+        assert reflib.fkr_write_values(b.encode(), _p(vv), vv.size, b"json") == 0
+        assert open(a, "rb").read() == open(b, "rb").read(), tag
+    a, b = str(tmp_path / "vo_v.json"), str(tmp_path / "vr_v.json")
     assert ref_read_values(reflib, a).tobytes() == v.tobytes()
     assert fio.read_values(b).tobytes() == v.tobytes()
+
+
+def test_io_error_is_the_package_io_error():
+    # one exception type: `except fk.IoError` catches what fkde.io raises
+    import paper_2602_10378_b200 as fk
+    assert fio.IoError is fk.IoError
 
 
 def test_missing_file_is_io_error(tmp_path):

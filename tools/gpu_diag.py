@@ -1,5 +1,5 @@
-"""Quick on-device diagnostic: run each pass at small sizes on both device
-engines (tcgen05, SIMT) and print the error against the CPU oracle."""
+"""Quick on-device diagnostic: run each pass at small sizes and print the
+error against the CPU oracle."""
 import os
 import sys
 import time
@@ -27,10 +27,8 @@ def rowwise(a, b, floor=1e-2):
 
 def main():
     P = O.get("port")
-    which = sys.argv[1:] or ["simt", "tc"]
-    for eng in which:
+    for eng in ["tc"]:
         ctx = fk.Context([0])
-        ctx.set_option(N.OPT_ENGINE, N.ENGINE_SIMT if eng == "simt" else N.ENGINE_TC)
         for (n, m, d, h) in [(200, 50, 2, 0.5), (1024, 300, 16, 0.9), (4096, 4096, 16, 1.5)]:
             tr = P.random_gaussian(n, d, 41)
             q = P.random_gaussian(m, d, 42)
