@@ -6,17 +6,23 @@
 One step = one full SD-KDE over n = 2^20 training points and m = 2^17 queries
 in d = 16 (score pass -> x + h^2/2 s -> density pass), inputs drawn from the
 reference's 16-D Gaussian mixture with its runtime-sweep seeds and SD-KDE
-rate bandwidth.  N > 1 runs under torchrun, one process per GPU: rows are
-sharded for the score pass, the debiased samples are allgathered (NCCL),
-queries are sharded for the density pass (total work fixed: strong scaling).
+rate bandwidth.  N > 1 runs one process per GPU: launched by the driver under
+torchrun, or -- when WORLD_SIZE is unset -- bench.py re-executes itself under
+``python -m torch.distributed.run --nproc-per-node N``.  Rows are sharded for
+the score pass, the debiased samples are allgathered (NCCL), queries are
+sharded for the density pass (total work fixed: strong scaling).
 
 value  = queries/s of the whole job, inputs resident in HBM (fp64), timed on
          the engine's stream with CUDA events, max over ranks.
 e2e    = same metric through the host C ABI call (fkde_gpu_sdkde) from pinned
-         host buffers: H2D of X and Y, D2H of densities and debiased samples.
---impl reference: the reference's own CPU oracle (oracle/_ref, or the C port
-         when _ref is absent) on a bounded row sample, all host threads,
-         extrapolated linearly in evaluated rows (rank 0 only).
+         host buffers: H2D of X and Y, D2H of densities and debiased samples
+         (e2e_pageable: the same from ordinary pageable numpy buffers, what a
+         std::vector caller of the C++ facade gets).
+--impl reference: the reference's own CPU oracle (oracle/_ref built from
+         /root/reference, or the C port when _ref is absent) on a bounded row
+         sample with all host threads, extrapolated linearly in evaluated rows
+         (rank 0 only).  This arm never imports the product package: inputs
+         and bandwidth come from the reference's own sampler and rules.
 """
 from __future__ import annotations
 
@@ -114,14 +120,40 @@ def make_inputs(n, m):
     return X, Y, h
 
 
+def make_inputs_oracle(n, m, orc):
+    """The same inputs from the oracle library alone (reference arm: the product
+    package is never imported).  Bitwise equal to make_inputs (tests/test_bench.py)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    w, mu, s = O.default_mixture_16d()
+    cs = orc.mix64(0 ^ orc.mix64(n))             # sweep.cpp:67-69 cell_data_seed
+    X = orc.sample_mixture(w, mu, s, n, cs)
+    Y = orc.sample_mixture(w, mu, s, m, orc.mix64(cs ^ 0x71))
+    h = orc.sdkde_bandwidth(X, orc.silverman_prefactor(X.shape[1]))
+    return X, Y, h
+
+
+def workload_config(n, m, d, h):
+    """Identical in both arms (the driver compares them)."""
+    return {"workload": f"SD-KDE n={n} m={m} d={d} (BASELINE config 5)", "h": h,
+            "n_train": n, "n_query": m, "d": d,
+            "l2": "inputs larger than L2 (X fp64 128 MiB; B-operand tiles 128 MiB)"}
+
+
 # ---- CPU baseline (the reference oracle, bounded sample) ------------------------------
-def cpu_oracle_sample(X, Y, h, rows_score=2048, rows_query=1024):
-    """Times the reference's naive oracle on a row sample; returns (extrapolated
-    full-workload seconds, details).  Cost is exactly linear in evaluated rows."""
+ROWS_SCORE, ROWS_QUERY = 1024, 512
+
+
+def oracle_handle():
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
     kind = "reference" if O.reference_available() else "port"
-    orc = O.get(kind)
+    return kind, O.get(kind)
+
+
+def cpu_oracle_sample(orc, kind, X, Y, h, rows_score=ROWS_SCORE, rows_query=ROWS_QUERY):
+    """Times the reference's naive oracle on a row sample; returns (sample wall s,
+    extrapolated full-workload s, details).  Cost is exactly linear in evaluated rows."""
     threads = os.cpu_count() or 1
     n, m = X.shape[0], Y.shape[0]
     rs = np.linspace(0, n - 1, rows_score).astype(np.int64)
@@ -134,32 +166,45 @@ def cpu_oracle_sample(X, Y, h, rows_score=2048, rows_query=1024):
     full = (t1 - t0) * n / rows_score + (t2 - t1) * m / rows_query
     sample = (f"score_naive on {rows_score} of {n} rows + kde_naive on {rows_query} of {m} "
               f"queries (x {n} train), {threads} threads, extrapolated linearly in rows")
-    return full, {"kind": kind, "cores": threads, "sample": sample,
-                  "sample_s": t2 - t0}
+    return t2 - t0, full, {"kind": kind, "cores": threads, "sample": sample,
+                           "sample_s": t2 - t0, "extrapolated": True,
+                           "sample_rows": {"score": rows_score, "query": rows_query}}
+
+
+REF_FLASH_NOTE = ("the reference's CPU flash engine (engine.cpp, Eigen3) is not buildable in "
+                  "this image (Eigen3 absent here and on the GPU box); the timed path is its "
+                  "naive oracle (oracle.cpp), the reference's declared ground truth")
 
 
 def run_reference(args):
     rank, world, _ = env_rank()
     if rank != 0:
         return 0
-    X, Y, h = make_inputs(N_TRAIN, N_QUERY)
+    kind, orc = oracle_handle()
+    X, Y, h = make_inputs_oracle(N_TRAIN, N_QUERY, orc)
     for _ in range(args.warmup):
-        cpu_oracle_sample(X, Y, h, 32, 32)
-    walls = []
+        cpu_oracle_sample(orc, kind, X, Y, h, 16, 16)
+    samples, fulls = [], []
     info = None
     for _ in range(args.steps):
-        full, info = cpu_oracle_sample(X, Y, h)
-        walls.append(full)
-    wall = float(np.median(walls))
+        smp, full, info = cpu_oracle_sample(orc, kind, X, Y, h)
+        samples.append(smp)
+        fulls.append(full)
+    wall = float(np.median(fulls))
     qps = N_QUERY / wall
     line = {
         "impl": "reference", "metric": METRIC, "value": qps, "unit": "queries/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": wall * 1e3, "wall_s": wall, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        # ms_per_step is what one timed step actually took (the bounded sample);
+        # value is the full workload's rate extrapolated from it
+        "ms_per_step": float(np.mean(samples)) * 1e3,
+        "extrapolated": True, "full_workload_wall_s": wall,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: reference 16-D Gaussian mixture, runtime-sweep seeds",
-        "config": {"workload": f"SD-KDE n={N_TRAIN} m={N_QUERY} d={DIM} (BASELINE config 5)",
-                   "h": h, "parallelism": "host threads"},
+        "config": workload_config(N_TRAIN, N_QUERY, DIM, h),
+        "parallelism": f"{info['cores']} host threads on rank 0 (CPU only; no GPU used)",
+        "reference_path": f"oracle/_ref ({'reference sources compiled' if kind == 'reference' else 'C port'})",
+        "reference_flash_engine": REF_FLASH_NOTE,
         "cpu_baseline": dict(info, value=qps, unit="queries/s"),
         "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -171,10 +216,13 @@ def run_reference(args):
 # ---- our arm ---------------------------------------------------------------------------
 def run_ours(args):
     import torch
+
+    rank, world, local = env_rank()
+    if args.dry_run:
+        return run_dry(args, rank, world)
     import paper_2602_10378_b200 as fk
     from paper_2602_10378_b200 import _native as N
 
-    rank, world, local = env_rank()
     dist = None
     if world > 1:
         import torch.distributed as dist
@@ -184,7 +232,7 @@ def run_ours(args):
         dist.broadcast_object_list(uid, src=0)
         ctx = fk.Context(rank=rank, world=world, device=local, nccl_id=uid[0])
     else:
-        torch.cuda.set_device(0)
+        torch.cuda.set_device(local)
         ctx = fk.Context([local])
     lib = N.load()
     dev = torch.device("cuda", local)
@@ -232,42 +280,51 @@ def run_ours(args):
     dev_ms = ev0.elapsed_time(ev1)
     clocks = sampler.stop()
 
-    # e2e through the host C ABI (pinned host buffers, H2D + D2H inside)
+    # e2e through the host C ABI: H2D of this step's inputs and D2H of its results
+    # inside the timed region, from pinned (headline) and from pageable buffers
+    import ctypes
+    dp = ctypes.POINTER(ctypes.c_double)
+    idx = ctypes.c_size_t(0)
     pX = torch.from_numpy(X).pin_memory()
     pY = torch.from_numpy(Y).pin_memory()
     pO = torch.empty(m, dtype=torch.float64).pin_memory()
     pD = torch.empty((n, d), dtype=torch.float64).pin_memory()
-    import ctypes
-    dp = ctypes.POINTER(ctypes.c_double)
-    idx = ctypes.c_size_t(0)
+    gX, gY = np.ascontiguousarray(X), np.ascontiguousarray(Y)
+    gO, gD = np.empty(m), np.empty((n, d))
 
-    def host_step():
-        rc = lib.fkde_gpu_sdkde(ctx.handle, ctypes.cast(pX.data_ptr(), dp), n,
-                                ctypes.cast(pY.data_ptr(), dp), m, d, h, h,
-                                ctypes.cast(pO.data_ptr(), dp), ctypes.cast(pD.data_ptr(), dp),
-                                ctypes.byref(idx))
+    def host_step(bufs):
+        x, y, o, db = bufs
+        rc = lib.fkde_gpu_sdkde(ctx.handle, ctypes.cast(x, dp), n, ctypes.cast(y, dp), m, d, h, h,
+                                ctypes.cast(o, dp), ctypes.cast(db, dp), ctypes.byref(idx))
         if rc != 0:
             raise RuntimeError(ctx.last_error())
 
-    host_step()
-    barrier()
-    e2e_steps = max(1, min(args.steps, 3))
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        host_step()
-    barrier()
-    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    def e2e_time(bufs):
+        host_step(bufs)
+        barrier()
+        steps = max(1, min(args.steps, 3))
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            host_step(bufs)
+        barrier()
+        return (time.perf_counter() - t0) / steps
+
+    pinned = (pX.data_ptr(), pY.data_ptr(), pO.data_ptr(), pD.data_ptr())
+    pageable = (gX.ctypes.data, gY.ctypes.data, gO.ctypes.data, gD.ctypes.data)
+    e2e_s = e2e_time(pinned)
     out_ok = bool(np.isfinite(pO.numpy()).all() and (pO.numpy() > 0).all())
+    e2e_pg_s = e2e_time(pageable)
+    out_ok = out_ok and bool(np.array_equal(gO, pO.numpy()))
 
     # max over ranks
-    vals = torch.tensor([dev_ms, e2e_s, float(np.mean(score_ms)), float(np.mean(query_ms))],
+    vals = torch.tensor([dev_ms, e2e_s, e2e_pg_s, float(np.mean(score_ms)), float(np.mean(query_ms))],
                         dtype=torch.float64, device=dev)
     if dist:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
         lsum = torch.tensor([launches], dtype=torch.float64, device=dev)
         dist.all_reduce(lsum)
         launches = int(lsum.item())
-    dev_ms, e2e_s, score_avg, query_avg = [float(v) for v in vals.tolist()]
+    dev_ms, e2e_s, e2e_pg_s, score_avg, query_avg = [float(v) for v in vals.tolist()]
 
     if rank == 0:
         ms_step = dev_ms / args.steps
@@ -296,11 +353,9 @@ def run_ours(args):
             "dtype": "f32 (fp16 hi/lo split tensor-core operands, f32 accumulate, f64 finalize)",
             "data": "synthetic: reference 16-D Gaussian mixture (configs/mixture-16d-default.json),"
                     " reference RNG + runtime-sweep seeds, SD-KDE rate bandwidth",
-            "config": {"workload": f"SD-KDE n={n} m={m} d={d} (BASELINE config 5)", "h": h,
-                       "n_train": n, "n_query": m, "d": d,
-                       "parallelism": f"dp{world}: score rows sharded, 1 NCCL allgather of "
-                                      f"debiased samples, queries sharded",
-                       "l2": "inputs larger than L2 (X fp64 128 MiB; B-operand tiles 128 MiB)"},
+            "config": workload_config(n, m, d, h),
+            "parallelism": f"dp{world}: score rows sharded, 1 NCCL allgather of debiased samples, "
+                           f"queries sharded",
             "phases_ms": {"score_pass": score_avg, "density_pass": query_avg},
             # the reference's own performance model of this run:
             # paper-model pipeline FLOPs (4d+12+d/4+3/2) k^2 (perfmodel.cpp:62-67) and
@@ -314,8 +369,13 @@ def run_ours(args):
                 "exp_count": float(n) * n + float(n) * m},
             "clocks": clocks,
             "e2e": {"value": m / e2e_s, "unit": "queries/s", "wall_s": e2e_s,
+                    "host_buffers": "pinned",
                     "h2d_bytes_per_step": (n + m) * d * 8,
                     "d2h_bytes_per_step": m * 8 + n * d * 8, "outputs_finite": out_ok},
+            "e2e_pageable": {"value": m / e2e_pg_s, "unit": "queries/s", "wall_s": e2e_pg_s,
+                             "host_buffers": "pageable (numpy)",
+                             "h2d_bytes_per_step": (n + m) * d * 8,
+                             "d2h_bytes_per_step": m * 8 + n * d * 8},
             "gpu_launches": launches,
             "roofline": {"bound": "mufu", "kernel": "pairwise_tc_kernel<Score>",
                          "achieved": achieved, "peak": peak, "unit": "Gexp/s",
@@ -330,14 +390,53 @@ def run_ours(args):
                                     "note": "algorithmic 2x(2d) flop/pair vs dense bf16 peak"}},
         }
         if world == 1 and not args.no_cpu_baseline:
-            full, info = cpu_oracle_sample(X, Y, h)
+            kind, orc = oracle_handle()
+            smp, full, info = cpu_oracle_sample(orc, kind, X, Y, h)
             line["cpu_baseline"] = dict(info, value=N_QUERY / full, unit="queries/s",
-                                        wall_s=full)
+                                        wall_s=full, reference_flash_engine=REF_FLASH_NOTE)
         print(json.dumps(line), flush=True)
     ctx.close()
     if dist:
         dist.destroy_process_group()
     return 0
+
+
+def run_dry(args, rank, world):
+    """--dry-run: the launcher and the rank protocol (process group, barrier,
+    max-over-ranks, one JSON line from rank 0) without a GPU (gloo), for the
+    CPU tests of the N-rank launch."""
+    import torch
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        dist.barrier()
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "dry_run": True, "n_gpus": world,
+                          "max_over_ranks": float(t.item()), "steps": args.steps,
+                          "warmup": args.warmup}), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def free_port():
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch(argv, n):
+    """bench.py --gpus N outside torchrun: one process per GPU via torchrun
+    (the same launch the driver uses), rank 0's JSON line passes through."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1",
+           "--master-port", str(free_port()), os.path.abspath(__file__)] + argv
+    return subprocess.run(cmd).returncode
 
 
 def main():
@@ -347,9 +446,16 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dry-run", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(sys.argv[1:], args.gpus)
+    rank, world, _ = env_rank()
+    if world != args.gpus and rank == 0:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; reporting n_gpus={world}",
+              file=sys.stderr)
     return run_ours(args)
 
 
