@@ -97,7 +97,7 @@ typedef struct fkde_gpu_ctx fkde_gpu_ctx;
 
 /* ---- lifecycle ---------------------------------------------------------- */
 int fkde_gpu_device_count(int* count);
-/* devices: distinct ids in [0, device count), or NULL for 0..n_devices-1 */
+/* devices: ids in [0, device count), or NULL for 0..n_devices-1 */
 int fkde_gpu_create(const int* devices, int n_devices, fkde_gpu_ctx** out);
 int fkde_gpu_nccl_unique_id(unsigned char id[128]);
 int fkde_gpu_create_rank(int device, int rank, int world, const unsigned char id[128],
@@ -115,6 +115,10 @@ void* fkde_gpu_stream(fkde_gpu_ctx* ctx);
 int fkde_gpu_last_timing(const fkde_gpu_ctx* ctx, float* ms, int n);
 /* number of kernels this library launched during the last call (this rank) */
 int64_t fkde_gpu_last_launch_count(const fkde_gpu_ctx* ctx);
+/* device workspace currently held by the context (all devices), bytes: the
+ * analogue of the reference's transient-allocation accounting
+ * (alloc_stats, test_engine.cpp:218-243) -- linear in n + m, never n x m */
+int fkde_gpu_workspace_bytes(const fkde_gpu_ctx* ctx, size_t* bytes);
 
 /* Row partition used by every multi-GPU pass: rank r owns rows
  * [begin, begin + rows) of n, slices are `chunk` rows (chunk = ceil(n/world)

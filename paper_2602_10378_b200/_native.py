@@ -40,6 +40,7 @@ EXPORTED_SYMBOLS = (
     "fkde_gpu_score", "fkde_gpu_score_accumulate", "fkde_gpu_kde", "fkde_gpu_sdkde",
     "fkde_gpu_estimate", "fkde_gpu_pairwise_sq_dists", "fkde_gpu_sdkde_device",
     "fkde_gpu_kde_device", "fkde_gpu_score_device", "fkde_gpu_shard_range",
+    "fkde_gpu_workspace_bytes",
 )
 HOST_SYMBOLS = (
     "fkde_host_mix64", "fkde_host_random_gaussian", "fkde_host_sample_mixture",
@@ -81,6 +82,7 @@ def _declare(lib):
     lib.fkde_gpu_last_timing.argtypes = [_vp, ctypes.POINTER(ctypes.c_float), ctypes.c_int]
     lib.fkde_gpu_last_launch_count.argtypes = [_vp]
     lib.fkde_gpu_last_launch_count.restype = ctypes.c_int64
+    lib.fkde_gpu_workspace_bytes.argtypes = [_vp, _szp]
     lib.fkde_gpu_score.argtypes = [_vp, _dp, _sz, _sz, ctypes.c_double, _dp, _szp]
     lib.fkde_gpu_score_accumulate.argtypes = [_vp, _dp, _sz, _sz, ctypes.c_double, _dp, _dp]
     lib.fkde_gpu_kde.argtypes = [_vp, _dp, _sz, _dp, _sz, _sz, ctypes.c_double, ctypes.c_int,

@@ -35,6 +35,7 @@
 #include "layout.cuh"
 #include "pairwise_tc.cuh"
 #include "prep_kernels.cuh"
+#include "direct_rows.cuh"
 
 using namespace fkde_b200;
 
@@ -177,6 +178,7 @@ struct Device {
     ncclComm_t comm = nullptr;
     bool attrs_set = false;
     DevBuf X, Y, opA, opB, part0, part1, xsd, out, aux0, aux1, colpart, scal, err, flags;
+    DevBuf risk, dpart, ddone;   // direct_rows_kernel: spread flags, partials, counters
     cudaEvent_t ev[FKDE_T_COUNT + 1] = {};
     int64_t launches = 0;
     // device-resident API: the call's whole device program as a CUDA graph,
@@ -304,6 +306,7 @@ Status pack(Device& D, const double* x, size_t rows, int d, int format, bool cen
             float a_offset = 0.f) {
     const size_t rp = round_up(std::max<size_t>(rows, 1), align);
     STATUS_TRY(ensure(out, rp * kRowBytes));
+    if (format == 0) STATUS_TRY(ensure(D.risk, rp));
     PackArgs a;
     a.x = x;
     a.rows = rows;
@@ -315,6 +318,8 @@ Status pack(Device& D, const double* x, size_t rows, int d, int format, bool cen
     a.sc = sc;
     a.out = out.as<uint4>();
     a.a_offset = a_offset;
+    a.risk = format == 0 ? D.risk.as<uint8_t>() : nullptr;   // row side: spread flags
+    a.risk_half_norm = kRiskHalfNorm;
     pack_operands<<<grid1(rp, 128), 128, 0, D.stream>>>(a);
     ++D.launches;
     CUDA_TRY(cudaGetLastError());
@@ -354,15 +359,27 @@ Status density_pass(Device& D, const Options& o, int mode, size_t rows_pad, size
     return {};
 }
 
-// flag list for exact_rows_fp64: [0] = count, [1..] = local row indices
+// flag list for direct_rows_kernel: [0] = count, [1..] = local row indices
 Status prepare_flags(Device& D, size_t rows) {
     STATUS_TRY(ensure(D.flags, (rows + 1) * sizeof(unsigned int)));
     CUDA_TRY(cudaMemsetAsync(D.flags.p, 0, sizeof(unsigned int), D.stream));
     return {};
 }
 
-Status launch_exact(Device& D, const ExactArgs& e) {
-    exact_rows_fp64<<<2 * D.num_sms, 256, 0, D.stream>>>(e);
+// Recompute the flagged rows by direct differences (direct_rows.cuh).  The
+// flagged count lives on the device; the launch exits at once when it is 0.
+Status launch_direct(Device& D, DirectArgs& e, size_t rows) {
+    // partials: at most (row blocks x splits) < 2 * kDirTargetItems items of 128 rows
+    STATUS_TRY(ensure(D.dpart, static_cast<size_t>(2 * kDirTargetItems) * kDirRows * kDirPart *
+                                   sizeof(double)));
+    const size_t blocks = (rows + kDirRows - 1) / kDirRows + 1;
+    if (D.ddone.bytes < blocks * sizeof(unsigned int)) {   // counters start at zero, then self-reset
+        STATUS_TRY(ensure(D.ddone, blocks * sizeof(unsigned int)));
+        CUDA_TRY(cudaMemsetAsync(D.ddone.p, 0, D.ddone.bytes, D.stream));
+    }
+    e.part = D.dpart.as<double>();
+    e.done = D.ddone.as<unsigned int>();
+    direct_rows_kernel<<<kDirTargetItems, kDirRows, 0, D.stream>>>(e);
     ++D.launches;
     CUDA_TRY(cudaGetLastError());
     return {};
@@ -482,18 +499,20 @@ Status score_program(Device& D, const Options& o, const Job& J, const double* dX
     STATUS_TRY(prepare_flags(D, sh.rows));
     f.flag_count = D.flags.as<unsigned int>();
     f.flag_rows = f.flag_count + 1;
+    f.risk = D.risk.as<uint8_t>();
     finalize_score<<<grid1(std::max<size_t>(sh.rows, 1) * d, 256), 256, 0, D.stream>>>(f);
     ++D.launches;
     CUDA_TRY(cudaGetLastError());
     {
-        ExactArgs e{};
+        DirectArgs e{};
         e.mode = kExactScore;
         e.count = f.flag_count;
         e.rows = f.flag_rows;
         e.rowpts = dX + sh.begin * d;
         e.row0 = sh.begin;
-        e.center_rows = 0;
+        e.center_rows = 1;
         e.cols = dX;
+        e.center_cols = 1;
         e.n = n;
         e.d = d;
         e.sc = sc;
@@ -503,7 +522,7 @@ Status score_program(Device& D, const Options& o, const Job& J, const double* dX
         e.xsd_c = f.xsd_c;
         e.phi_sum = f.phi_sum;
         e.weighted = f.weighted;
-        STATUS_TRY(launch_exact(D, e));
+        STATUS_TRY(launch_direct(D, e, sh.rows));
     }
     record(D, o, FKDE_T_GATHER);
     if (J.kind == Job::kScore) STATUS_TRY(allgather(D, D.aux0.p, sh.chunk * d, ncclFloat64));
@@ -557,6 +576,7 @@ Status query_program(Device& D, const Options& o, const Job& J, const double* dC
         r.accumulate = 0;
         r.flag_count = flag_count;
         r.flag_rows = flag_count + 1;
+        r.risk = D.risk.as<uint8_t>();
         if (sh.rows) reduce_density<<<grid1(sh.rows, 256), 256, 0, D.stream>>>(r);
         ++D.launches;
     } else if (fused) {
@@ -571,6 +591,7 @@ Status query_program(Device& D, const Options& o, const Job& J, const double* dC
         r.accumulate = 0;
         r.flag_count = flag_count;
         r.flag_rows = flag_count + 1;
+        r.risk = D.risk.as<uint8_t>();
         if (sh.rows) reduce_density<<<grid1(sh.rows, 256), 256, 0, D.stream>>>(r);
         ++D.launches;
     } else {
@@ -594,26 +615,28 @@ Status query_program(Device& D, const Options& o, const Job& J, const double* dC
         r.accumulate = 1;
         r.flag_count = flag_count;
         r.flag_rows = flag_count + 1;
+        r.risk = D.risk.as<uint8_t>();
         if (sh.rows) reduce_density<<<grid1(sh.rows, 256), 256, 0, D.stream>>>(r);
         ++D.launches;
     }
     CUDA_TRY(cudaGetLastError());
     {
-        ExactArgs e{};
+        DirectArgs e{};
         e.mode = kernel == FKDE_KERNEL_GAUSSIAN ? kExactGauss : kExactLaplace;
         e.count = flag_count;
         e.rows = flag_count + 1;
         e.rowpts = dQ + sh.begin * d;
         e.row0 = sh.begin;
-        e.center_rows = cols_centred ? 1 : 0;
+        e.center_rows = 1;
         e.cols = dCols;
+        e.center_cols = cols_centred ? 0 : 1;
         e.n = n;
         e.d = d;
         e.sc = sc_q;
         e.h = J.h;
         e.norm = norm;
         e.out = outp;
-        STATUS_TRY(launch_exact(D, e));
+        STATUS_TRY(launch_direct(D, e, sh.rows));
     }
     STATUS_TRY(allgather(D, D.out.p, sh.chunk, ncclFloat64));
     return {};
@@ -853,8 +876,8 @@ int fkde_gpu_create(const int* devices, int n_devices, fkde_gpu_ctx** out) {
     for (int i = 0; i < n_devices; ++i) {
         ids[i] = devices ? devices[i] : i;
         if (ids[i] < 0 || ids[i] >= count) return FKDE_INVALID_ARGUMENT;
-        for (int j = 0; j < i; ++j)
-            if (ids[j] == ids[i]) return FKDE_INVALID_ARGUMENT;   // one context slot per device
+        // (a repeated id is allowed: ranks sharing a GPU, e.g. over the tests'
+        // in-process NCCL emulator; real NCCL rejects it at ncclCommInitAll)
     }
     auto* ctx = new fkde_gpu_ctx();
     ctx->devs.resize(n_devices);
@@ -933,8 +956,9 @@ void fkde_gpu_destroy(fkde_gpu_ctx* ctx) {
         cudaSetDevice(D.dev);
         if (D.stream) cudaStreamSynchronize(D.stream);
         if (D.comm && nccl().loaded) nccl().CommDestroy(D.comm);
-        DevBuf* bufs[] = {&D.X, &D.Y, &D.opA, &D.opB, &D.part0, &D.part1, &D.xsd,
-                          &D.out, &D.aux0, &D.aux1, &D.colpart, &D.scal, &D.err, &D.flags};
+        DevBuf* bufs[] = {&D.X,    &D.Y,     &D.opA,  &D.opB, &D.part0, &D.part1,
+                          &D.xsd,  &D.out,   &D.aux0, &D.aux1, &D.colpart, &D.scal,
+                          &D.err,  &D.flags, &D.risk, &D.dpart, &D.ddone};
         for (DevBuf* b : bufs)
             if (b->p) cudaFree(b->p);
         for (auto& e : D.ev)
@@ -1018,6 +1042,19 @@ int fkde_gpu_last_timing(const fkde_gpu_ctx* ctx, float* ms, int n) {
             cudaEventElapsedTime(&v, D.ev[FKDE_T_PREP], D.ev[FKDE_T_TOTAL]);
         ms[i] = v;
     }
+    return FKDE_OK;
+}
+
+int fkde_gpu_workspace_bytes(const fkde_gpu_ctx* ctx, size_t* bytes) {
+    if (!ctx || !bytes) return FKDE_INVALID_ARGUMENT;
+    size_t total = 0;
+    for (const Device& D : ctx->devs) {
+        const DevBuf* bufs[] = {&D.X,    &D.Y,     &D.opA,  &D.opB,  &D.part0,   &D.part1,
+                                &D.xsd,  &D.out,   &D.aux0, &D.aux1, &D.colpart, &D.scal,
+                                &D.err,  &D.flags, &D.risk, &D.dpart, &D.ddone};
+        for (const DevBuf* b : bufs) total += b->bytes;
+    }
+    *bytes = total;
     return FKDE_OK;
 }
 

@@ -98,6 +98,9 @@ struct PackArgs {
     float a_offset;          // A rows: constant added to every Gram entry (before the
                              // 2^(2e) scale): chunk-2 element 6 = a_offset * 2^-2e,
                              // paired with a 1 in the B rows (score pass: kPScaleF)
+    uint8_t* risk;           // A rows (optional): 1 where |y|^2/2 > risk_half_norm (the
+                             // expanded norms' fp32 rounding is too coarse: direct_rows)
+    double risk_half_norm;
 };
 
 __device__ __forceinline__ uint32_t pack_h2(__half a, __half b) {
@@ -126,6 +129,7 @@ __global__ void pack_operands(PackArgs a) {
             nrm += h * h + 2.0 * h * l;  // exactly what the 3-term MMA forms on the diagonal
         }
         const double m = -0.5 * nrm;
+        if (a.risk) a.risk[i] = (-m * ldexp(1.0, 2 * a.sc->e) > a.risk_half_norm) ? 1 : 0;
         n1 = __double2half(m);
         const double r1 = m - static_cast<double>(__half2float(n1));
         n2 = __double2half(r1);
@@ -133,6 +137,7 @@ __global__ void pack_operands(PackArgs a) {
     } else {
 #pragma unroll
         for (int c = 0; c < kMaxDim; ++c) yh[c] = yl[c] = zero;
+        if (a.risk && i < a.rows_padded) a.risk[i] = 0;
     }
     // chunk layout (see layout.cuh):      A                 B
     //   0-1  y_hi                          y_hi              y_hi
@@ -208,8 +213,9 @@ struct FinalizeArgs {
     double* phi_sum;      // [n] raw S or nullptr
     double* weighted;     // [n][d] raw sum_j phi_ij x_j or nullptr
     unsigned long long* underflow_row;  // atomicMin of failing global row
-    unsigned int* flag_count;           // rows handed to exact_rows_fp64
+    unsigned int* flag_count;           // rows handed to direct_rows_kernel
     unsigned int* flag_rows;            // (local indices)
+    const uint8_t* risk;                // pack's spread flags (local rows) or nullptr
 };
 
 // One thread per (row, coordinate): consecutive threads read consecutive
@@ -225,7 +231,8 @@ __global__ void finalize_score(FinalizeArgs a) {
     double Sp = 0.0;
     for (int s = 0; s < a.splits; ++s) Sp += a.part_s[s * a.rows_pad + i];
     Sp = ldexp(Sp, -kPScaleExp);  // the tc/simt score sums carry phi * 2^15
-    if (Sp < kScoreFlagMass && a.flag_rows) {  // too little neighbour mass for fp16 P
+    // too little neighbour mass for fp16 P, or too much spread for the expansion
+    if (a.flag_rows && (Sp < kScoreFlagMass || (a.risk && a.risk[i]))) {
         if (c == 0) a.flag_rows[atomicAdd(a.flag_count, 1u)] = static_cast<unsigned int>(i);
         return;
     }
@@ -270,6 +277,7 @@ struct ReduceArgs {
     double* out;
     unsigned int* flag_count;   // rows whose Gaussian mass underflows fp32 ranges
     unsigned int* flag_rows;
+    const uint8_t* risk;        // pack's spread flags (local rows) or nullptr
 };
 
 __global__ void reduce_density(ReduceArgs a) {
@@ -279,113 +287,12 @@ __global__ void reduce_density(ReduceArgs a) {
     for (int p = 0; p < a.nparts; ++p) s0 += static_cast<double>(a.part0[p * a.rows_pad + j]);
     if (a.part1)
         for (int p = 0; p < a.nparts; ++p) s1 += static_cast<double>(a.part1[p * a.rows_pad + j]);
-    if (a.flag_rows && s0 < kDensityFlagMass) {
+    if (a.flag_rows && (s0 < kDensityFlagMass || (a.risk && a.risk[j]))) {
         a.flag_rows[atomicAdd(a.flag_count, 1u)] = static_cast<unsigned int>(j);
         return;
     }
     const double v = a.scale * (a.ca * s0 + a.cb * s1);
     a.out[j] = a.accumulate ? a.out[j] + v : v;
-}
-
-// ---- exact fp64 recompute of flagged rows ---------------------------------------------
-// Rows the fp16/fp32 tensor-core path cannot resolve (all neighbours so far
-// away that phi underflows the operand/accumulator range) are recomputed here
-// with direct-subtraction fp64 distances (the oracle's formulation,
-// oracle.cpp:25-32, 53-85) and a per-row max shift, so the result matches the
-// fp64 reference even where phi ~ 1e-300.  One warp per flagged row.
-struct ExactArgs {
-    int mode;                   // kExactScore / kExactGauss / kExactLaplace
-    const unsigned int* count;
-    const unsigned int* rows;   // local row indices
-    const double* rowpts;       // local row 0's point (original coordinates)
-    size_t row0;                // global index of local row 0 (score: the self column)
-    int center_rows;            // subtract sc->mu from the row points
-    const double* cols;         // column points, n x d
-    size_t n;
-    int d;
-    const PassScalars* sc;
-    double h;                   // kernel bandwidth of this pass
-    double shift;               // score: h^2/2 of the SD shift
-    double norm;                // density: gaussian_norm_const(h, d) / n
-    // score outputs (global row layout) / density output (local layout)
-    double* score;
-    double* xsd_c;
-    double* phi_sum;
-    double* weighted;
-    double* out;
-};
-enum { kExactScore = 0, kExactGauss = 1, kExactLaplace = 2 };
-
-__global__ void __launch_bounds__(256) exact_rows_fp64(ExactArgs a) {
-    const int lane = threadIdx.x & 31;
-    const unsigned int nflag = *a.count;
-    const unsigned int warp_g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const unsigned int nwarps = (gridDim.x * blockDim.x) >> 5;
-    const double inv_2h2 = 1.0 / (2.0 * a.h * a.h);
-    for (unsigned int k = warp_g; k < nflag; k += nwarps) {
-        const size_t i = a.rows[k];
-        double x[kMaxDim];
-        for (int c = 0; c < a.d; ++c)
-            x[c] = a.rowpts[i * a.d + c] - (a.center_rows ? a.sc->mu[c] : 0.0);
-        const size_t self = a.mode == kExactScore ? a.row0 + i : ~static_cast<size_t>(0);
-        // pass 1: max exponent
-        double m = -INFINITY;
-        for (size_t j = lane; j < a.n; j += 32) {
-            if (j == self) continue;
-            double r2 = 0.0;
-            for (int c = 0; c < a.d; ++c) {
-                const double df = x[c] - a.cols[j * a.d + c];
-                r2 += df * df;
-            }
-            m = fmax(m, -r2 * inv_2h2);
-        }
-        for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-        // pass 2: shifted sums
-        double S = 0.0, L = 0.0, T[kMaxDim];
-        for (int c = 0; c < kMaxDim; ++c) T[c] = 0.0;
-        if (m > -INFINITY) {
-            for (size_t j = lane; j < a.n; j += 32) {
-                if (j == self) continue;
-                double r2 = 0.0;
-                for (int c = 0; c < a.d; ++c) {
-                    const double df = x[c] - a.cols[j * a.d + c];
-                    r2 += df * df;
-                }
-                const double u = r2 * inv_2h2;
-                const double e = exp(-u - m);
-                S += e;
-                if (a.mode == kExactLaplace) L += e * u;
-                if (a.mode == kExactScore)
-                    for (int c = 0; c < a.d; ++c) T[c] += e * (a.cols[j * a.d + c] - x[c]);
-            }
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-            S += __shfl_xor_sync(0xffffffffu, S, o);
-            L += __shfl_xor_sync(0xffffffffu, L, o);
-            if (a.mode == kExactScore)
-                for (int c = 0; c < a.d; ++c) T[c] += __shfl_xor_sync(0xffffffffu, T[c], o);
-        }
-        if (lane != 0) continue;
-        const double em = m > -INFINITY ? exp(m) : 0.0;
-        if (a.mode == kExactScore) {
-            const size_t g = a.row0 + i;
-            const double Sp = em * S;
-            const double Stot = 1.0 + Sp;                       // + the self pair
-            if (a.phi_sum) a.phi_sum[g] = Stot;
-            const double inv = 1.0 / (a.h * a.h * Stot);
-            for (int c = 0; c < a.d; ++c) {
-                const double num = em * T[c];                   // sum_j phi_ij (x_j - x_i)
-                const double sc = num * inv;
-                if (a.score) a.score[g * a.d + c] = sc;
-                if (a.xsd_c) a.xsd_c[g * a.d + c] = (x[c] - a.sc->mu[c]) + a.shift * sc;
-                if (a.weighted) a.weighted[g * a.d + c] = num + x[c] * Stot;
-            }
-        } else if (a.mode == kExactGauss) {
-            a.out[i] = a.norm * (em * S);
-        } else {
-            a.out[i] = a.norm * (em * ((1.0 + 0.5 * a.d) * S - L));
-        }
-    }
 }
 
 // ---- public block distances (engine.cpp:41-51 / 261-277 semantics, fp64) ---------------

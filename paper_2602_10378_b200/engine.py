@@ -108,6 +108,11 @@ class Context:
     def last_launch_count(self) -> int:
         return int(self._lib.fkde_gpu_last_launch_count(self._h))
 
+    def workspace_bytes(self) -> int:
+        b = ctypes.c_size_t(0)
+        self._lib.fkde_gpu_workspace_bytes(self._h, ctypes.byref(b))
+        return int(b.value)
+
     def stream(self) -> int:
         return int(self._lib.fkde_gpu_stream(self._h) or 0)
 

@@ -240,9 +240,10 @@ def test_large_offset_data_is_centred(ctx, port):
 
 
 def test_wide_spread_data_scales_operands(ctx, port):
-    # |y|^2/2 beyond 2^13 -> the operand scale exponent e > 0 path.  Accuracy
-    # of any Gram-expansion engine degrades with |x - mu|^2 / h^2 (fp32
-    # accumulation of the expanded norms); the bound here is looser, stated.
+    # |y|^2/2 beyond 2^13 -> the operand scale exponent e > 0 path.  The Gram
+    # expansion's fp32 rounding grows with |x - mu|^2 / h^2, so these rows
+    # (|y|^2/2 > kRiskHalfNorm = 256) are flagged and recomputed by direct
+    # differences: the normal tolerances hold.
     centres = np.array([[40.0, 0, 0, 0], [-40.0, 0, 0, 0], [0, 40.0, 0, 0], [0, -40.0, 0, 0]])
     tr = port.random_gaussian(800, 4, 75) + np.repeat(centres, 200, axis=0)
     q = port.random_gaussian(80, 4, 76) + np.repeat(centres, 20, axis=0)
@@ -251,12 +252,13 @@ def test_wide_spread_data_scales_operands(ctx, port):
     ref = port.kde_naive(tr, q, h)
     err = max_component_rel(v, ref)
     print("wide-spread kde rel err", err)
-    assert err < 2e-2
+    assert err < TOL_DENS
     s = fk.score_flash(tr, h, ctx=ctx).values
     ref_s = port.score_naive(tr, tr, h)
     err_s = max_rel_global_floor(s, ref_s)
-    print("wide-spread score err", err_s)
-    assert err_s < 5e-2
+    err_r = max_rowwise_rel(s, ref_s)
+    print("wide-spread score err", err_s, err_r)
+    assert err_s < TOL_SCORE and err_r < TOL_SCORE
 
 
 def test_estimate_dispatch(ctx, port):
@@ -375,7 +377,7 @@ def test_device_ids_are_validated():
     with pytest.raises(fk.DeviceError):
         fk.Context([0, 4096])
     with pytest.raises(fk.DeviceError):
-        fk.Context([0, 0])
+        fk.Context([-1])
     # the reference accepts any worker count: default contexts cap it at the GPUs present
     c = fk.engine.default_context(threads=4096)
     assert c.world()[1] == fk.engine.device_count()
@@ -445,11 +447,21 @@ def test_rank_context_world1_matches(ctx, port):
     assert np.array_equal(r1, r2)
 
 
-# ---- full-size configurations: size-independent checks on row subsamples ------------------
+# ---- full-size configurations ------------------------------------------------------------
+# The oracle is exactly linear in evaluated rows; where it cannot finish every row
+# (configs 4 and 5) parity is checked on a deterministic row subsample, with the
+# measured maxima printed.
+def _report(tag, **errs):
+    print(tag, " ".join(f"{k}={v:.3e}" for k, v in errs.items()))
+
+
 @pytest.mark.slow
 def test_config5_headline_subsample(ctx, port):
-    # n = 2^20, m = 2^17 (BASELINE config 5).  The oracle is exactly linear in
-    # evaluated rows, so parity is checked on a deterministic row subsample.
+    # n = 2^20, m = 2^17 (BASELINE config 5).  Score checked directly on 4096
+    # rows with both floored metrics of proj/tests/test_util.hpp:53-93; x^SD on
+    # the same rows; densities of 4096 queries against the engine's own x^SD
+    # (the oracle's x^SD needs all 2^20 score rows: 1.1e12 pairs -- the density
+    # pass is pinned end to end at config 2, where it is affordable).
     n, m = 1 << 20, 1 << 17
     tr, q = _mixture_inputs(port, n, m)
     h = port.sdkde_bandwidth(tr, port.silverman_prefactor(16))
@@ -458,44 +470,53 @@ def test_config5_headline_subsample(ctx, port):
     assert np.isfinite(v).all() and (v > 0).all()
     rows = np.linspace(0, n - 1, 4096).astype(int)
     sc = port.score_naive(tr, tr[rows], h, threads=os.cpu_count())
+    s = fk.score_flash(tr, h, ctx=ctx).values[rows]
     ref_deb = tr[rows] + 0.5 * h * h * sc
-    assert max_rowwise_rel(deb[rows], ref_deb) < TOL_DEB
     qs = np.linspace(0, m - 1, 4096).astype(int)
     ref_v = port.kde_naive(deb, q[qs], h, threads=os.cpu_count())
-    assert max_component_rel(v[qs], ref_v) < TOL_DENS
-    assert max_log_rel(v[qs], ref_v) < 1e-3
+    e = dict(score_rowwise=max_rowwise_rel(s, sc), score_global=max_rel_global_floor(s, sc),
+             debiased=max_rowwise_rel(deb[rows], ref_deb), density=max_component_rel(v[qs], ref_v),
+             log_density=max_log_rel(v[qs], ref_v))
+    _report("config5", **e)
+    assert e["score_rowwise"] < TOL_SCORE and e["score_global"] < TOL_SCORE
+    assert e["debiased"] < TOL_DEB
+    assert e["density"] < TOL_DENS and e["log_density"] < 1e-3
 
 
 @pytest.mark.slow
 def test_config4_laplace_subsample(ctx, port):
+    # n = 262144, m = 65536 Laplace-corrected (fused), 8192 queries (1/8) vs the oracle
     n, m = 262144, 65536
     tr, q = _mixture_inputs(port, n, m)
     h = port.silverman_bandwidth(tr)
     v = fk.kde_flash(tr, q, h, fk.KernelKind.LaplaceCorrected, True, ctx=ctx).values
-    qs = np.linspace(0, m - 1, 2048).astype(int)
+    qs = np.linspace(0, m - 1, 8192).astype(int)
     ref = port.laplace_naive(tr, q[qs], h, threads=os.cpu_count())
-    assert max_rel_vs_peak(v[qs], ref) < TOL_LAP
+    e = max_rel_vs_peak(v[qs], ref)
+    _report("config4", laplace_vs_peak=e)
+    assert e < TOL_LAP
 
 
 @pytest.mark.slow
 def test_config2_sdkde_32k_full(ctx, port):
-    # BASELINE config 2: SD-KDE n = m = 32768 (score rows + densities on subsamples,
-    # debiased samples of the sampled rows through the full score pass)
+    # BASELINE config 2: SD-KDE n = m = 32768, every row and every query, end to
+    # end: the densities are compared with the oracle's densities at the ORACLE's
+    # own debiased samples (oracle.cpp:87-101), not at the engine's
     n = m = 32768
     tr, q = _mixture_inputs(port, n, m)
     h = port.sdkde_bandwidth(tr, port.silverman_prefactor(16))
     r = fk.sdkde_flash(tr, q, fk.Bandwidth.uniform(h), ctx=ctx)
-    rows = np.arange(n)   # every row: full-size parity at BASELINE config 2
-    sc = port.score_naive(tr, tr[rows], h, threads=os.cpu_count())
-    ref_deb = tr[rows] + 0.5 * h * h * sc
-    assert max_rowwise_rel(r.debiased_samples.values[rows], ref_deb) < TOL_DEB
+    sc = port.score_naive(tr, tr, h, threads=os.cpu_count())
+    ref_deb = tr + 0.5 * h * h * sc
     s = fk.score_flash(tr, h, ctx=ctx).values
-    assert max_rowwise_rel(s[rows], sc) < TOL_SCORE
-    assert max_rel_global_floor(s[rows], sc) < TOL_SCORE
-    qs = np.arange(m)
-    ref_v = port.kde_naive(r.debiased_samples.values, q[qs], h, threads=os.cpu_count())
-    assert max_component_rel(r.values[qs], ref_v) < TOL_DENS
-    assert max_log_rel(r.values[qs], ref_v) < 1e-3
+    ref_v = port.kde_naive(ref_deb, q, h, threads=os.cpu_count())
+    e = dict(debiased=max_rowwise_rel(r.debiased_samples.values, ref_deb),
+             score_rowwise=max_rowwise_rel(s, sc), score_global=max_rel_global_floor(s, sc),
+             density=max_component_rel(r.values, ref_v), log_density=max_log_rel(r.values, ref_v))
+    _report("config2", **e)
+    assert e["debiased"] < TOL_DEB
+    assert e["score_rowwise"] < TOL_SCORE and e["score_global"] < TOL_SCORE
+    assert e["density"] < TOL_DENS and e["log_density"] < 1e-3
 
 
 @pytest.mark.slow
@@ -505,10 +526,133 @@ def test_config3_plain_kde_32k_full(ctx, port):
     tr, q = _mixture_inputs(port, n, m)
     h = port.silverman_bandwidth(tr)
     v = fk.kde_flash(tr, q, h, ctx=ctx).values
-    qs = np.arange(m)   # every query: full-size parity at BASELINE config 3
-    ref = port.kde_naive(tr, q[qs], h, threads=os.cpu_count())
-    assert max_component_rel(v[qs], ref) < TOL_DENS
-    assert max_log_rel(v[qs], ref) < 1e-3
+    ref = port.kde_naive(tr, q, h, threads=os.cpu_count())   # every query
+    e = dict(density=max_component_rel(v, ref), log_density=max_log_rel(v, ref))
+    _report("config3", **e)
+    assert e["density"] < TOL_DENS and e["log_density"] < 1e-3
+
+
+# ---- acceptance criteria (proj/tests/acceptance/acceptance_main.cpp) --------------------
+def _acceptance_instance(port, i):
+    # acceptance_main.cpp:65-83 (the generator); n = 4096 instances are made here
+    # with the C port (bitwise the reference's RNG, tests/test_oracle.py)
+    ns, ds = [3, 64, 1024, 4096], [1, 2, 16]
+    n, d = ns[(i % 12) // 3], ds[i % 3]
+    tr = port.random_gaussian(n, d, 1000 + i, 1.5)
+    q = port.random_gaussian(max(1, n // 8), d, 2000 + i, 1.5)
+    h = (0.8 + 0.8 * port.uniform01(3000 + i, 1)[0]) * 0.75 * np.sqrt(float(d))
+    return tr, q, h
+
+
+BIG_ACCEPT = [i for i in range(50) if [3, 64, 1024, 4096][(i % 12) // 3] == 4096]
+
+
+@pytest.mark.parametrize("i", BIG_ACCEPT)
+def test_acceptance_instances_n4096(ctx, port, i):
+    # the 12 n = 4096 instances of crit. 1 (make_golden.py stores the n <= 1024 ones)
+    tr, q, h = _acceptance_instance(port, i)
+    th = os.cpu_count()
+    kde = port.kde_naive(tr, q, h, threads=th)
+    lap = port.laplace_naive(tr, q, h, threads=th)
+    score = port.score_naive(tr, tr, h, threads=th)
+    sd, deb = port.sdkde_naive(tr, q, h, threads=th)
+    e = dict(kde=max_component_rel(fk.kde_flash(tr, q, h, ctx=ctx).values, kde),
+             laplace=max_rel_vs_peak(fk.kde_flash(tr, q, h, fk.KernelKind.LaplaceCorrected, True,
+                                                  ctx=ctx).values, lap),
+             score=max_rel_global_floor(fk.score_flash(tr, h, ctx=ctx).values, score))
+    r = fk.sdkde_flash(tr, q, fk.Bandwidth.uniform(h), ctx=ctx)
+    e["sdkde"] = max_component_rel(r.values, sd)
+    e["debiased"] = max_rowwise_rel(r.debiased_samples.values, deb)
+    # crit. 2 (acceptance_main.cpp:137-152): fused == non-fused Laplace
+    e["fused_vs_nonfused"] = max_rel_vs_peak(
+        fk.kde_flash(tr, q, h, fk.KernelKind.LaplaceCorrected, True, ctx=ctx).values,
+        fk.kde_flash(tr, q, h, fk.KernelKind.LaplaceCorrected, False, ctx=ctx).values)
+    _report(f"accept_{i:02d}", **e)
+    assert e["kde"] < TOL_DENS and e["laplace"] < TOL_LAP and e["score"] < TOL_SCORE
+    assert e["sdkde"] < TOL_DENS and e["debiased"] < TOL_DEB
+    assert e["fused_vs_nonfused"] < 1e-5
+
+
+@pytest.mark.slow
+def test_acceptance_crit8_shape(ctx, port):
+    # crit. 8 (acceptance_main.cpp:354-390): n = 32768, m = 4096, d = 16, h = 2.5,
+    # random Gaussian -- parity against the oracle, the >= 5x speed-up over the
+    # naive oracle, and a linear (never n^2) device workspace
+    import time
+    n, m, d = 32768, 4096, 16
+    tr = port.random_gaussian(n, d, 81, 1.0)
+    q = port.random_gaussian(m, d, 82, 1.0)
+    c = fk.Context([0])
+    best = 1e300
+    for _ in range(3):
+        t0 = time.perf_counter()
+        r = fk.sdkde_flash(tr, q, fk.Bandwidth.uniform(2.5), ctx=c)
+        best = min(best, time.perf_counter() - t0)
+    ws = c.workspace_bytes()
+    t0 = time.perf_counter()
+    ref_v, ref_deb = port.sdkde_naive(tr, q, 2.5, threads=1)   # the reference's serial oracle
+    naive = time.perf_counter() - t0
+    e = dict(sdkde=max_component_rel(r.values, ref_v),
+             debiased=max_rowwise_rel(r.debiased_samples.values, ref_deb))
+    _report("crit8", speedup=naive / best, **e)
+    assert e["sdkde"] < TOL_DENS and e["debiased"] < TOL_DEB
+    assert naive >= 5.0 * best
+    # n^2 fp64 would be 8 GiB; the engine's workspace is linear in n + m
+    assert ws < 64 * 2**20 + 4096 * (n + m), ws
+    c.close()
+
+
+def test_device_workspace_is_linear(port):
+    # test_engine.cpp:218-243 analogue: the device workspace of every pass grows
+    # linearly in the data (no n x m buffer); 4x the points -> at most ~4x bytes
+    sizes = []
+    for n in (8192, 32768):
+        c = fk.Context([0])
+        tr = port.random_gaussian(n, 16, 63)
+        q = port.random_gaussian(n // 4, 16, 64)
+        fk.kde_flash(tr, q, 0.9, ctx=c)
+        fk.score_flash(tr, 0.9, ctx=c)
+        fk.sdkde_flash(tr, q, fk.Bandwidth.uniform(0.9), ctx=c)
+        sizes.append(c.workspace_bytes())
+        c.close()
+    print("workspace bytes", sizes)
+    fixed = 48 * 2**20    # n-independent: direct-row partials, counters, rounding
+    assert sizes[1] - fixed <= 4.5 * max(sizes[0] - fixed, 1) + 8 * 2**20
+    assert sizes[1] < 64 * 2**20 + 4096 * (32768 + 8192)
+
+
+def test_moderate_spread_stays_on_tensor_cores_within_tolerance(ctx, port):
+    # |y|^2/2 up to ~200 (just under the direct-row threshold, above every BASELINE
+    # config's maximum of ~170): the expansion's rounding must stay inside 1e-3
+    centres = np.array([[10.0, 0, 0, 0], [-10.0, 0, 0, 0], [0, 10.0, 0, 0], [0, -10.0, 0, 0]])
+    tr = port.random_gaussian(2000, 4, 91) + np.repeat(centres, 500, axis=0)
+    q = port.random_gaussian(200, 4, 92) + np.repeat(centres, 50, axis=0)
+    h = 0.62
+    s = fk.score_flash(tr, h, ctx=ctx).values
+    ref_s = port.score_naive(tr, tr, h)
+    v = fk.kde_flash(tr, q, h, ctx=ctx).values
+    ref_v = port.kde_naive(tr, q, h)
+    e = dict(score_global=max_rel_global_floor(s, ref_s), score_rowwise=max_rowwise_rel(s, ref_s),
+             density=max_component_rel(v, ref_v))
+    _report("moderate-spread", **e)
+    assert e["score_global"] < TOL_SCORE and e["score_rowwise"] < TOL_SCORE
+    assert e["density"] < TOL_DENS
+
+
+def test_small_bandwidth_rows_fall_back_without_cliff(port):
+    # config-1 data at h/3: many rows have too little neighbour mass for fp16 P and
+    # go to the direct-difference kernel; results stay at fp64-oracle accuracy
+    c = golden("config1")
+    tr, q = _mixture_inputs(port, 4096, 4096)
+    h = float(c["h"]) / 3
+    ctx = fk.Context([0])
+    r = fk.sdkde_flash(tr, q, fk.Bandwidth.uniform(h), ctx=ctx)
+    ctx.close()
+    ref_v, ref_deb = port.sdkde_naive(tr, q, h, threads=os.cpu_count())
+    e = dict(sdkde=max_component_rel(r.values, ref_v),
+             debiased=max_rowwise_rel(r.debiased_samples.values, ref_deb))
+    _report("h/3", **e)
+    assert e["sdkde"] < TOL_DENS and e["debiased"] < TOL_DEB
 
 
 def test_device_api_graph_replay_is_bitwise(ctx, port):
