@@ -76,8 +76,11 @@ enum {
                                  extended-precision register sums every k column
                                  tiles; k a power of two in [1, 2^20], or 0 for
                                  the default (~256 columns)                      */
-    FKDE_OPT_TRACE_PTR = 6    /* debug: device pointer (32*8*256 int64) receiving
+    FKDE_OPT_TRACE_PTR = 6,   /* debug: device pointer (32*8*256 int64) receiving
                                  clock64 stamps of the score kernel's block 0   */
+    FKDE_OPT_SPATIAL = 7      /* score pass on a spatial (Morton / principal-axis)
+                                 order of the points with exact-zero tile skipping:
+                                 0 = auto (n >= 32768), 1 = always, 2 = never    */
 };
 enum { FKDE_ENGINE_TC = 0 };
 
@@ -115,6 +118,11 @@ void* fkde_gpu_stream(fkde_gpu_ctx* ctx);
 int fkde_gpu_last_timing(const fkde_gpu_ctx* ctx, float* ms, int n);
 /* number of kernels this library launched during the last call (this rank) */
 int64_t fkde_gpu_last_launch_count(const fkde_gpu_ctx* ctx);
+/* score-pass tile skipping of the last call on device 0 (synchronises):
+ * out[0] = quadrant-tiles checked, out[1] = quadrant-tiles whose P was all zero
+ * (exps skipped), out[2] = tiles whose GEMM2 was skipped, out[3] = 1 if the
+ * pass ran on the spatial order */
+int fkde_gpu_last_skip_stats(fkde_gpu_ctx* ctx, uint64_t* out4);
 /* device workspace currently held by the context (all devices), bytes: the
  * analogue of the reference's transient-allocation accounting
  * (alloc_stats, test_engine.cpp:218-243) -- linear in n + m, never n x m */

@@ -29,6 +29,7 @@ KERNEL_LAPLACE_CORRECTED = 1
 METHOD_KDE, METHOD_SDKDE, METHOD_LAPLACE = 0, 1, 2
 
 OPT_ENGINE, OPT_SPLITS, OPT_TIMING, OPT_MAX_CTAS, OPT_FLUSH_TILES = 1, 2, 3, 4, 5
+OPT_SPATIAL = 7
 ENGINE_TC = 0
 
 T_PREP, T_SCORE, T_FINALIZE, T_GATHER, T_QUERY, T_REDUCE, T_TOTAL, T_COUNT = range(8)
@@ -40,7 +41,7 @@ EXPORTED_SYMBOLS = (
     "fkde_gpu_score", "fkde_gpu_score_accumulate", "fkde_gpu_kde", "fkde_gpu_sdkde",
     "fkde_gpu_estimate", "fkde_gpu_pairwise_sq_dists", "fkde_gpu_sdkde_device",
     "fkde_gpu_kde_device", "fkde_gpu_score_device", "fkde_gpu_shard_range",
-    "fkde_gpu_workspace_bytes",
+    "fkde_gpu_workspace_bytes", "fkde_gpu_last_skip_stats",
 )
 HOST_SYMBOLS = (
     "fkde_host_mix64", "fkde_host_random_gaussian", "fkde_host_sample_mixture",
@@ -83,6 +84,7 @@ def _declare(lib):
     lib.fkde_gpu_last_launch_count.argtypes = [_vp]
     lib.fkde_gpu_last_launch_count.restype = ctypes.c_int64
     lib.fkde_gpu_workspace_bytes.argtypes = [_vp, _szp]
+    lib.fkde_gpu_last_skip_stats.argtypes = [_vp, ctypes.POINTER(ctypes.c_uint64)]
     lib.fkde_gpu_score.argtypes = [_vp, _dp, _sz, _sz, ctypes.c_double, _dp, _szp]
     lib.fkde_gpu_score_accumulate.argtypes = [_vp, _dp, _sz, _sz, ctypes.c_double, _dp, _dp]
     lib.fkde_gpu_kde.argtypes = [_vp, _dp, _sz, _dp, _sz, _sz, ctypes.c_double, ctypes.c_int,

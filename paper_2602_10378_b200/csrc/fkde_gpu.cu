@@ -36,6 +36,9 @@
 #include "pairwise_tc.cuh"
 #include "prep_kernels.cuh"
 #include "direct_rows.cuh"
+#include "spatial_order.cuh"
+
+#include <cub/device/device_radix_sort.cuh>
 
 using namespace fkde_b200;
 
@@ -160,6 +163,7 @@ Status ensure(DevBuf& b, size_t bytes) {
 
 struct Options {
     int engine = FKDE_ENGINE_TC;
+    int spatial = 0;       // FKDE_OPT_SPATIAL: 0 auto (n >= kSpatialMinN), 1 on, 2 off
     int splits = 0;
     int timing = 0;
     int max_ctas = 0;
@@ -179,6 +183,10 @@ struct Device {
     bool attrs_set = false;
     DevBuf X, Y, opA, opB, part0, part1, xsd, out, aux0, aux1, colpart, scal, err, flags;
     DevBuf risk, dpart, ddone;   // direct_rows_kernel: spread flags, partials, counters
+    // spatial order of the score pass (spatial_order.cuh): sorted points, permutation,
+    // keys, CUB scratch, axes, tile centroids, skip statistics, un-permuted outputs
+    DevBuf Xs, perm, keys, cubtmp, ordsc, cenA, cenB, skipstats, unperm0, unperm1;
+    bool ordered = false;        // last score pass ran on the spatial order
     cudaEvent_t ev[FKDE_T_COUNT + 1] = {};
     int64_t launches = 0;
     // device-resident API: the call's whole device program as a CUDA graph,
@@ -414,14 +422,61 @@ struct Job {
     bool sync = true;
 };
 
+// smallest n for which the score pass runs on the spatial order by default: below
+// it the few extra launches outweigh the skipped tiles (BASELINE configs 2-5 use it)
+constexpr size_t kSpatialMinN = 32768;
+// centroid half-distance^2 (log2 units) above which a tile pair is checked for
+// skipping: skipping needs max log2 phi' < -26, i.e. r^2/2 > 41 for every pair
+constexpr float kSkipPredict = 40.0f;
+
+bool use_spatial(const Options& o, size_t n) {
+    return o.spatial == 1 || (o.spatial == 0 && n >= kSpatialMinN);
+}
+
+// Spatial order of the training points (spatial_order.cuh): D.Xs = X[perm],
+// D.perm = perm.  Identical on every rank (deterministic from the same input).
+Status spatial_order(Device& D, const double* dX, size_t n, int d, const PassScalars* sc) {
+    const int nparts = static_cast<int>(std::min<size_t>(296, std::max<size_t>(1, n / 256)));
+    STATUS_TRY(ensure(D.colpart, static_cast<size_t>(nparts) * 256 * sizeof(double)));
+    STATUS_TRY(ensure(D.ordsc, sizeof(OrderScalars)));
+    cov_stage1<<<nparts, 256, 0, D.stream>>>(dX, n, d, sc, D.colpart.as<double>());
+    order_axes<<<1, 256, 0, D.stream>>>(D.colpart.as<double>(), nparts, d, D.ordsc.as<OrderScalars>());
+    STATUS_TRY(ensure(D.keys, 2 * n * sizeof(uint32_t)));        // keys in | keys out
+    STATUS_TRY(ensure(D.perm, 2 * n * sizeof(uint32_t)));        // idx in | perm
+    uint32_t* kin = D.keys.as<uint32_t>();
+    uint32_t* kout = kin + n;
+    uint32_t* iin = D.perm.as<uint32_t>() + n;
+    uint32_t* perm = D.perm.as<uint32_t>();
+    morton_keys<<<grid1(n, 256), 256, 0, D.stream>>>(dX, n, d, std::sqrt(static_cast<double>(n)), sc,
+                                                      D.ordsc.as<OrderScalars>(), kin, iin);
+    size_t tmp = 0;
+    CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin, kout, iin, perm, static_cast<int>(n),
+                                             0, kOrderAxes * kMortonBits, D.stream));
+    STATUS_TRY(ensure(D.cubtmp, tmp));
+    CUDA_TRY(cub::DeviceRadixSort::SortPairs(D.cubtmp.p, tmp, kin, kout, iin, perm, static_cast<int>(n),
+                                             0, kOrderAxes * kMortonBits, D.stream));
+    STATUS_TRY(ensure(D.Xs, n * d * sizeof(double)));
+    gather_rows<<<grid1(n * d, 256), 256, 0, D.stream>>>(dX, perm, n, d, D.Xs.as<double>());
+    D.launches += 4;   // (+ CUB's own sort kernels)
+    CUDA_TRY(cudaGetLastError());
+    return {};
+}
+
 // Score pass on this rank's row shard; leaves the requested per-row outputs in
-// D.aux0 / D.aux1 / D.xsd in global row layout (gathered when world > 1).
+// D.aux0 / D.aux1 / D.xsd in global row layout (gathered when world > 1).  With
+// the spatial order (D.ordered) that layout is the sorted one: unpermute_score()
+// restores the caller's order for the host / device outputs.
 Status score_program(Device& D, const Options& o, const Job& J, const double* dX,
                      PassScalars* sc, bool want_xsd) {
     const int d = J.d;
     const size_t n = J.n;
     const double ks = std::sqrt(kLog2e) / J.h_score;
     STATUS_TRY(compute_mean(D, dX, n, d, sc));
+    D.ordered = use_spatial(o, n);
+    if (D.ordered) {
+        STATUS_TRY(spatial_order(D, dX, n, d, sc));
+        dX = D.Xs.as<double>();
+    }
     max_half_norm<<<grid1(n, 256), 256, 0, D.stream>>>(dX, n, d, ks, sc, sc);
     set_scale_exponent<<<1, 1, 0, D.stream>>>(sc);
     D.launches += 2;
@@ -463,6 +518,21 @@ Status score_program(Device& D, const Options& o, const Job& J, const double* dX
     a.rows_pad = rows_pad;
     a.diag_row0 = static_cast<long long>(sh.begin);
     a.trace = o.trace;
+    STATUS_TRY(ensure(D.skipstats, 4 * sizeof(unsigned long long)));
+    CUDA_TRY(cudaMemsetAsync(D.skipstats.p, 0, 4 * sizeof(unsigned long long), D.stream));
+    a.stats = D.skipstats.as<unsigned long long>();
+    if (D.ordered) {
+        STATUS_TRY(ensure(D.cenA, rt * kMaxDim * sizeof(float)));
+        STATUS_TRY(ensure(D.cenB, ct * kMaxDim * sizeof(float)));
+        tile_centroids<<<static_cast<unsigned>(rt), 128, 0, D.stream>>>(
+            dX + sh.begin * d, sh.rows, d, sc, ks, kTileRows, D.cenA.as<float>());
+        tile_centroids<<<static_cast<unsigned>(ct), 128, 0, D.stream>>>(
+            dX, n, d, sc, ks, static_cast<int>(kScoreNCol), D.cenB.as<float>());
+        D.launches += 2;
+        a.cenA = D.cenA.as<float>();
+        a.cenB = D.cenB.as<float>();
+        a.skip_pred = kSkipPredict;
+    }
     STATUS_TRY(launch_pairwise<kModeScore>(D, o, a, n));
     record(D, o, FKDE_T_FINALIZE);
 
@@ -531,6 +601,24 @@ Status score_program(Device& D, const Options& o, const Job& J, const double* dX
         STATUS_TRY(allgather(D, D.aux1.p, sh.chunk * d, ncclFloat64));
     }
     if (want_xsd) STATUS_TRY(allgather(D, D.xsd.p, sh.chunk * d, ncclFloat64));
+    if (D.ordered) {   // per-row outputs back to the caller's order
+        const uint32_t* perm = D.perm.as<uint32_t>();
+        if (J.kind == Job::kScore) {
+            STATUS_TRY(ensure(D.unperm0, n * d * sizeof(double)));
+            scatter_rows<<<grid1(n * d, 256), 256, 0, D.stream>>>(D.aux0.as<double>(), perm, n, d,
+                                                                  nullptr, D.unperm0.as<double>());
+            ++D.launches;
+        } else if (J.kind == Job::kScoreAcc) {
+            STATUS_TRY(ensure(D.unperm0, n * sizeof(double)));
+            STATUS_TRY(ensure(D.unperm1, n * d * sizeof(double)));
+            scatter_rows<<<grid1(n, 256), 256, 0, D.stream>>>(D.aux0.as<double>(), perm, n, 1,
+                                                              nullptr, D.unperm0.as<double>());
+            scatter_rows<<<grid1(n * d, 256), 256, 0, D.stream>>>(D.aux1.as<double>(), perm, n, d,
+                                                                  nullptr, D.unperm1.as<double>());
+            D.launches += 2;
+        }
+        CUDA_TRY(cudaGetLastError());
+    }
     return {};
 }
 
@@ -702,8 +790,12 @@ Status run_job(Device& D, const Options& o, const Job& J) {
                 // debiased samples to the host on the side stream, overlapping the
                 // density pass (it only reads D.xsd)
                 STATUS_TRY(ensure(D.aux1, J.n * d * sizeof(double)));
-                add_mean<<<grid1(J.n * d, 256), 256, 0, D.stream>>>(D.xsd.as<double>(), J.n, d, sc_s,
-                                                                    D.aux1.as<double>());
+                if (D.ordered)   // x_sd = x_sd_c + mu, back in the caller's order
+                    scatter_rows<<<grid1(J.n * d, 256), 256, 0, D.stream>>>(
+                        D.xsd.as<double>(), D.perm.as<uint32_t>(), J.n, d, sc_s, D.aux1.as<double>());
+                else
+                    add_mean<<<grid1(J.n * d, 256), 256, 0, D.stream>>>(D.xsd.as<double>(), J.n, d,
+                                                                        sc_s, D.aux1.as<double>());
                 ++D.launches;
                 CUDA_TRY(cudaGetLastError());
                 CUDA_TRY(cudaEventRecord(D.ev_side_in, D.stream));
@@ -746,19 +838,20 @@ Status run_job(Device& D, const Options& o, const Job& J) {
         if (J.kind == Job::kSdkde && J.out2)   // the side-stream copy joins the main stream
             CUDA_TRY(cudaStreamWaitEvent(D.stream, D.ev_side_out, 0));
     } else if (J.kind == Job::kScore) {   // (host outputs only on the first device)
+        const void* src = D.ordered ? D.unperm0.p : D.aux0.p;
         if (J.d_out)
-            CUDA_TRY(cudaMemcpyAsync(J.d_out, D.aux0.p, nd * sizeof(double),
-                                     cudaMemcpyDeviceToDevice, D.stream));
+            CUDA_TRY(cudaMemcpyAsync(J.d_out, src, nd * sizeof(double), cudaMemcpyDeviceToDevice,
+                                     D.stream));
         if (J.out)
-            CUDA_TRY(cudaMemcpyAsync(J.out, D.aux0.p, nd * sizeof(double), cudaMemcpyDeviceToHost,
+            CUDA_TRY(cudaMemcpyAsync(J.out, src, nd * sizeof(double), cudaMemcpyDeviceToHost,
                                      D.stream));
     } else if (J.kind == Job::kScoreAcc) {
         if (J.out)
-            CUDA_TRY(cudaMemcpyAsync(J.out, D.aux0.p, J.n * sizeof(double), cudaMemcpyDeviceToHost,
-                                     D.stream));
+            CUDA_TRY(cudaMemcpyAsync(J.out, D.ordered ? D.unperm0.p : D.aux0.p, J.n * sizeof(double),
+                                     cudaMemcpyDeviceToHost, D.stream));
         if (J.out2)
-            CUDA_TRY(cudaMemcpyAsync(J.out2, D.aux1.p, nd * sizeof(double), cudaMemcpyDeviceToHost,
-                                     D.stream));
+            CUDA_TRY(cudaMemcpyAsync(J.out2, D.ordered ? D.unperm1.p : D.aux1.p, nd * sizeof(double),
+                                     cudaMemcpyDeviceToHost, D.stream));
     }
     record(D, o, FKDE_T_TOTAL);
     if (!J.sync) return {};
@@ -772,6 +865,11 @@ Status run_job(Device& D, const Options& o, const Job& J) {
     if (J.kind == Job::kScore || J.kind == Job::kScoreAcc || J.kind == Job::kSdkde) {
         unsigned long long row = ~0ull;
         CUDA_TRY(cudaMemcpy(&row, D.err.p, sizeof(row), cudaMemcpyDeviceToHost));
+        if (row != ~0ull && D.ordered) {   // sorted position -> the caller's row index
+            uint32_t orig = 0;
+            CUDA_TRY(cudaMemcpy(&orig, D.perm.as<uint32_t>() + row, sizeof(orig), cudaMemcpyDeviceToHost));
+            row = orig;
+        }
         if (row != ~0ull && J.kind != Job::kScoreAcc) {
             Status s = make_status(FKDE_SCORE_UNDERFLOW,
                                    "score denominator underflowed to zero at train point %llu",
@@ -958,7 +1056,9 @@ void fkde_gpu_destroy(fkde_gpu_ctx* ctx) {
         if (D.comm && nccl().loaded) nccl().CommDestroy(D.comm);
         DevBuf* bufs[] = {&D.X,    &D.Y,     &D.opA,  &D.opB, &D.part0, &D.part1,
                           &D.xsd,  &D.out,   &D.aux0, &D.aux1, &D.colpart, &D.scal,
-                          &D.err,  &D.flags, &D.risk, &D.dpart, &D.ddone};
+                          &D.err,  &D.flags, &D.risk, &D.dpart, &D.ddone,
+                          &D.Xs,   &D.perm,  &D.keys, &D.cubtmp, &D.ordsc, &D.cenA,
+                          &D.cenB, &D.skipstats, &D.unperm0, &D.unperm1};
         for (DevBuf* b : bufs)
             if (b->p) cudaFree(b->p);
         for (auto& e : D.ev)
@@ -1004,6 +1104,10 @@ int fkde_gpu_set_option(fkde_gpu_ctx* ctx, int key, int64_t value) {
             return FKDE_OK;
         case FKDE_OPT_TRACE_PTR:
             ctx->opt.trace = reinterpret_cast<long long*>(value);
+            return FKDE_OK;
+        case FKDE_OPT_SPATIAL:
+            if (value < 0 || value > 2) return FKDE_INVALID_ARGUMENT;
+            ctx->opt.spatial = static_cast<int>(value);
             return FKDE_OK;
         case FKDE_OPT_FLUSH_TILES:
             if (value < 0 || value > 1 << 20 || (value & (value - 1))) return FKDE_INVALID_ARGUMENT;
@@ -1051,10 +1155,27 @@ int fkde_gpu_workspace_bytes(const fkde_gpu_ctx* ctx, size_t* bytes) {
     for (const Device& D : ctx->devs) {
         const DevBuf* bufs[] = {&D.X,    &D.Y,     &D.opA,  &D.opB,  &D.part0,   &D.part1,
                                 &D.xsd,  &D.out,   &D.aux0, &D.aux1, &D.colpart, &D.scal,
-                                &D.err,  &D.flags, &D.risk, &D.dpart, &D.ddone};
+                                &D.err,  &D.flags, &D.risk, &D.dpart, &D.ddone,
+                                &D.Xs,   &D.perm,  &D.keys, &D.cubtmp, &D.ordsc, &D.cenA,
+                                &D.cenB, &D.skipstats, &D.unperm0, &D.unperm1};
         for (const DevBuf* b : bufs) total += b->bytes;
     }
     *bytes = total;
+    return FKDE_OK;
+}
+
+int fkde_gpu_last_skip_stats(fkde_gpu_ctx* ctx, uint64_t* out4) {
+    if (!ctx || !out4) return FKDE_INVALID_ARGUMENT;
+    const Device& D = ctx->devs[0];
+    for (int i = 0; i < 4; ++i) out4[i] = 0;
+    if (!D.skipstats.p) return FKDE_OK;
+    cudaSetDevice(D.dev);
+    if (cudaStreamSynchronize(D.stream) != cudaSuccess) return FKDE_CUDA_ERROR;
+    unsigned long long h[3] = {0, 0, 0};
+    if (cudaMemcpy(h, D.skipstats.p, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess)
+        return FKDE_CUDA_ERROR;
+    for (int i = 0; i < 3; ++i) out4[i] = h[i];
+    out4[3] = D.ordered ? 1 : 0;
     return FKDE_OK;
 }
 
@@ -1225,10 +1346,10 @@ Status run_device_job(fkde_gpu_ctx* ctx, const Job& J) {
     // (per-phase event timing and the debug trace run eagerly)
     if (D.world != 1 || o.trace || o.timing) return run_job(D, o, J);
     char buf[512];
-    std::snprintf(buf, sizeof(buf), "%d|%p|%p|%p|%zu|%zu|%d|%a|%a|%d|%d|%d|%d|%d|%d|%d", J.kind,
+    std::snprintf(buf, sizeof(buf), "%d|%p|%p|%p|%zu|%zu|%d|%a|%a|%d|%d|%d|%d|%d|%d|%d|%d", J.kind,
                   (const void*)J.dX, (const void*)J.dY, (void*)J.d_out, J.n, J.m, J.d, J.h,
                   J.h_score, J.kernel, J.fused, o.engine, o.splits, o.timing, o.max_ctas,
-                  o.flush_tiles);
+                  o.flush_tiles, o.spatial);
     const std::string key(buf);
     CUDA_TRY(cudaSetDevice(D.dev));
     if (D.graph && key == D.graph_key && D.graph_epoch == g_alloc_epoch.load()) {

@@ -65,7 +65,20 @@ struct PairArgs {
     // debug (builds with -DFKDE_ENABLE_TRACE only): per-event clock64 trace of
     // block 0 (nullptr = off).  Layout [warp][event slot][tile] -> long long
     long long* trace;
+    // SCORE tile skipping (spatial_order.cuh): per-tile centroids (log2 units) of
+    // the row tiles (128) and column tiles (kNCol); a tile pair whose centroid
+    // half-distance^2 exceeds skip_pred is checked exactly (max log2 phi' over
+    // the tile) and, where every pair rounds to fp16 zero, its exps and (if all
+    // four lane quadrants agree) its GEMM2 are skipped.  nullptr = no skipping.
+    const float* cenA;
+    const float* cenB;
+    float skip_pred;
+    unsigned long long* stats;   // optional: [0] tiles checked (x4 quadrants),
+                                 // [1] quadrant-tiles skipped, [2] GEMM2 tiles skipped
 };
+// log2 phi' (S * dscale, with the 2^15 offset) below which both fp16 halves of
+// phi' are exactly zero (phi' < 2^-25 rounds to zero; one unit of margin for ex2.approx)
+constexpr float kSkipLog2 = -26.0f;
 #ifdef FKDE_ENABLE_TRACE
 #define FKDE_TRACE(slot, tile)                                                               \
     do {                                                                                     \
@@ -179,6 +192,9 @@ pairwise_tc_kernel(PairArgs args) {
     uint64_t* o_full = s_free + kSB;      // [2]
     uint64_t* o_empty = o_full + 2;       // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
+    // score: per S/P buffer, one byte per lane quadrant = "this quadrant's P is all zero"
+    // (written before p_full's arrive, read by the GEMM2 warp after its wait)
+    uint32_t* skipf = tmem_slot + 1;   // [kSBuf]
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -269,6 +285,7 @@ pairwise_tc_kernel(PairArgs args) {
         const uint64_t descB = ptx::smem_desc_sw128(ptx::smem_u32(smB), 16, 1024);
         const uint64_t descBmn = ptx::smem_desc_sw128(ptx::smem_u32(smB), kTileBytes, 1024);
         uint32_t it_a = 0, it_b = 0, it_s = 0, it_u = 0;
+        bool o_started = false;   // GEMM2: an MMA has written the current O sub-unit
         const bool g1 = warp == 1;
         // GEMM2 (warp 10): O += P_hi.B + P_lo.B, P read from TMEM.  The
         // epilogue stored, for each 32-column chunk c of S buffer sb, P_hi
@@ -327,27 +344,39 @@ pairwise_tc_kernel(PairArgs args) {
                     FKDE_TRACE(2, it_s);
                     ptx::mbar_wait(&p_full[sb], ph);
                     FKDE_TRACE(3, it_s);
-                    if (first) ptx::mbar_wait(&o_empty[ob], ((it_u >> 1) & 1) ^ 1);
+                    if (first) {
+                        ptx::mbar_wait(&o_empty[ob], ((it_u >> 1) & 1) ^ 1);
+                        o_started = false;
+                    }
+                    // every lane quadrant's P of this tile is zero: no MMA needed,
+                    // unless the sub-unit would otherwise end with O never written
+                    const bool all_zero = *reinterpret_cast<volatile uint32_t*>(&skipf[sb]) == 0x01010101u;
+                    const bool issue = !all_zero || (last && !o_started);
                     ptx::tc_fence_after();
                     if (ptx::elect_one()) {
-                        const uint64_t db0 = descBmn + ((st * kTileBytes) >> 4);
-                        const uint32_t ta0 = tmem_base + sb * Cfg::kNCol;
-                        const uint32_t to = tmem_base + Cfg::kTmemO + ob * 64;
+                        if (issue) {
+                            const uint64_t db0 = descBmn + ((st * kTileBytes) >> 4);
+                            const uint32_t ta0 = tmem_base + sb * Cfg::kNCol;
+                            const uint32_t to = tmem_base + Cfg::kTmemO + ob * 64;
 #pragma unroll
-                        for (int k = 0; k < Cfg::kNCol / 16; ++k) {
+                            for (int k = 0; k < Cfg::kNCol / 16; ++k) {
 #pragma unroll
-                            for (int part = 0; part < 2; ++part) {
-                                // one N=48 MMA per K step: columns 0-15 T_hi, 16 S, 32-47 T_lo
-                                ptx::umma_f16_ts(to, ta0 + (k >> 1) * 32 + part * 16 + (k & 1) * 8,
-                                                 db0 + ((k * 2048) >> 4), part ? idesc2_lo : idesc2,
-                                                 (first && part == 0 && k == 0) ? 0u : 1u);
+                                for (int part = 0; part < 2; ++part) {
+                                    // one N=48 MMA per K step: columns 0-15 T_hi, 16 S, 32-47 T_lo
+                                    ptx::umma_f16_ts(to, ta0 + (k >> 1) * 32 + part * 16 + (k & 1) * 8,
+                                                     db0 + ((k * 2048) >> 4), part ? idesc2_lo : idesc2,
+                                                     (!o_started && part == 0 && k == 0) ? 0u : 1u);
+                                }
                             }
+                        } else if (args.stats) {
+                            atomicAdd(&args.stats[2], 1ull);
                         }
                         ptx::umma_commit(&b_empty[st]);
                         ptx::umma_commit(&s_free[sb]);
                         if (last) ptx::umma_commit(&o_full[ob]);
                     }
                     __syncwarp();
+                    o_started = o_started || issue;
                     FKDE_TRACE(5, it_s);
                     if (last) ++it_u;
                 }
@@ -477,8 +506,48 @@ pairwise_tc_kernel(PairArgs args) {
                                           : -1;   // this row's diagonal column (if in this tile)
                     const float2 neg1 = make_float2(-1.f, -1.f);
                     const float2 vk2 = make_float2(8193.f, 8193.f);   // 2^13 + 1
+                    // tile skipping: predicted from the tile centroids (warp-uniform),
+                    // then checked exactly on this quadrant's 32 rows
+                    bool skip = false;
+                    if (args.cenA) {
+                        const float* ca = args.cenA + (size_t)rt * kMaxDim;
+                        const float* cb = args.cenB + (size_t)(ct0 + rel) * kMaxDim;
+                        float dd = 0.f;
+#pragma unroll
+                        for (int c = 0; c < kMaxDim; ++c) {
+                            const float df = __ldg(ca + c) - __ldg(cb + c);
+                            dd = fmaf(df, df, dd);
+                        }
+                        if (0.5f * dd > args.skip_pred) {
+                            float mx = -INFINITY;
 #pragma unroll 1
-                    for (int ch = 0; ch < Cfg::kNCol / 32; ++ch) {
+                            for (int ch = 0; ch < Cfg::kNCol / 32; ++ch) {
+                                uint32_t v[32];
+                                ptx::tmem_ld32(ts + ch * 32, v);
+                                ptx::tmem_ld_wait();
+#pragma unroll
+                                for (int c = 0; c < 32; ++c) mx = fmaxf(mx, __uint_as_float(v[c]));
+                            }
+                            skip = __all_sync(0xffffffffu, mx * dsc < kSkipLog2);
+                            if (args.stats && lane == 0) {
+                                atomicAdd(&args.stats[0], 1ull);
+                                if (skip) atomicAdd(&args.stats[1], 1ull);
+                            }
+                        }
+                    }
+                    if (skip) {   // P = 0 for this quadrant (GEMM2 may still read it)
+                        uint32_t z[16];
+#pragma unroll
+                        for (int w = 0; w < 16; ++w) z[w] = 0u;
+#pragma unroll
+                        for (int ch = 0; ch < Cfg::kNCol / 32; ++ch) {
+                            ptx::tmem_st16(ts + ch * 32, z);
+                            ptx::tmem_st16(ts + ch * 32 + 16, z);
+                        }
+                    }
+                    if (lane == 0) reinterpret_cast<volatile uint8_t*>(&skipf[sb])[q] = skip ? 1 : 0;
+#pragma unroll 1
+                    for (int ch = 0; ch < (skip ? 0 : Cfg::kNCol / 32); ++ch) {
                         uint32_t v[32];
                         ptx::tmem_ld32(ts + ch * 32, v);
                         ptx::tmem_ld_wait();

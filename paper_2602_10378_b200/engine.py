@@ -108,6 +108,13 @@ class Context:
     def last_launch_count(self) -> int:
         return int(self._lib.fkde_gpu_last_launch_count(self._h))
 
+    def skip_stats(self) -> dict:
+        """Tile skipping of the last score pass (fkde_gpu_last_skip_stats)."""
+        b = (ctypes.c_uint64 * 4)()
+        self._lib.fkde_gpu_last_skip_stats(self._h, b)
+        return {"quadrant_tiles_checked": int(b[0]), "quadrant_tiles_skipped": int(b[1]),
+                "gemm2_tiles_skipped": int(b[2]), "spatial_order": bool(b[3])}
+
     def workspace_bytes(self) -> int:
         b = ctypes.c_size_t(0)
         self._lib.fkde_gpu_workspace_bytes(self._h, ctypes.byref(b))

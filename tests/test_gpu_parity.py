@@ -639,6 +639,58 @@ def test_moderate_spread_stays_on_tensor_cores_within_tolerance(ctx, port):
     assert e["density"] < TOL_DENS
 
 
+@pytest.mark.parametrize("n,d,h", [(5000, 16, 1.3), (3000, 4, 0.6), (700, 2, 0.4), (257, 16, 2.0)])
+def test_spatial_order_matches_input_order(port, n, d, h):
+    # FKDE_OPT_SPATIAL=1 (Morton order + exact-zero tile skipping) vs 2 (input
+    # order): same results within fp32 reassociation, both against the oracle,
+    # outputs in the caller's row order (scores, debiased samples, raw sums)
+    w, mu, s = __import__("oracle").default_mixture_16d()
+    if d == 16:
+        tr, q = _mixture_inputs(port, n, n // 4 + 1)
+    else:
+        tr = port.random_gaussian(n, d, 700 + n, 1.0) + np.repeat(
+            np.eye(4, d) * 6.0, -(-n // 4), axis=0)[:n]
+        q = port.random_gaussian(n // 4 + 1, d, 800 + n, 1.0)
+    outs = {}
+    for sp in (1, 2):
+        c = fk.Context([0])
+        c.set_option(N.OPT_SPATIAL, sp)
+        sc = fk.score_flash(tr, h, ctx=c).values
+        st = c.skip_stats()
+        r = fk.sdkde_flash(tr, q, fk.Bandwidth.uniform(h), ctx=c)
+        acc = fk.score_accumulate(tr, h, ctx=c)
+        outs[sp] = (sc, r.values, r.debiased_samples.values, acc.phi_sum, acc.weighted_sum.values, st)
+        c.close()
+    assert outs[1][5]["spatial_order"] and not outs[2][5]["spatial_order"]
+    ref_s = port.score_naive(tr, tr, h)
+    ref_v, ref_deb = port.sdkde_naive(tr, q, h)
+    for sp in (1, 2):
+        sc, v, deb, phi, wsum, _ = outs[sp]
+        assert max_rel_global_floor(sc, ref_s) < TOL_SCORE, sp
+        assert max_rowwise_rel(sc, ref_s) < TOL_SCORE, sp
+        assert max_component_rel(v, ref_v) < TOL_DENS, sp
+        assert max_rowwise_rel(deb, ref_deb) < TOL_DEB, sp
+    assert max_component_rel(outs[1][3], outs[2][3]) < 1e-5
+    assert max_rowwise_rel(outs[1][4], outs[2][4]) < 1e-5
+    print("skip stats", outs[1][5])
+
+
+def test_spatial_order_skips_tiles_on_clustered_data(port):
+    # four far-apart clusters: most tile pairs contribute exactly zero and are skipped
+    tr = port.random_gaussian(8192, 16, 97) + np.repeat(np.eye(4, 16) * 40.0, 2048, axis=0)
+    h = 3.0   # |y|^2/2 ~ 50 (tensor-core rows), clusters ~250 log2 units apart
+    c = fk.Context([0])
+    c.set_option(N.OPT_SPATIAL, 1)
+    s = fk.score_flash(tr, h, ctx=c).values
+    st = c.skip_stats()
+    c.close()
+    print("skip stats", st)
+    assert st["quadrant_tiles_skipped"] > 0 and st["gemm2_tiles_skipped"] > 0
+    rows = np.arange(0, 8192, 7)
+    ref = port.score_naive(tr, tr[rows], h)
+    assert max_rowwise_rel(s[rows], ref) < TOL_SCORE
+
+
 def test_small_bandwidth_rows_fall_back_without_cliff(port):
     # config-1 data at h/3: many rows have too little neighbour mass for fp16 P and
     # go to the direct-difference kernel; results stay at fp64-oracle accuracy
