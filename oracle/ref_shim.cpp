@@ -14,7 +14,9 @@
 //   fkde::io::{write_samples_bin, write_samples_csv, write_values} (io.hpp) and
 //   fkde::bench::{load_mixture, mixture_hash, mixture_pdf} (mixture.hpp),
 //   fkde::perfmodel::{flops_nd, flops_1d, bytes_nd, bytes_1d, bytes_linear,
-//   intensity_asymptotic} (perfmodel.hpp) -- the §8f rows' file formats and models
+//   intensity_asymptotic} (perfmodel.hpp) -- the §8f rows' file formats and models,
+//   fkde::bench::error_metrics (metrics.hpp:31-32, metrics.cpp:47-120) with the
+//   estimator supplied by the caller (a C callback: the GPU engine or the oracle)
 #include <cstring>
 #include <exception>
 #include <thread>
@@ -25,6 +27,7 @@
 #include "fkde/io.hpp"
 #include "fkde/perfmodel.hpp"
 #include "fkde/kernels.hpp"
+#include "fkde/metrics.hpp"
 #include "fkde/mixture.hpp"
 #include "fkde/oracle.hpp"
 #include "fkde/rng.hpp"
@@ -259,6 +262,31 @@ int fkr_mixture_pdf(const char* config_path, const double* x, std::size_t n, dou
         const auto mix = bench::load_mixture(config_path);
         const auto v = bench::mixture_pdf(mix, make_set(x, n, mix.dim()));
         std::memcpy(out, v.data(), n * 8);
+        return 0;
+    } catch (...) {
+        return map_exception(nullptr);
+    }
+}
+// error_metrics(estimate_at, mixture, mode, n_eval, seed): the estimator is
+// the callback est(points, n, d, out, user) -> 0 on success.  out6 = {mise,
+// mise_se, miae, miae_se, negative_mass, negative_mass_se}.
+typedef int (*fkr_estimate_cb)(const double* pts, std::size_t n, std::size_t d, double* out,
+                               void* user);
+int fkr_error_metrics(const char* config_path, int grid, std::size_t n_eval, std::uint64_t seed,
+                      fkr_estimate_cb est, void* user, double* out6) {
+    try {
+        const auto mix = bench::load_mixture(config_path);
+        const bench::EstimateFn fn = [&](const SampleSet& pts) {
+            std::vector<double> v(pts.n);
+            if (est(pts.values.data(), pts.n, pts.d, v.data(), user) != 0)
+                throw std::runtime_error("estimate callback failed");
+            return v;
+        };
+        const auto r = bench::error_metrics(
+            fn, mix, grid ? bench::ErrorMode::Grid1D : bench::ErrorMode::ImportanceMC, n_eval, seed);
+        const double o[6] = {r.mise, r.mise_se, r.miae, r.miae_se, r.negative_mass,
+                             r.negative_mass_se};
+        std::memcpy(out6, o, sizeof(o));
         return 0;
     } catch (...) {
         return map_exception(nullptr);

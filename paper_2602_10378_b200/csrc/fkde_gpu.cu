@@ -531,7 +531,11 @@ Status score_program(Device& D, const Options& o, const Job& J, const double* dX
         D.launches += 2;
         a.cenA = D.cenA.as<float>();
         a.cenB = D.cenB.as<float>();
-        a.skip_pred = kSkipPredict;
+        static const float pred = [] {   // debug override for A/B runs (tools/spatial_probe.py)
+            const char* e = std::getenv("FKDE_SKIP_PRED");
+            return e && *e ? static_cast<float>(std::atof(e)) : kSkipPredict;
+        }();
+        a.skip_pred = pred;
     }
     STATUS_TRY(launch_pairwise<kModeScore>(D, o, a, n));
     record(D, o, FKDE_T_FINALIZE);

@@ -79,6 +79,7 @@ struct PairArgs {
 // log2 phi' (S * dscale, with the 2^15 offset) below which both fp16 halves of
 // phi' are exactly zero (phi' < 2^-25 rounds to zero; one unit of margin for ex2.approx)
 constexpr float kSkipLog2 = -26.0f;
+constexpr uint32_t kCenBytes = kMaxDim * sizeof(float);   // one tile centroid
 #ifdef FKDE_ENABLE_TRACE
 #define FKDE_TRACE(slot, tile)                                                               \
     do {                                                                                     \
@@ -89,6 +90,10 @@ constexpr float kSkipLog2 = -26.0f;
 #define FKDE_TRACE(slot, tile) \
     do {                       \
     } while (0)
+#endif
+
+#ifndef FKDE_LO_SEPARATE
+#define FKDE_LO_SEPARATE 0
 #endif
 
 template <int MODE>
@@ -127,7 +132,14 @@ struct TcConfig {
         kScore ? (kLaunchRegs * kThreads - 128 * kCtrlRegs - 128 * kLaunchRegs) / (128 * kNP) / 8 * 8
                : 0;
     static_assert(!kScore || (kEpiRegs >= kLaunchRegs && kEpiRegs <= 256), "setmaxnreg split");
-    static constexpr int kStages = 8;
+    // B-stage ring: the score pass streams 12 KiB column tiles; with tile skipping a
+    // tile can be done in a fraction of its exp time, so the ring must cover the L2
+    // latency of many tiles in flight (ncu: GEMM1 waiting on b_full with 8 stages).
+    // Score stages are 13 KiB (tile + the centroid slot, 1 KiB aligned), KDE 16 KiB.
+#ifndef FKDE_SCORE_STAGES
+#define FKDE_SCORE_STAGES 14
+#endif
+    static constexpr int kStages = kScore ? FKDE_SCORE_STAGES : 8;
     static constexpr uint32_t kOffA = 0;
     // column tile width: score 96 points (4 S/P buffers of 96 TMEM columns fit
     // beside the two O buffers; 3 of 128 made the S ring the bottleneck), KDE 128
@@ -137,8 +149,10 @@ struct TcConfig {
     static constexpr int kNCol = kScore ? FKDE_SCORE_NCOL : 128;
     static constexpr uint32_t kColBytes = kNCol * kRowBytes;   // one B column tile
     static_assert(kNCol % 32 == 0 && kColBytes % 1024 == 0, "column tiles of whole SW128 atoms");
+    static constexpr uint32_t kBStride = kScore ? kColBytes + 1024 : kTileBytes;   // B stage stride
+    static_assert(kBStride % 1024 == 0 && (!kScore || kColBytes + 64 <= kBStride), "SW128 stages + centroid slot");
     static constexpr uint32_t kOffB = 2 * kTileBytes;
-    static constexpr uint32_t kOffAcc = kOffB + kStages * kTileBytes;
+    static constexpr uint32_t kOffAcc = kOffB + kStages * kBStride;
     static constexpr uint32_t kAccBytes = 0;
     static constexpr uint32_t kOffBar = kOffAcc + kAccBytes;
     // S accumulators in TMEM.  Score: 4 S/P buffers of 96 columns (a tile's S is
@@ -148,8 +162,15 @@ struct TcConfig {
     static constexpr uint32_t kNumBars = 4 + 2 * kStages + 4 * kSBuf + 4;
     // + tmem slot, 1 KiB alignment slack
     static constexpr uint32_t kSmemBytes = kOffBar + kNumBars * 8 + 64 + 1024;
+    static_assert(4 * (1 + kSBuf + 2) <= 64, "tmem slot + skip flags + o_zero fit the 64 B tail");
     static constexpr uint32_t kTmemCols = 512;
     static constexpr uint32_t kTmemO = 384;   // score: O[2] (2 x 64 cols: T_hi, S, T_lo)
+    // FKDE_LO_SEPARATE: the P_lo half of GEMM2 accumulates into its own 32 columns
+    // (O_lo, next to O), so the main accumulator takes half the MMA steps per tile
+    // and P_lo's small products are not truncated against the large main sums;
+    // the 80 columns fit once, so O is single-buffered
+    static constexpr int kOBuf = FKDE_LO_SEPARATE ? 1 : 2;
+    static constexpr uint32_t kOStride = 64;
     static_assert(!kScore || kSBuf * kNCol <= kTmemO, "S/P buffers overlap O");
     static constexpr uint32_t kN2 = 48;       // GEMM2 N
 };
@@ -166,6 +187,7 @@ struct TcConfig {
 #ifndef FKDE_G2_LO_N
 #define FKDE_G2_LO_N 32
 #endif
+
 
 template <int MODE>
 __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1)
@@ -195,6 +217,10 @@ pairwise_tc_kernel(PairArgs args) {
     // score: per S/P buffer, one byte per lane quadrant = "this quadrant's P is all zero"
     // (written before p_full's arrive, read by the GEMM2 warp after its wait)
     uint32_t* skipf = tmem_slot + 1;   // [kSBuf]
+    // score: O sub-unit produced no MMA (every tile of it skipped): one byte per
+    // drain warp, all set by the GEMM2 warp before its plain arrive on o_full, each
+    // cleared by its own drain warp before that warp releases the buffer (O = 0)
+    volatile uint32_t* o_zero = skipf + Cfg::kSBuf;   // [2] x 4 bytes
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -218,6 +244,7 @@ pairwise_tc_kernel(PairArgs args) {
             ptx::mbar_init(&o_full[i], 1);
             ptx::mbar_init(&o_empty[i], 4);
         }
+        if constexpr (kScore) o_zero[0] = o_zero[1] = 0u;
 
         ptx::fence_barrier_init();
     }
@@ -260,9 +287,15 @@ pairwise_tc_kernel(PairArgs args) {
                 const int st = it_b % kStages;
                 ptx::mbar_wait(&b_empty[st], ((it_b / kStages) & 1) ^ 1);
                 if (ptx::elect_one()) {
-                    ptx::mbar_arrive_expect_tx(&b_full[st], Cfg::kColBytes);
-                    ptx::bulk_g2s_hint(smB + st * kTileBytes, args.opB + (size_t)ct * Cfg::kColBytes,
+                    // score tile skipping: the column tile's centroid (64 B) rides in the
+                    // stage's unused tail, on the same barrier
+                    const uint32_t extra = (kScore && args.cenB) ? kCenBytes : 0u;
+                    ptx::mbar_arrive_expect_tx(&b_full[st], Cfg::kColBytes + extra);
+                    ptx::bulk_g2s_hint(smB + st * Cfg::kBStride, args.opB + (size_t)ct * Cfg::kColBytes,
                                        Cfg::kColBytes, &b_full[st], pol_b);
+                    if (extra)
+                        ptx::bulk_g2s(smB + st * Cfg::kBStride + Cfg::kColBytes,
+                                      args.cenB + (size_t)ct * kMaxDim, kCenBytes, &b_full[st]);
                 }
                 __syncwarp();
                 ++it_b;
@@ -280,12 +313,13 @@ pairwise_tc_kernel(PairArgs args) {
         constexpr uint32_t idesc2 = ptx::idesc_f16_f32(128, Cfg::kN2, false, true);
         // P_lo rows only need the y_hi and ones columns: P_lo . y_lo is 2^-22 of the
         // sum and is dropped, which takes 1/6 of GEMM2's MACs (and power) away
-        constexpr uint32_t idesc2_lo = ptx::idesc_f16_f32(128, FKDE_G2_LO_N, false, true);
+        constexpr uint32_t idesc2_lo = ptx::idesc_f16_f32(128, FKDE_G2_LO_N > 0 ? FKDE_G2_LO_N : 32, false, true);
         const uint64_t descA = ptx::smem_desc_sw128(ptx::smem_u32(smA), 16, 1024);
         const uint64_t descB = ptx::smem_desc_sw128(ptx::smem_u32(smB), 16, 1024);
         const uint64_t descBmn = ptx::smem_desc_sw128(ptx::smem_u32(smB), kTileBytes, 1024);
         uint32_t it_a = 0, it_b = 0, it_s = 0, it_u = 0;
         bool o_started = false;   // GEMM2: an MMA has written the current O sub-unit
+        unsigned long long n_g2skip = 0;   // statistics: tiles whose GEMM2 was skipped
         const bool g1 = warp == 1;
         // GEMM2 (warp 10): O += P_hi.B + P_lo.B, P read from TMEM.  The
         // epilogue stored, for each 32-column chunk c of S buffer sb, P_hi
@@ -321,7 +355,7 @@ pairwise_tc_kernel(PairArgs args) {
                     ptx::tc_fence_after();
                     if (ptx::elect_one()) {
                         const uint64_t da0 = descA + ((ab * kTileBytes) >> 4);
-                        const uint64_t db0 = descB + ((st * kTileBytes) >> 4);
+                        const uint64_t db0 = descB + ((st * Cfg::kBStride) >> 4);
                         // K-step order: the half-norm chunk first, then y_hi.y_hi, so the
                         // large terms cancel inside one fused MMA step before the small
                         // hi/lo cross terms are added.
@@ -340,40 +374,51 @@ pairwise_tc_kernel(PairArgs args) {
                     const int rel = ct - ct0;
                     const bool first = (rel & fmask) == 0;
                     const bool last = (rel & fmask) == fmask || ct == ct1 - 1;
-                    const uint32_t ob = it_u & 1;
+                    const uint32_t ob = it_u % Cfg::kOBuf;
                     FKDE_TRACE(2, it_s);
                     ptx::mbar_wait(&p_full[sb], ph);
                     FKDE_TRACE(3, it_s);
                     if (first) {
-                        ptx::mbar_wait(&o_empty[ob], ((it_u >> 1) & 1) ^ 1);
+                        ptx::mbar_wait(&o_empty[ob], ((it_u / Cfg::kOBuf) & 1) ^ 1);
                         o_started = false;
                     }
                     // every lane quadrant's P of this tile is zero: no MMA needed,
                     // unless the sub-unit would otherwise end with O never written
                     const bool all_zero = *reinterpret_cast<volatile uint32_t*>(&skipf[sb]) == 0x01010101u;
-                    const bool issue = !all_zero || (last && !o_started);
+                    const bool issue = !all_zero;
                     ptx::tc_fence_after();
                     if (ptx::elect_one()) {
                         if (issue) {
-                            const uint64_t db0 = descBmn + ((st * kTileBytes) >> 4);
+                            const uint64_t db0 = descBmn + ((st * Cfg::kBStride) >> 4);
                             const uint32_t ta0 = tmem_base + sb * Cfg::kNCol;
-                            const uint32_t to = tmem_base + Cfg::kTmemO + ob * 64;
+                            const uint32_t to = tmem_base + Cfg::kTmemO + ob * Cfg::kOStride;
 #pragma unroll
                             for (int k = 0; k < Cfg::kNCol / 16; ++k) {
 #pragma unroll
-                                for (int part = 0; part < 2; ++part) {
+                                for (int part = 0; part < (FKDE_G2_LO_N > 0 ? 2 : 1); ++part) {
                                     // one N=48 MMA per K step: columns 0-15 T_hi, 16 S, 32-47 T_lo
-                                    ptx::umma_f16_ts(to, ta0 + (k >> 1) * 32 + part * 16 + (k & 1) * 8,
+                                    // (separate: P_lo into O_lo at +48, columns 0-15 T, 16 S)
+                                    const uint32_t dst = (FKDE_LO_SEPARATE && part) ? to + 48 : to;
+                                    const bool zero = FKDE_LO_SEPARATE ? (!o_started && k == 0)
+                                                                       : (!o_started && part == 0 && k == 0);
+                                    ptx::umma_f16_ts(dst, ta0 + (k >> 1) * 32 + part * 16 + (k & 1) * 8,
                                                      db0 + ((k * 2048) >> 4), part ? idesc2_lo : idesc2,
-                                                     (!o_started && part == 0 && k == 0) ? 0u : 1u);
+                                                     zero ? 0u : 1u);
                                 }
                             }
-                        } else if (args.stats) {
-                            atomicAdd(&args.stats[2], 1ull);
+                        } else {
+                            ++n_g2skip;
                         }
                         ptx::umma_commit(&b_empty[st]);
                         ptx::umma_commit(&s_free[sb]);
-                        if (last) ptx::umma_commit(&o_full[ob]);
+                        if (last) {
+                            if (o_started || issue) {
+                                ptx::umma_commit(&o_full[ob]);
+                            } else {   // nothing written to O in this sub-unit
+                                o_zero[ob] = 0x01010101u;
+                                ptx::mbar_arrive(&o_full[ob]);
+                            }
+                        }
                     }
                     __syncwarp();
                     o_started = o_started || issue;
@@ -389,6 +434,7 @@ pairwise_tc_kernel(PairArgs args) {
             }
             ++it_a;
         }
+        if (kScore && !g1 && args.stats && n_g2skip && ptx::elect_one()) atomicAdd(&args.stats[2], n_g2skip);
     }
     } else if (warp < Cfg::kEpi0) {
         if constexpr (kScore) {
@@ -416,23 +462,46 @@ pairwise_tc_kernel(PairArgs args) {
 #pragma unroll 1
                 for (int j = 0; j < nsub; ++j, ++it_u) {
                     const uint32_t g = it_u;
-                    const uint32_t to = lane_addr + Cfg::kTmemO + (g & 1) * 64;
+                    const uint32_t gb = g % Cfg::kOBuf, gph = (g / Cfg::kOBuf) & 1;
+                    const uint32_t to = lane_addr + Cfg::kTmemO + gb * Cfg::kOStride;
                     uint32_t od[16], ol[16], os_;
+#if FKDE_LO_SEPARATE
+                    uint32_t oq[16], oqs;
+#endif
                     FKDE_TRACE(4, g);
-                    ptx::mbar_wait(&o_full[g & 1], (g >> 1) & 1);
+                    ptx::mbar_wait(&o_full[gb], gph);
                     FKDE_TRACE(5, g);
                     ptx::tc_fence_after();
+                    volatile uint8_t* oz = reinterpret_cast<volatile uint8_t*>(&o_zero[gb]) + q;
+                    if (*oz) {   // every tile of this sub-unit was skipped: O = 0
+                        __syncwarp();
+                        if (lane == 0) {
+                            *oz = 0;
+                            ptx::mbar_arrive(&o_empty[gb]);
+                        }
+                        continue;
+                    }
                     ptx::tmem_ld16(to, od);
                     ptx::tmem_ld1(to + 16, os_);
                     ptx::tmem_ld16(to + 32, ol);
+#if FKDE_LO_SEPARATE
+                    ptx::tmem_ld16(to + 48, oq);
+                    ptx::tmem_ld1(to + 64, oqs);
+#endif
                     ptx::tmem_ld_wait();
                     ptx::tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(&o_empty[g & 1]);
+                    if (lane == 0) ptx::mbar_arrive(&o_empty[gb]);
 #pragma unroll
                     for (int c = 0; c <= kMaxDim; ++c) {
+#if FKDE_LO_SEPARATE
+                        const float x = c < kMaxDim ? __uint_as_float(od[c]) + (__uint_as_float(ol[c]) +
+                                                                                __uint_as_float(oq[c]))
+                                                    : __uint_as_float(os_) + __uint_as_float(oqs);
+#else
                         const float x = c < kMaxDim ? __uint_as_float(od[c]) + __uint_as_float(ol[c])
                                                     : __uint_as_float(os_);
+#endif
                         const float s2 = ahi[c] + x;           // 2Sum(ahi, x)
                         const float bb = s2 - ahi[c];
                         const float e = (ahi[c] - (s2 - bb)) + (x - bb);
@@ -466,6 +535,7 @@ pairwise_tc_kernel(PairArgs args) {
         const float dsc = args.sc->dscale;
         const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
         uint32_t it_s = 0;                           // global tile counter (all phases)
+        unsigned long long n_checked = 0, n_skipped = 0;   // tile-skip statistics (lane-uniform)
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
             const int sp = u / args.n_row_tiles, rt = u % args.n_row_tiles;
             const int ct0 = static_cast<int>((long long)sp * args.n_col_tiles / args.splits);
@@ -493,6 +563,10 @@ pairwise_tc_kernel(PairArgs args) {
             const bool has_diag = args.diag_row0 >= 0;
             const int drel_lo = has_diag ? static_cast<int>(fdiv(drow0)) : INT_MAX;
             const int drel_hi = has_diag ? static_cast<int>(fdiv(drow0 + kTileRows - 1)) : -1;
+            // tile skipping (score): this unit's row-tile centroid, one coordinate per
+            // lane (the column tile's centroid arrives with its B stage)
+            float ca_l = 0.f;
+            if (kScore && args.cenA && lane < kMaxDim) ca_l = __ldg(args.cenA + (size_t)rt * kMaxDim + lane);
             for (; rel < len; rel += NP) {
                 FKDE_TRACE(0, it_s + rel);
                 ptx::mbar_wait(&s_full[sb], ph);
@@ -510,29 +584,39 @@ pairwise_tc_kernel(PairArgs args) {
                     // then checked exactly on this quadrant's 32 rows
                     bool skip = false;
                     if (args.cenA) {
-                        const float* ca = args.cenA + (size_t)rt * kMaxDim;
-                        const float* cb = args.cenB + (size_t)(ct0 + rel) * kMaxDim;
-                        float dd = 0.f;
+                        // centroid half-distance^2: lane c < 16 holds coordinate c.  The
+                        // column centroid sits in this tile's B stage (that phase of
+                        // b_full is complete: GEMM1 waited on it, and the stage cannot
+                        // be refilled before this tile's P is consumed)
+                        const uint32_t gt = it_s + static_cast<uint32_t>(rel);
+                        const uint32_t bst = gt % kStages;
+                        ptx::mbar_wait(&b_full[bst], (gt / kStages) & 1);
+                        const float cb = lane < kMaxDim
+                            ? reinterpret_cast<const float*>(smB + bst * Cfg::kBStride + Cfg::kColBytes)[lane]
+                            : 0.f;
+                        const float df = ca_l - cb;
+                        float dd = df * df;
 #pragma unroll
-                        for (int c = 0; c < kMaxDim; ++c) {
-                            const float df = __ldg(ca + c) - __ldg(cb + c);
-                            dd = fmaf(df, df, dd);
-                        }
+                        for (int o = 16; o > 0; o >>= 1) dd += __shfl_xor_sync(0xffffffffu, dd, o);
                         if (0.5f * dd > args.skip_pred) {
-                            float mx = -INFINITY;
+                            float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
 #pragma unroll 1
                             for (int ch = 0; ch < Cfg::kNCol / 32; ++ch) {
                                 uint32_t v[32];
                                 ptx::tmem_ld32(ts + ch * 32, v);
                                 ptx::tmem_ld_wait();
 #pragma unroll
-                                for (int c = 0; c < 32; ++c) mx = fmaxf(mx, __uint_as_float(v[c]));
+                                for (int c = 0; c < 32; c += 4) {
+                                    m0 = fmaxf(m0, __uint_as_float(v[c]));
+                                    m1 = fmaxf(m1, __uint_as_float(v[c + 1]));
+                                    m2 = fmaxf(m2, __uint_as_float(v[c + 2]));
+                                    m3 = fmaxf(m3, __uint_as_float(v[c + 3]));
+                                }
                             }
+                            const float mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
                             skip = __all_sync(0xffffffffu, mx * dsc < kSkipLog2);
-                            if (args.stats && lane == 0) {
-                                atomicAdd(&args.stats[0], 1ull);
-                                if (skip) atomicAdd(&args.stats[1], 1ull);
-                            }
+                            ++n_checked;
+                            n_skipped += skip ? 1u : 0u;
                         }
                     }
                     if (skip) {   // P = 0 for this quadrant (GEMM2 may still read it)
@@ -634,6 +718,10 @@ pairwise_tc_kernel(PairArgs args) {
                     args.part1[idx] = (accl2[0].x + accl2[0].y) + (accl2[1].x + accl2[1].y);
             }
             it_s += len;
+        }
+        if (kScore && args.stats && lane == 0 && n_checked) {
+            atomicAdd(&args.stats[0], n_checked);
+            atomicAdd(&args.stats[1], n_skipped);
         }
     }
 

@@ -30,9 +30,10 @@ def main():
         dS = torch.empty((n, 16), dtype=torch.float64, device="cuda")
         rows = np.linspace(0, n - 1, 1024).astype(int)
         ref = P.score_naive(X, X[rows], h, threads=os.cpu_count())
-        for sp in (2, 1):
+        for sp, fl in ((2, 0), (1, 0), (1, 1)):
             c = fk.Context([0])
             c.set_option(N.OPT_SPATIAL, sp)
+            c.set_option(N.OPT_FLUSH_TILES, fl)
             c.set_option(N.OPT_TIMING, 1)
             stream = torch.cuda.ExternalStream(c.stream())
             ts = []
@@ -45,7 +46,7 @@ def main():
             st = c.skip_stats()
             s = dS.cpu().numpy()[rows]
             prep, score, fin, tot = np.median(np.array(ts[1:]), axis=0)
-            print(f"n={n} spatial={'on' if sp == 1 else 'off'} prep={prep:.3f} score_kernel={score:.3f} "
+            print(f"n={n} spatial={'on' if sp == 1 else 'off'} flush={fl} pred={os.environ.get('FKDE_SKIP_PRED', 'default')} prep={prep:.3f} score_kernel={score:.3f} "
                   f"finalize+={fin:.3f} total={tot:.3f} ms  skip={st}  "
                   f"err global={max_rel_global_floor(s, ref):.2e} rowwise={max_rowwise_rel(s, ref):.2e}",
                   flush=True)
