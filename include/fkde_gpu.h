@@ -78,9 +78,11 @@ enum {
                                  the default (~256 columns)                      */
     FKDE_OPT_TRACE_PTR = 6,   /* debug: device pointer (32*8*256 int64) receiving
                                  clock64 stamps of the score kernel's block 0   */
-    FKDE_OPT_SPATIAL = 7      /* score pass on a spatial (Morton / principal-axis)
+    FKDE_OPT_SPATIAL = 7,     /* score pass on a spatial (Morton / principal-axis)
                                  order of the points with exact-zero tile skipping:
                                  0 = auto (n >= 32768), 1 = always, 2 = never    */
+    FKDE_OPT_PDL = 8          /* 1 (default) = launch the kernel chain with
+                                 programmatic dependent launch; 0 = plain launches */
 };
 enum { FKDE_ENGINE_TC = 0 };
 

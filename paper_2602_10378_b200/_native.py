@@ -30,6 +30,7 @@ METHOD_KDE, METHOD_SDKDE, METHOD_LAPLACE = 0, 1, 2
 
 OPT_ENGINE, OPT_SPLITS, OPT_TIMING, OPT_MAX_CTAS, OPT_FLUSH_TILES = 1, 2, 3, 4, 5
 OPT_SPATIAL = 7
+OPT_PDL = 8
 ENGINE_TC = 0
 
 T_PREP, T_SCORE, T_FINALIZE, T_GATHER, T_QUERY, T_REDUCE, T_TOTAL, T_COUNT = range(8)

@@ -113,6 +113,8 @@ __device__ __forceinline__ void direct_finish_row(const DirectArgs& a, size_t i,
 }
 
 __global__ void __launch_bounds__(kDirRows) direct_rows_kernel(DirectArgs a) {
+    pdl_launch_dependents();
+    pdl_wait();
     __shared__ float4 tile[kDirTileCols][kMaxDim / 4];
     __shared__ int s_last;
     const unsigned int count = *a.count;

@@ -161,9 +161,16 @@ Status ensure(DevBuf& b, size_t bytes) {
     return {};
 }
 
+// FKDE_PDL=0 in the environment switches programmatic dependent launch off by default
+bool g_pdl_default = [] {
+    const char* e = std::getenv("FKDE_PDL");
+    return !(e && *e == '0');
+}();
+
 struct Options {
     int engine = FKDE_ENGINE_TC;
     int spatial = 0;       // FKDE_OPT_SPATIAL: 0 auto (n >= kSpatialMinN), 1 on, 2 off
+    bool pdl = g_pdl_default;   // FKDE_OPT_PDL: programmatic dependent launch of the kernel chain
     int splits = 0;
     int timing = 0;
     int max_ctas = 0;
@@ -183,6 +190,8 @@ struct Device {
     bool attrs_set = false;
     DevBuf X, Y, opA, opB, part0, part1, xsd, out, aux0, aux1, colpart, scal, err, flags;
     DevBuf risk, dpart, ddone;   // direct_rows_kernel: spread flags, partials, counters
+    DevBuf pdone;                // prep_stats / scale_two completion counters (self-resetting)
+    DevBuf qmax;                 // scale_two per-block maxima
     // spatial order of the score pass (spatial_order.cuh): sorted points, permutation,
     // keys, CUB scratch, axes, tile centroids, skip statistics, un-permuted outputs
     DevBuf Xs, perm, keys, cubtmp, ordsc, cenA, cenB, skipstats, unperm0, unperm1;
@@ -269,6 +278,30 @@ int choose_splits(const Options& o, size_t row_tiles, size_t col_tiles, int ctas
     return best_s;
 }
 
+inline unsigned grid1(size_t n, unsigned bs) { return static_cast<unsigned>((n + bs - 1) / bs); }
+
+// Kernel-chain launch with programmatic dependent launch (layout.cuh: every chain
+// kernel waits on griddepcontrol before touching global memory), so each kernel's
+// launch and prologue (block scheduling, barrier init, TMEM allocation) overlap
+// the tail of its predecessor.  FKDE_OPT_PDL = 0 launches them plainly.
+
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_chain(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                         cudaStream_t stream, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 template <int MODE>
 Status launch_pairwise(Device& D, const Options& o, const PairArgs& a, size_t n_cols) {
     {
@@ -283,39 +316,71 @@ Status launch_pairwise(Device& D, const Options& o, const PairArgs& a, size_t n_
         const int units = a.n_row_tiles * a.splits;
         int grid = std::min(units, D.num_sms);
         if (o.max_ctas > 0) grid = std::min(grid, o.max_ctas);
-        pairwise_tc_kernel<MODE><<<grid, Cfg::kThreads, Cfg::kSmemBytes, D.stream>>>(a);
+        CUDA_TRY(launch_chain(o.pdl, pairwise_tc_kernel<MODE>, dim3(grid), dim3(Cfg::kThreads),
+                              Cfg::kSmemBytes, D.stream, a));
     }
     ++D.launches;
     CUDA_TRY(cudaGetLastError());
     return {};
 }
 
-inline unsigned grid1(size_t n, unsigned bs) { return static_cast<unsigned>((n + bs - 1) / bs); }
+
 
 void record(Device& D, const Options& o, int idx) {
     if (o.timing) cudaEventRecord(D.ev[idx], D.stream);
 }
 
 // ---- building blocks ------------------------------------------------------------
-// mean of X (n x d) into sc->mu; also zero-initialises sc.
-Status compute_mean(Device& D, const double* dX, size_t n, int d, PassScalars* sc) {
-    CUDA_TRY(cudaMemsetAsync(sc, 0, sizeof(PassScalars), D.stream));
+// Per-call device scratch that the fused prologue kernels clear: flag lists (sized
+// for either pass), the underflow row, the skip statistics and the completion
+// counters.  Allocated before any kernel of the call is enqueued, so no buffer
+// moves between the kernel that clears it and the ones that use it.
+Status ensure_call_scratch(Device& D, size_t flag_rows) {
+    STATUS_TRY(ensure(D.flags, (flag_rows + 1) * sizeof(unsigned int)));
+    STATUS_TRY(ensure(D.err, sizeof(unsigned long long)));
+    STATUS_TRY(ensure(D.skipstats, 4 * sizeof(unsigned long long)));
+    if (!D.pdone.p) {   // counters start at zero and reset themselves
+        STATUS_TRY(ensure(D.pdone, 4 * sizeof(unsigned int)));
+        CUDA_TRY(cudaMemsetAsync(D.pdone.p, 0, D.pdone.bytes, D.stream));
+    }
+    return {};
+}
+
+// mean (+ the operand scale for scale factor k, 0 = none) of X into sc, and the
+// per-call counters cleared -- one launch (prep_stats)
+Status prep(Device& D, bool pdl, const double* dX, size_t n, int d, double k, PassScalars* sc,
+            bool score) {
     const int nparts = static_cast<int>(std::min<size_t>(256, std::max<size_t>(1, n / 64)));
-    STATUS_TRY(ensure(D.colpart, nparts * 16 * sizeof(double)));
-    colsum_stage1<<<nparts, 256, 0, D.stream>>>(dX, n, d, D.colpart.as<double>(), sc);
-    colsum_stage2<<<1, 16, 0, D.stream>>>(D.colpart.as<double>(), nparts, n, d, sc);
-    D.launches += 2;
+    STATUS_TRY(ensure(D.colpart, static_cast<size_t>(nparts) * 48 * sizeof(double)));
+    PrepArgs a{};
+    a.x = dX;
+    a.n = n;
+    a.d = d;
+    a.k = k;
+    a.sc = sc;
+    a.part = D.colpart.as<double>();
+    a.done = D.pdone.as<unsigned int>();
+    a.clear_u32[0] = D.flags.as<unsigned int>();
+    if (score) {
+        a.clear_max = D.err.as<unsigned long long>();
+        a.clear_stats = D.skipstats.as<unsigned long long>();
+    }
+    CUDA_TRY(launch_chain(pdl, prep_stats, dim3(nparts), dim3(256), 0, D.stream, a));
+    ++D.launches;
     CUDA_TRY(cudaGetLastError());
     return {};
 }
 
-Status pack(Device& D, const double* x, size_t rows, int d, int format, bool center, double k,
-            const PassScalars* sc, DevBuf& out, size_t* rows_padded, size_t align = kTileRows,
-            float a_offset = 0.f) {
+// operand packing arguments (pack_two packs the row and column operands of a pass
+// in one launch)
+Status pack_args(Device& D, const double* x, size_t rows, int d, int format, bool center, double k,
+                 const PassScalars* sc, DevBuf& out, size_t* rows_padded, PackArgs* pa,
+                 size_t align = kTileRows, float a_offset = 0.f) {
     const size_t rp = round_up(std::max<size_t>(rows, 1), align);
     STATUS_TRY(ensure(out, rp * kRowBytes));
     if (format == 0) STATUS_TRY(ensure(D.risk, rp));
-    PackArgs a;
+    PackArgs& a = *pa;
+    a = PackArgs{};
     a.x = x;
     a.rows = rows;
     a.rows_padded = rp;
@@ -328,10 +393,15 @@ Status pack(Device& D, const double* x, size_t rows, int d, int format, bool cen
     a.a_offset = a_offset;
     a.risk = format == 0 ? D.risk.as<uint8_t>() : nullptr;   // row side: spread flags
     a.risk_half_norm = kRiskHalfNorm;
-    pack_operands<<<grid1(rp, 128), 128, 0, D.stream>>>(a);
+    *rows_padded = rp;
+    return {};
+}
+
+Status pack2(Device& D, bool pdl, const PackArgs& a, const PackArgs& b) {
+    const unsigned ba = grid1(a.rows_padded, 128), bb = grid1(b.rows_padded, 128);
+    CUDA_TRY(launch_chain(pdl, pack_two, dim3(ba + bb), dim3(128), 0, D.stream, a, b, ba));
     ++D.launches;
     CUDA_TRY(cudaGetLastError());
-    *rows_padded = rp;
     return {};
 }
 
@@ -367,16 +437,12 @@ Status density_pass(Device& D, const Options& o, int mode, size_t rows_pad, size
     return {};
 }
 
-// flag list for direct_rows_kernel: [0] = count, [1..] = local row indices
-Status prepare_flags(Device& D, size_t rows) {
-    STATUS_TRY(ensure(D.flags, (rows + 1) * sizeof(unsigned int)));
-    CUDA_TRY(cudaMemsetAsync(D.flags.p, 0, sizeof(unsigned int), D.stream));
-    return {};
-}
+// flag list for direct_rows_kernel: D.flags = [0] count, [1..] local row indices
+// (sized by ensure_call_scratch, the count cleared by prep_stats / scale_two)
 
 // Recompute the flagged rows by direct differences (direct_rows.cuh).  The
 // flagged count lives on the device; the launch exits at once when it is 0.
-Status launch_direct(Device& D, DirectArgs& e, size_t rows) {
+Status launch_direct(Device& D, bool pdl, DirectArgs& e, size_t rows) {
     // partials: at most (row blocks x splits) < 2 * kDirTargetItems items of 128 rows
     STATUS_TRY(ensure(D.dpart, static_cast<size_t>(2 * kDirTargetItems) * kDirRows * kDirPart *
                                    sizeof(double)));
@@ -387,7 +453,7 @@ Status launch_direct(Device& D, DirectArgs& e, size_t rows) {
     }
     e.part = D.dpart.as<double>();
     e.done = D.ddone.as<unsigned int>();
-    direct_rows_kernel<<<kDirTargetItems, kDirRows, 0, D.stream>>>(e);
+    CUDA_TRY(launch_chain(pdl, direct_rows_kernel, dim3(kDirTargetItems), dim3(kDirRows), 0, D.stream, e));
     ++D.launches;
     CUDA_TRY(cudaGetLastError());
     return {};
@@ -471,26 +537,26 @@ Status score_program(Device& D, const Options& o, const Job& J, const double* dX
     const int d = J.d;
     const size_t n = J.n;
     const double ks = std::sqrt(kLog2e) / J.h_score;
-    STATUS_TRY(compute_mean(D, dX, n, d, sc));
+    // mean + operand scale (bounding-box bound) + per-call counters: one launch
+    STATUS_TRY(prep(D, o.pdl, dX, n, d, ks, sc, true));
     D.ordered = use_spatial(o, n);
     if (D.ordered) {
         STATUS_TRY(spatial_order(D, dX, n, d, sc));
         dX = D.Xs.as<double>();
     }
-    max_half_norm<<<grid1(n, 256), 256, 0, D.stream>>>(dX, n, d, ks, sc, sc);
-    set_scale_exponent<<<1, 1, 0, D.stream>>>(sc);
-    D.launches += 2;
     // row shards start on a tile boundary so the diagonal is tile aligned
     const Shard sh = shard_of(n, D.world, D.rank, kTileRows);
     size_t rows_pad = 0, cols_pad = 0;
+    PackArgs pa, pb;
     // A rows carry the P' = phi * 2^15 offset (layout.cuh): S = log2 P' off the tensor core
-    STATUS_TRY(pack(D, dX + sh.begin * d, sh.rows, d, 0, true, ks, sc, D.opA, &rows_pad, kTileRows,
-                    kPScaleF));
+    STATUS_TRY(pack_args(D, dX + sh.begin * d, sh.rows, d, 0, true, ks, sc, D.opA, &rows_pad, &pa,
+                         kTileRows, kPScaleF));
     // score-pass column tiles are TcConfig<kModeScore>::kNCol points wide: pad the
     // column operand to a whole number of those and of 128-point pack tiles
     constexpr size_t kScoreNCol = TcConfig<kModeScore>::kNCol;
     const size_t col_align = std::lcm<size_t>(kScoreNCol, kTileRows);
-    STATUS_TRY(pack(D, dX, n, d, 1, true, ks, sc, D.opB, &cols_pad, col_align));
+    STATUS_TRY(pack_args(D, dX, n, d, 1, true, ks, sc, D.opB, &cols_pad, &pb, col_align));
+    STATUS_TRY(pack2(D, o.pdl, pa, pb));
     record(D, o, FKDE_T_SCORE);
 
     const size_t rt = rows_pad / kTileRows;
@@ -518,9 +584,7 @@ Status score_program(Device& D, const Options& o, const Job& J, const double* dX
     a.rows_pad = rows_pad;
     a.diag_row0 = static_cast<long long>(sh.begin);
     a.trace = o.trace;
-    STATUS_TRY(ensure(D.skipstats, 4 * sizeof(unsigned long long)));
-    CUDA_TRY(cudaMemsetAsync(D.skipstats.p, 0, 4 * sizeof(unsigned long long), D.stream));
-    a.stats = D.skipstats.as<unsigned long long>();
+    a.stats = D.skipstats.as<unsigned long long>();   // (cleared by prep_stats)
     if (D.ordered) {
         STATUS_TRY(ensure(D.cenA, rt * kMaxDim * sizeof(float)));
         STATUS_TRY(ensure(D.cenB, ct * kMaxDim * sizeof(float)));
@@ -554,9 +618,7 @@ Status score_program(Device& D, const Options& o, const Job& J, const double* dX
     f.k = ks;
     f.h_score = J.h_score;
     f.shift = 0.5 * J.h * J.h;
-    STATUS_TRY(ensure(D.err, sizeof(unsigned long long)));
-    CUDA_TRY(cudaMemsetAsync(D.err.p, 0xFF, sizeof(unsigned long long), D.stream));
-    f.underflow_row = D.err.as<unsigned long long>();
+    f.underflow_row = D.err.as<unsigned long long>();   // (set to ~0 by prep_stats)
     if (J.kind == Job::kScore) {
         STATUS_TRY(ensure(D.aux0, nrows_g * d * sizeof(double)));
         f.score = D.aux0.as<double>();
@@ -570,11 +632,11 @@ Status score_program(Device& D, const Options& o, const Job& J, const double* dX
         STATUS_TRY(ensure(D.xsd, nrows_g * d * sizeof(double)));
         f.xsd_c = D.xsd.as<double>();
     }
-    STATUS_TRY(prepare_flags(D, sh.rows));
     f.flag_count = D.flags.as<unsigned int>();
     f.flag_rows = f.flag_count + 1;
     f.risk = D.risk.as<uint8_t>();
-    finalize_score<<<grid1(std::max<size_t>(sh.rows, 1) * d, 256), 256, 0, D.stream>>>(f);
+    CUDA_TRY(launch_chain(o.pdl, finalize_score, dim3(grid1(std::max<size_t>(sh.rows, 1) * d, 256)),
+                          dim3(256), 0, D.stream, f));
     ++D.launches;
     CUDA_TRY(cudaGetLastError());
     {
@@ -596,7 +658,7 @@ Status score_program(Device& D, const Options& o, const Job& J, const double* dX
         e.xsd_c = f.xsd_c;
         e.phi_sum = f.phi_sum;
         e.weighted = f.weighted;
-        STATUS_TRY(launch_direct(D, e, sh.rows));
+        STATUS_TRY(launch_direct(D, o.pdl, e, sh.rows));
     }
     record(D, o, FKDE_T_GATHER);
     if (J.kind == Job::kScore) STATUS_TRY(allgather(D, D.aux0.p, sh.chunk * d, ncclFloat64));
@@ -629,21 +691,39 @@ Status score_program(Device& D, const Options& o, const Job& J, const double* dX
 // Density of the rank's query shard against `dCols` (n x d; centred iff
 // !center_cols), gathered into D.out (m doubles, gather layout).
 Status query_program(Device& D, const Options& o, const Job& J, const double* dCols,
-                     bool cols_centred, const double* dQ, PassScalars* sc_q, int kernel,
-                     int fused) {
+                     bool cols_centred, const double* dQ, const PassScalars* mu_src,
+                     PassScalars* sc_q, int kernel, int fused) {
     const int d = J.d;
     const size_t n = J.n, m = J.m;
     const double kh = std::sqrt(kLog2e) / J.h;
-    // scale exponent over both point sets (identical on every rank)
-    max_half_norm<<<grid1(n, 256), 256, 0, D.stream>>>(dCols, n, d, kh,
-                                                       cols_centred ? nullptr : sc_q, sc_q);
-    max_half_norm<<<grid1(m, 256), 256, 0, D.stream>>>(dQ, m, d, kh, sc_q, sc_q);
-    set_scale_exponent<<<1, 1, 0, D.stream>>>(sc_q);
-    D.launches += 3;
+    // scale exponent over both point sets (identical on every rank), the mean copied
+    // from mu_src, the density flag counter cleared: one launch (scale_two)
+    {
+        const unsigned g = grid1(n + m, 256);
+        STATUS_TRY(ensure(D.qmax, g * sizeof(unsigned int)));
+        ScaleArgs s2{};
+        s2.cols = dCols;
+        s2.n = n;
+        s2.cols_centred = cols_centred ? 1 : 0;
+        s2.rows = dQ;
+        s2.m = m;
+        s2.d = d;
+        s2.k = kh;
+        s2.mu_src = mu_src;
+        s2.sc = sc_q;
+        s2.block_max = D.qmax.as<unsigned int>();
+        s2.done = D.pdone.as<unsigned int>() + 1;
+        s2.clear_u32 = D.flags.as<unsigned int>();
+        CUDA_TRY(launch_chain(o.pdl, scale_two, dim3(g), dim3(256), 0, D.stream, s2));
+        ++D.launches;
+        CUDA_TRY(cudaGetLastError());
+    }
     const Shard sh = shard_of(m, D.world, D.rank);
     size_t rows_pad = 0, cols_pad = 0;
-    STATUS_TRY(pack(D, dCols, n, d, 1, !cols_centred, kh, sc_q, D.opB, &cols_pad));
-    STATUS_TRY(pack(D, dQ + sh.begin * d, sh.rows, d, 0, true, kh, sc_q, D.opA, &rows_pad));
+    PackArgs pa, pb;
+    STATUS_TRY(pack_args(D, dQ + sh.begin * d, sh.rows, d, 0, true, kh, sc_q, D.opA, &rows_pad, &pa));
+    STATUS_TRY(pack_args(D, dCols, n, d, 1, !cols_centred, kh, sc_q, D.opB, &cols_pad, &pb));
+    STATUS_TRY(pack2(D, o.pdl, pa, pb));
     record(D, o, FKDE_T_QUERY);
 
     const double norm = std::pow(2.0 * M_PI, -0.5 * d) * std::pow(J.h, -static_cast<double>(d)) /
@@ -655,7 +735,6 @@ Status query_program(Device& D, const Options& o, const Job& J, const double* dC
     r.rows = sh.rows;
     r.scale = norm;
     r.out = outp;
-    STATUS_TRY(prepare_flags(D, sh.rows));
     unsigned int* flag_count = D.flags.as<unsigned int>();
     int nparts = 0;
     if (kernel == FKDE_KERNEL_GAUSSIAN) {
@@ -669,7 +748,7 @@ Status query_program(Device& D, const Options& o, const Job& J, const double* dC
         r.flag_count = flag_count;
         r.flag_rows = flag_count + 1;
         r.risk = D.risk.as<uint8_t>();
-        if (sh.rows) reduce_density<<<grid1(sh.rows, 256), 256, 0, D.stream>>>(r);
+        if (sh.rows) CUDA_TRY(launch_chain(o.pdl, reduce_density, dim3(grid1(sh.rows, 256)), dim3(256), 0, D.stream, r));
         ++D.launches;
     } else if (fused) {
         // LaplaceFused: phi (1 + d/2 - u) = (1 + d/2) phi + ln2 * phi * log2(phi)
@@ -684,7 +763,7 @@ Status query_program(Device& D, const Options& o, const Job& J, const double* dC
         r.flag_count = flag_count;
         r.flag_rows = flag_count + 1;
         r.risk = D.risk.as<uint8_t>();
-        if (sh.rows) reduce_density<<<grid1(sh.rows, 256), 256, 0, D.stream>>>(r);
+        if (sh.rows) CUDA_TRY(launch_chain(o.pdl, reduce_density, dim3(grid1(sh.rows, 256)), dim3(256), 0, D.stream, r));
         ++D.launches;
     } else {
         // engine.cpp:372-379: Gaussian pass, then the correction pass
@@ -695,7 +774,7 @@ Status query_program(Device& D, const Options& o, const Job& J, const double* dC
         r.ca = 1.0;
         r.cb = 0.0;
         r.accumulate = 0;
-        if (sh.rows) reduce_density<<<grid1(sh.rows, 256), 256, 0, D.stream>>>(r);
+        if (sh.rows) CUDA_TRY(launch_chain(o.pdl, reduce_density, dim3(grid1(sh.rows, 256)), dim3(256), 0, D.stream, r));
         ++D.launches;
         STATUS_TRY(density_pass(D, o, kModeLaplace, rows_pad, n, sc_q, &nparts));
         record(D, o, FKDE_T_REDUCE);
@@ -708,7 +787,7 @@ Status query_program(Device& D, const Options& o, const Job& J, const double* dC
         r.flag_count = flag_count;
         r.flag_rows = flag_count + 1;
         r.risk = D.risk.as<uint8_t>();
-        if (sh.rows) reduce_density<<<grid1(sh.rows, 256), 256, 0, D.stream>>>(r);
+        if (sh.rows) CUDA_TRY(launch_chain(o.pdl, reduce_density, dim3(grid1(sh.rows, 256)), dim3(256), 0, D.stream, r));
         ++D.launches;
     }
     CUDA_TRY(cudaGetLastError());
@@ -728,7 +807,7 @@ Status query_program(Device& D, const Options& o, const Job& J, const double* dC
         e.h = J.h;
         e.norm = norm;
         e.out = outp;
-        STATUS_TRY(launch_direct(D, e, sh.rows));
+        STATUS_TRY(launch_direct(D, o.pdl, e, sh.rows));
     }
     STATUS_TRY(allgather(D, D.out.p, sh.chunk, ncclFloat64));
     return {};
@@ -780,6 +859,8 @@ Status run_job(Device& D, const Options& o, const Job& J) {
     CUDA_TRY(cudaMemsetAsync(D.scal.p, 0, 2 * sizeof(PassScalars), D.stream));
     PassScalars* sc_s = D.scal.as<PassScalars>();
     PassScalars* sc_q = sc_s + 1;
+    STATUS_TRY(ensure_call_scratch(
+        D, std::max(shard_of(J.n, D.world, D.rank, kTileRows).rows, shard_of(J.m, D.world, D.rank).rows)));
 
     switch (J.kind) {
         case Job::kScore:
@@ -808,20 +889,18 @@ Status run_job(Device& D, const Options& o, const Job& J) {
                                          cudaMemcpyDeviceToHost, D.side));
                 CUDA_TRY(cudaEventRecord(D.ev_side_out, D.side));
             }
-            // sc_q: same centring mean, fresh scale (x_sd is already centred)
-            CUDA_TRY(cudaMemcpyAsync(sc_q, sc_s, sizeof(PassScalars), cudaMemcpyDeviceToDevice,
-                                     D.stream));
-            CUDA_TRY(cudaMemsetAsync(&sc_q->max_half_norm_bits, 0, sizeof(unsigned int), D.stream));
-            STATUS_TRY(query_program(D, o, J, D.xsd.as<double>(), true, dY, sc_q,
+            // sc_q: same centring mean (copied from sc_s by scale_two), fresh scale
+            // (x_sd is already centred)
+            STATUS_TRY(query_program(D, o, J, D.xsd.as<double>(), true, dY, sc_s, sc_q,
                                      FKDE_KERNEL_GAUSSIAN, 1));
             break;
         }
         case Job::kKde: {
-            STATUS_TRY(compute_mean(D, dX, J.n, d, sc_q));
+            STATUS_TRY(prep(D, o.pdl, dX, J.n, d, 0.0, sc_q, false));   // the mean only
             record(D, o, FKDE_T_SCORE);
             record(D, o, FKDE_T_FINALIZE);
             record(D, o, FKDE_T_GATHER);
-            STATUS_TRY(query_program(D, o, J, dX, false, dY, sc_q, J.kernel, J.fused));
+            STATUS_TRY(query_program(D, o, J, dX, false, dY, sc_q, sc_q, J.kernel, J.fused));
             break;
         }
         default:
@@ -1062,7 +1141,7 @@ void fkde_gpu_destroy(fkde_gpu_ctx* ctx) {
                           &D.xsd,  &D.out,   &D.aux0, &D.aux1, &D.colpart, &D.scal,
                           &D.err,  &D.flags, &D.risk, &D.dpart, &D.ddone,
                           &D.Xs,   &D.perm,  &D.keys, &D.cubtmp, &D.ordsc, &D.cenA,
-                          &D.cenB, &D.skipstats, &D.unperm0, &D.unperm1};
+                          &D.cenB, &D.skipstats, &D.unperm0, &D.unperm1, &D.pdone, &D.qmax};
         for (DevBuf* b : bufs)
             if (b->p) cudaFree(b->p);
         for (auto& e : D.ev)
@@ -1108,6 +1187,9 @@ int fkde_gpu_set_option(fkde_gpu_ctx* ctx, int key, int64_t value) {
             return FKDE_OK;
         case FKDE_OPT_TRACE_PTR:
             ctx->opt.trace = reinterpret_cast<long long*>(value);
+            return FKDE_OK;
+        case FKDE_OPT_PDL:
+            ctx->opt.pdl = value != 0;
             return FKDE_OK;
         case FKDE_OPT_SPATIAL:
             if (value < 0 || value > 2) return FKDE_INVALID_ARGUMENT;
@@ -1161,7 +1243,7 @@ int fkde_gpu_workspace_bytes(const fkde_gpu_ctx* ctx, size_t* bytes) {
                                 &D.xsd,  &D.out,   &D.aux0, &D.aux1, &D.colpart, &D.scal,
                                 &D.err,  &D.flags, &D.risk, &D.dpart, &D.ddone,
                                 &D.Xs,   &D.perm,  &D.keys, &D.cubtmp, &D.ordsc, &D.cenA,
-                                &D.cenB, &D.skipstats, &D.unperm0, &D.unperm1};
+                                &D.cenB, &D.skipstats, &D.unperm0, &D.unperm1, &D.pdone, &D.qmax};
         for (const DevBuf* b : bufs) total += b->bytes;
     }
     *bytes = total;
@@ -1353,7 +1435,7 @@ Status run_device_job(fkde_gpu_ctx* ctx, const Job& J) {
     std::snprintf(buf, sizeof(buf), "%d|%p|%p|%p|%zu|%zu|%d|%a|%a|%d|%d|%d|%d|%d|%d|%d|%d", J.kind,
                   (const void*)J.dX, (const void*)J.dY, (void*)J.d_out, J.n, J.m, J.d, J.h,
                   J.h_score, J.kernel, J.fused, o.engine, o.splits, o.timing, o.max_ctas,
-                  o.flush_tiles, o.spatial);
+                  o.flush_tiles, o.spatial * 2 + (o.pdl ? 1 : 0));
     const std::string key(buf);
     CUDA_TRY(cudaSetDevice(D.dev));
     if (D.graph && key == D.graph_key && D.graph_epoch == g_alloc_epoch.load()) {

@@ -69,4 +69,14 @@ struct PassScalars {
 
 __host__ __device__ inline size_t round_up(size_t x, size_t m) { return (x + m - 1) / m * m; }
 
+// Programmatic dependent launch (the engine launches its kernel chain with
+// cudaLaunchAttributeProgrammaticStreamSerialization): a kernel may be scheduled
+// while its predecessor is still running, so every chain kernel first lets its own
+// successor launch, then waits for its predecessor's completion (and memory) before
+// touching any global data.  Both are no-ops without a programmatic dependency.
+__device__ __forceinline__ void pdl_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 }  // namespace fkde_b200

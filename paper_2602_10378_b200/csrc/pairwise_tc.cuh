@@ -248,11 +248,14 @@ pairwise_tc_kernel(PairArgs args) {
 
         ptx::fence_barrier_init();
     }
+    pdl_launch_dependents();
     if (warp == 1) ptx::tmem_alloc<Cfg::kTmemCols>(tmem_slot);
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // (barriers and TMEM are set up while the previous kernel of the chain drains)
+    pdl_wait();
 
     const int n_units = args.n_row_tiles * args.splits;
 

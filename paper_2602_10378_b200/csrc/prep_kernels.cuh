@@ -13,73 +13,168 @@ namespace fkde_b200 {
 constexpr double kLog2e = 1.4426950408889634073599246810019;
 constexpr double kLn2 = 0.69314718055994530941723212145818;
 
-// ---- deterministic column sums: stage 1 (per-block partials) -----------------
-// Thread t sums column (t % 16) over rows start + (t/16), +16, ...; the 16
-// row-phases are then added in a fixed order.  Same inputs -> same bits on
-// every rank and every run.
-// Also flags non-finite entries (SampleSet::validate, types.cpp:21-33).
-__global__ void colsum_stage1(const double* __restrict__ x, size_t n, int d,
-                              double* __restrict__ part /* [gridDim.x][16] */,
-                              PassScalars* flag) {
-    __shared__ double sm[16][17];
+// ---- fused pass prologue -------------------------------------------------------------------
+// One launch instead of colsum_stage1 + colsum_stage2 + max_half_norm + set_scale_exponent
+// (+ memsets): per-block column sums (same partition and summation order as
+// colsum_stage1, so the mean is deterministic) and per-column min / max; the last
+// block to finish (threadfence + counter) reduces the partials in block order into
+// mu, bounds max_i |(x_i - mu) k|^2 / 2 by the bounding box (>= the exact maximum,
+// so the fp16 operand range stays safe; the scale is a power of two, so a larger
+// one costs no precision), sets e / dscale, and clears the per-call counters.
+struct PrepArgs {
+    const double* x;
+    size_t n;
+    int d;
+    double k;                       // sqrt(log2 e) / h of the pass that packs x (0: no scale)
+    PassScalars* sc;                // out: mu, e, dscale, nonfinite (zeroed here first)
+    double* part;                   // [grid][3][16] sums, min, max
+    unsigned int* done;             // self-resetting completion counter
+    unsigned int* clear_u32[4];     // per-call counters to zero (nullptr: unused)
+    unsigned long long* clear_max;  // set to ~0 (underflow row), nullptr: unused
+    unsigned long long* clear_stats;   // 4 x 0, nullptr: unused
+};
+
+__global__ void __launch_bounds__(256) prep_stats(PrepArgs a) {
+    pdl_launch_dependents();
+    pdl_wait();
+    __shared__ double sm[16][17], mn[16][17], mx[16][17];
+    __shared__ int s_last;
     const int c = threadIdx.x & 15, g = threadIdx.x >> 4;
-    const size_t b0 = n * blockIdx.x / gridDim.x, b1 = n * (blockIdx.x + 1) / gridDim.x;
-    double acc = 0.0;
+    const size_t b0 = a.n * blockIdx.x / gridDim.x, b1 = a.n * (blockIdx.x + 1) / gridDim.x;
+    double acc = 0.0, lo = INFINITY, hi = -INFINITY;
     bool bad = false;
-    if (c < d)
+    if (c < a.d)
         for (size_t r = b0 + g; r < b1; r += 16) {
-            const double v = x[r * d + c];
+            const double v = a.x[r * a.d + c];
             bad |= !isfinite(v);
             acc += v;
+            lo = fmin(lo, v);
+            hi = fmax(hi, v);
         }
-    if (bad) flag->nonfinite = 1u;
     sm[g][c] = acc;
+    mn[g][c] = lo;
+    mx[g][c] = hi;
     __syncthreads();
+    double* p = a.part + static_cast<size_t>(blockIdx.x) * 48;
     if (threadIdx.x < 16) {
-        double s = 0.0;
-        for (int k = 0; k < 16; ++k) s += sm[k][threadIdx.x];
-        part[blockIdx.x * 16 + threadIdx.x] = s;
+        double s = 0.0, l = INFINITY, h = -INFINITY;
+        for (int k = 0; k < 16; ++k) {
+            s += sm[k][threadIdx.x];
+            l = fmin(l, mn[k][threadIdx.x]);
+            h = fmax(h, mx[k][threadIdx.x]);
+        }
+        p[threadIdx.x] = s;
+        p[16 + threadIdx.x] = l;
+        p[32 + threadIdx.x] = h;
+    }
+    const int any_bad = __syncthreads_or(bad ? 1 : 0);
+    if (threadIdx.x == 0) {
+        if (any_bad) atomicOr(&a.sc->nonfinite, 1u);
+        __threadfence();
+        s_last = atomicAdd(a.done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    __shared__ double bound[16];
+    if (threadIdx.x < 16) {
+        const int cc = threadIdx.x;
+        double s = 0.0, l = INFINITY, h = -INFINITY;
+        for (unsigned b = 0; b < gridDim.x; ++b) {   // block order: deterministic
+            const double* q = a.part + static_cast<size_t>(b) * 48;
+            s += __ldcg(q + cc);
+            l = fmin(l, __ldcg(q + 16 + cc));
+            h = fmax(h, __ldcg(q + 32 + cc));
+        }
+        const double mu = (cc < a.d) ? s / static_cast<double>(a.n) : 0.0;
+        a.sc->mu[cc] = mu;
+        const double ext = cc < a.d ? fmax(h - mu, mu - l) : 0.0;
+        bound[cc] = ext * ext;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double b = 0.0;
+        for (int cc = 0; cc < 16; ++cc) b += bound[cc];
+        const double hn = 0.5 * b * a.k * a.k * 1.0000001;
+        float hf = !(hn == hn) || hn > 3.0e38 ? 3.0e38f : static_cast<float>(hn);
+        a.sc->max_half_norm_bits = __float_as_uint(hf);
+        int e = 0;
+        while (e < 60 && ldexpf(hf, -2 * e) > 8192.0f) ++e;
+        a.sc->e = e;
+        a.sc->dscale = ldexpf(1.0f, 2 * e);
+        for (int i = 0; i < 4; ++i)
+            if (a.clear_u32[i]) *a.clear_u32[i] = 0u;
+        if (a.clear_max) *a.clear_max = ~0ull;
+        if (a.clear_stats)
+            for (int i = 0; i < 4; ++i) a.clear_stats[i] = 0ull;
+        *a.done = 0u;   // ready for the next call
     }
 }
 
-// stage 2: one block of 16 threads -> mean into PassScalars.mu
-__global__ void colsum_stage2(const double* __restrict__ part, int nparts, size_t n, int d,
-                              PassScalars* sc) {
-    const int c = threadIdx.x;
-    if (c >= kMaxDim) return;
-    double s = 0.0;
-    for (int b = 0; b < nparts; ++b) s += part[b * 16 + c];
-    sc->mu[c] = (c < d) ? s / static_cast<double>(n) : 0.0;
-}
+// Density-pass scale over both point sets (columns: centred or not; queries:
+// centred by mu) in one launch, last-block reduction of the exact maxima
+// (replaces max_half_norm x 2 + set_scale_exponent + the PassScalars copy).
+struct ScaleArgs {
+    const double* cols;
+    size_t n;
+    int cols_centred;
+    const double* rows;
+    size_t m;
+    int d;
+    double k;
+    const PassScalars* mu_src;   // mean (both sets are centred by it)
+    PassScalars* sc;             // out: mu (copied), e, dscale, max_half_norm_bits, nonfinite
+    unsigned int* block_max;     // [grid] float bits
+    unsigned int* done;
+    unsigned int* clear_u32;     // flag counter of the density pass (nullptr: unused)
+};
 
-// ---- operand scale: max_i |(x_i - mu) k|^2 / 2 ------------------------------------
-// center: subtract sc_mu->mu (nullptr -> points already centred)
-__global__ void max_half_norm(const double* __restrict__ x, size_t rows, int d, double k,
-                              const PassScalars* __restrict__ sc_mu, PassScalars* sc_out) {
+__global__ void __launch_bounds__(256) scale_two(ScaleArgs a) {
+    pdl_launch_dependents();
+    pdl_wait();
+    __shared__ float wmax[8];
+    __shared__ int s_last;
     const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
     float hn = 0.f;
-    if (i < rows) {
+    bool bad = false;
+    if (i < a.n + a.m) {
+        const bool is_col = i < a.n;
+        const double* x = is_col ? a.cols + i * a.d : a.rows + (i - a.n) * a.d;
+        const bool center = !is_col || !a.cols_centred;
         double s = 0.0;
-        for (int c = 0; c < d; ++c) {
-            const double raw = x[i * d + c];
-            if (!isfinite(raw)) sc_out->nonfinite = 1u;
-            const double v = (raw - (sc_mu ? sc_mu->mu[c] : 0.0)) * k;
+        for (int c = 0; c < a.d; ++c) {
+            const double raw = x[c];
+            bad |= !isfinite(raw);
+            const double v = (raw - (center ? a.mu_src->mu[c] : 0.0)) * a.k;
             s += v * v;
         }
         hn = static_cast<float>(0.5 * s);
-        if (!(hn == hn) || hn > 3.0e38f) hn = 3.0e38f;  // NaN/overflow -> saturate
+        if (!(hn == hn) || hn > 3.0e38f) hn = 3.0e38f;
     }
     for (int o = 16; o > 0; o >>= 1) hn = fmaxf(hn, __shfl_xor_sync(0xffffffffu, hn, o));
-    if ((threadIdx.x & 31) == 0) atomicMax(&sc_out->max_half_norm_bits, __float_as_uint(hn));
-}
-
-// e = smallest exponent with max|y|^2/2 * 2^-2e <= 2^13 (fp16-safe operands)
-__global__ void set_scale_exponent(PassScalars* sc) {
-    const float hn = __uint_as_float(sc->max_half_norm_bits);
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = hn;
+    const int any_bad = __syncthreads_or(bad ? 1 : 0);
+    if (threadIdx.x == 0) {
+        float m = 0.f;
+        for (int w = 0; w < 8; ++w) m = fmaxf(m, wmax[w]);
+        a.block_max[blockIdx.x] = __float_as_uint(m);
+        if (any_bad) atomicOr(&a.sc->nonfinite, 1u);
+        __threadfence();
+        s_last = atomicAdd(a.done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last || threadIdx.x != 0) return;
+    __threadfence();
+    float m = 0.f;
+    for (unsigned b = 0; b < gridDim.x; ++b) m = fmaxf(m, __uint_as_float(__ldcg(a.block_max + b)));
+    for (int c = 0; c < kMaxDim; ++c) a.sc->mu[c] = a.mu_src->mu[c];
+    a.sc->max_half_norm_bits = __float_as_uint(m);
     int e = 0;
-    while (e < 60 && ldexpf(hn, -2 * e) > 8192.0f) ++e;
-    sc->e = e;
-    sc->dscale = ldexpf(1.0f, 2 * e);
+    while (e < 60 && ldexpf(m, -2 * e) > 8192.0f) ++e;
+    a.sc->e = e;
+    a.sc->dscale = ldexpf(1.0f, 2 * e);
+    if (a.clear_u32) *a.clear_u32 = 0u;
+    *a.done = 0u;
 }
 
 // ---- operand packing ------------------------------------------------------------
@@ -108,9 +203,27 @@ __device__ __forceinline__ uint32_t pack_h2(__half a, __half b) {
            (static_cast<uint32_t>(__half_as_ushort(b)) << 16);
 }
 
+__device__ __forceinline__ void pack_row(const PackArgs& a, size_t i);
+
 __global__ void pack_operands(PackArgs a) {
     const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-    if (i >= a.rows_padded) return;
+    if (i < a.rows_padded) pack_row(a, i);
+}
+
+// both operands of a pass in one launch: blocks [0, blocks_a) pack a, the rest b
+__global__ void pack_two(PackArgs a, PackArgs b, unsigned int blocks_a) {
+    pdl_launch_dependents();
+    pdl_wait();
+    if (blockIdx.x < blocks_a) {
+        const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+        if (i < a.rows_padded) pack_row(a, i);
+    } else {
+        const size_t i = (blockIdx.x - blocks_a) * (size_t)blockDim.x + threadIdx.x;
+        if (i < b.rows_padded) pack_row(b, i);
+    }
+}
+
+__device__ __forceinline__ void pack_row(const PackArgs& a, size_t i) {
     __half yh[kMaxDim], yl[kMaxDim];
     __half n1 = __float2half(0.f), n2 = n1, n3 = n1;
     const __half one = __float2half(1.f), zero = __float2half(0.f);
@@ -222,6 +335,8 @@ struct FinalizeArgs {
 // doubles of the [split][row][16] partials and write consecutive score /
 // x^SD entries (a thread per row strided every access by 128 B).
 __global__ void finalize_score(FinalizeArgs a) {
+    pdl_launch_dependents();
+    pdl_wait();
     const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
     const size_t i = t / static_cast<size_t>(a.d);
     const int c = static_cast<int>(t % static_cast<size_t>(a.d));
@@ -281,6 +396,8 @@ struct ReduceArgs {
 };
 
 __global__ void reduce_density(ReduceArgs a) {
+    pdl_launch_dependents();
+    pdl_wait();
     const size_t j = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
     if (j >= a.rows) return;
     double s0 = 0.0, s1 = 0.0;
