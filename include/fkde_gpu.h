@@ -80,7 +80,9 @@ enum {
                                  clock64 stamps of the score kernel's block 0   */
     FKDE_OPT_SPATIAL = 7,     /* score pass on a spatial (Morton / principal-axis)
                                  order of the points with exact-zero tile skipping:
-                                 0 = auto (n >= 32768), 1 = always, 2 = never    */
+                                 0 = auto (n >= 32768), 1 = always, 2 = never,
+                                 3 = the order without skipping (tests: skipping
+                                 must not change a bit)                          */
     FKDE_OPT_PDL = 8          /* 1 (default) = launch the kernel chain with
                                  programmatic dependent launch; 0 = plain launches */
 };
@@ -121,9 +123,9 @@ int fkde_gpu_last_timing(const fkde_gpu_ctx* ctx, float* ms, int n);
 /* number of kernels this library launched during the last call (this rank) */
 int64_t fkde_gpu_last_launch_count(const fkde_gpu_ctx* ctx);
 /* score-pass tile skipping of the last call on device 0 (synchronises):
- * out[0] = quadrant-tiles checked, out[1] = quadrant-tiles whose P was all zero
- * (exps skipped), out[2] = tiles whose GEMM2 was skipped, out[3] = 1 if the
- * pass ran on the spatial order */
+ * out[0] = (row tile, column tile) pairs checked exactly, out[1] = pairs
+ * skipped (every pair of points in them contributes exactly zero), out[2] =
+ * pairs in the pass, out[3] = 1 if the pass ran on the spatial order */
 int fkde_gpu_last_skip_stats(fkde_gpu_ctx* ctx, uint64_t* out4);
 /* device workspace currently held by the context (all devices), bytes: the
  * analogue of the reference's transient-allocation accounting

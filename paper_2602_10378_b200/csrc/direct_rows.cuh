@@ -35,7 +35,7 @@ enum { kExactScore = 0, kExactGauss = 1, kExactLaplace = 2 };
 // |y|^2/2 (y = (x - mu) sqrt(log2 e) / h, i.e. log2 units) above which a row's
 // expanded-norm rounding (~|y|^2/2 * 2^-23 in log2 phi) is no longer well
 // inside the 1e-3 score tolerance: such rows are recomputed here.
-constexpr double kRiskHalfNorm = 256.0;
+constexpr double kRiskHalfNorm = 128.0;
 
 constexpr int kDirRows = 128;        // rows per block (one per thread)
 constexpr int kDirTileCols = 128;    // columns per shared-memory tile

@@ -188,13 +188,15 @@ struct Device {
     cudaEvent_t ev_side_in = nullptr, ev_side_out = nullptr;
     ncclComm_t comm = nullptr;
     bool attrs_set = false;
-    DevBuf X, Y, opA, opB, part0, part1, xsd, out, aux0, aux1, colpart, scal, err, flags;
+    DevBuf X, Y, opA, opB, opB2, part0, part1, xsd, out, aux0, aux1, colpart, scal, err, flags;
     DevBuf risk, dpart, ddone;   // direct_rows_kernel: spread flags, partials, counters
     DevBuf pdone;                // prep_stats / scale_two completion counters (self-resetting)
     DevBuf qmax;                 // scale_two per-block maxima
     // spatial order of the score pass (spatial_order.cuh): sorted points, permutation,
     // keys, CUB scratch, axes, tile centroids, skip statistics, un-permuted outputs
-    DevBuf Xs, perm, keys, cubtmp, ordsc, cenA, cenB, skipstats, unperm0, unperm1;
+    DevBuf Xs, perm, keys, cubtmp, ordsc, cenA, cenB, skipstats, unperm0, unperm1, pmask, smask;
+    size_t mask_bytes = 0;       // skip mask of the last score pass (0: none)
+    uint64_t tiles_total = 0;    // tile pairs of the last score pass
     bool ordered = false;        // last score pass ran on the spatial order
     cudaEvent_t ev[FKDE_T_COUNT + 1] = {};
     int64_t launches = 0;
@@ -496,7 +498,7 @@ constexpr size_t kSpatialMinN = 32768;
 constexpr float kSkipPredict = 40.0f;
 
 bool use_spatial(const Options& o, size_t n) {
-    return o.spatial == 1 || (o.spatial == 0 && n >= kSpatialMinN);
+    return o.spatial == 1 || o.spatial == 3 || (o.spatial == 0 && n >= kSpatialMinN);
 }
 
 // Spatial order of the training points (spatial_order.cuh): D.Xs = X[perm],
@@ -585,21 +587,64 @@ Status score_program(Device& D, const Options& o, const Job& J, const double* dX
     a.diag_row0 = static_cast<long long>(sh.begin);
     a.trace = o.trace;
     a.stats = D.skipstats.as<unsigned long long>();   // (cleared by prep_stats)
+    D.mask_bytes = 0;
+    D.tiles_total = static_cast<uint64_t>(rt) * ct;
     if (D.ordered) {
+        // spatial order: tile centroids, and GEMM2 on the column operand centred per
+        // column tile (B2, layout.cuh) with a drain after every visited tile
         STATUS_TRY(ensure(D.cenA, rt * kMaxDim * sizeof(float)));
         STATUS_TRY(ensure(D.cenB, ct * kMaxDim * sizeof(float)));
         tile_centroids<<<static_cast<unsigned>(rt), 128, 0, D.stream>>>(
             dX + sh.begin * d, sh.rows, d, sc, ks, kTileRows, D.cenA.as<float>());
         tile_centroids<<<static_cast<unsigned>(ct), 128, 0, D.stream>>>(
             dX, n, d, sc, ks, static_cast<int>(kScoreNCol), D.cenB.as<float>());
-        D.launches += 2;
-        a.cenA = D.cenA.as<float>();
-        a.cenB = D.cenB.as<float>();
+        size_t b2_pad = 0;
+        PackArgs p2;
+        STATUS_TRY(pack_args(D, dX, n, d, 2, true, ks, sc, D.opB2, &b2_pad, &p2, col_align));
+        p2.cen = D.cenB.as<float>();
+        p2.cen_tile = static_cast<int>(kScoreNCol);
+        pack_operands<<<grid1(b2_pad, 128), 128, 0, D.stream>>>(p2);
+        D.launches += 3;
+        CUDA_TRY(cudaGetLastError());
+        static const bool no_b2 = std::getenv("FKDE_NO_B2") != nullptr;   // debug A/B
+        if (!no_b2) {
+            a.opB2 = D.opB2.as<uint8_t>();
+            a.cenB = D.cenB.as<float>();
+            a.flush_log2 = 0;
+        }
+    }
+    if (D.ordered && o.spatial != 3) {
+        // tile skipping: centroids -> predicted pairs -> exact check -> skip mask
+        const int words = static_cast<int>((ct + 31) / 32);
+        const size_t mbytes = rt * words * sizeof(uint32_t);
+        STATUS_TRY(ensure(D.pmask, mbytes));
+        STATUS_TRY(ensure(D.smask, mbytes));
         static const float pred = [] {   // debug override for A/B runs (tools/spatial_probe.py)
             const char* e = std::getenv("FKDE_SKIP_PRED");
             return e && *e ? static_cast<float>(std::atof(e)) : kSkipPredict;
         }();
-        a.skip_pred = pred;
+        tile_predict<<<grid1(rt * words, 128), 128, 0, D.stream>>>(
+            D.cenA.as<float>(), static_cast<int>(rt), D.cenB.as<float>(), static_cast<int>(ct), words,
+            pred, D.pmask.as<uint32_t>(), D.smask.as<uint32_t>());
+        D.launches += 1;
+        CUDA_TRY(cudaGetLastError());
+        PairArgs c = a;
+        c.opB2 = nullptr;
+        c.cenB = nullptr;
+        if (std::getenv("FKDE_TRACE_CHECK")) {   // debug: trace the check pass, not the score pass
+            c.trace = a.trace;
+            a.trace = nullptr;
+        } else {
+            c.trace = nullptr;
+        }
+        c.pred_mask = D.pmask.as<uint32_t>();
+        c.skip_mask = D.smask.as<uint32_t>();
+        c.mask_words = words;
+        c.splits = choose_splits(o, rt, ct, ctas);
+        STATUS_TRY(launch_pairwise<kModeCheck>(D, o, c, n));
+        a.skip_mask = D.smask.as<uint32_t>();
+        a.mask_words = words;
+        D.mask_bytes = mbytes;
     }
     STATUS_TRY(launch_pairwise<kModeScore>(D, o, a, n));
     record(D, o, FKDE_T_FINALIZE);
@@ -1141,7 +1186,7 @@ void fkde_gpu_destroy(fkde_gpu_ctx* ctx) {
                           &D.xsd,  &D.out,   &D.aux0, &D.aux1, &D.colpart, &D.scal,
                           &D.err,  &D.flags, &D.risk, &D.dpart, &D.ddone,
                           &D.Xs,   &D.perm,  &D.keys, &D.cubtmp, &D.ordsc, &D.cenA,
-                          &D.cenB, &D.skipstats, &D.unperm0, &D.unperm1, &D.pdone, &D.qmax};
+                          &D.cenB, &D.skipstats, &D.unperm0, &D.unperm1, &D.pdone, &D.qmax, &D.pmask, &D.smask, &D.opB2};
         for (DevBuf* b : bufs)
             if (b->p) cudaFree(b->p);
         for (auto& e : D.ev)
@@ -1192,7 +1237,7 @@ int fkde_gpu_set_option(fkde_gpu_ctx* ctx, int key, int64_t value) {
             ctx->opt.pdl = value != 0;
             return FKDE_OK;
         case FKDE_OPT_SPATIAL:
-            if (value < 0 || value > 2) return FKDE_INVALID_ARGUMENT;
+            if (value < 0 || value > 3) return FKDE_INVALID_ARGUMENT;
             ctx->opt.spatial = static_cast<int>(value);
             return FKDE_OK;
         case FKDE_OPT_FLUSH_TILES:
@@ -1243,7 +1288,7 @@ int fkde_gpu_workspace_bytes(const fkde_gpu_ctx* ctx, size_t* bytes) {
                                 &D.xsd,  &D.out,   &D.aux0, &D.aux1, &D.colpart, &D.scal,
                                 &D.err,  &D.flags, &D.risk, &D.dpart, &D.ddone,
                                 &D.Xs,   &D.perm,  &D.keys, &D.cubtmp, &D.ordsc, &D.cenA,
-                                &D.cenB, &D.skipstats, &D.unperm0, &D.unperm1, &D.pdone, &D.qmax};
+                                &D.cenB, &D.skipstats, &D.unperm0, &D.unperm1, &D.pdone, &D.qmax, &D.pmask, &D.smask, &D.opB2};
         for (const DevBuf* b : bufs) total += b->bytes;
     }
     *bytes = total;
@@ -1257,10 +1302,19 @@ int fkde_gpu_last_skip_stats(fkde_gpu_ctx* ctx, uint64_t* out4) {
     if (!D.skipstats.p) return FKDE_OK;
     cudaSetDevice(D.dev);
     if (cudaStreamSynchronize(D.stream) != cudaSuccess) return FKDE_CUDA_ERROR;
-    unsigned long long h[3] = {0, 0, 0};
+    unsigned long long h[1] = {0};
     if (cudaMemcpy(h, D.skipstats.p, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess)
         return FKDE_CUDA_ERROR;
-    for (int i = 0; i < 3; ++i) out4[i] = h[i];
+    uint64_t skipped = 0;
+    if (D.mask_bytes) {   // popcount of the skip mask
+        std::vector<uint32_t> m(D.mask_bytes / sizeof(uint32_t));
+        if (cudaMemcpy(m.data(), D.smask.p, D.mask_bytes, cudaMemcpyDeviceToHost) != cudaSuccess)
+            return FKDE_CUDA_ERROR;
+        for (uint32_t w : m) skipped += static_cast<uint64_t>(__builtin_popcount(w));
+    }
+    out4[0] = h[0];
+    out4[1] = skipped;
+    out4[2] = D.tiles_total;
     out4[3] = D.ordered ? 1 : 0;
     return FKDE_OK;
 }

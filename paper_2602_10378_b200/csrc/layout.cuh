@@ -26,6 +26,14 @@
 // phi as T), 32-47 = sum_j phi_ij y_lo_j.  The first 32 columns (T_hi, S) are
 // drained to fp64 every few tiles; T_lo (2^-11 smaller) only at the end.
 //
+// Score pass on the spatial order: GEMM2 reads a third operand image instead of B,
+// "B2" (format 2): v = y - c_J with c_J the column tile's centroid, chunks 0-1
+// v_hi, chunk 2 = [1 0 0 0 0 0 0 0] (column 16: S), 4-5 v_lo, the rest zero.  The
+// tensor core's fp32 accumulation loses bits in proportion to the accumulator's
+// magnitude; centring each column tile on its own centroid (tiles are spatially
+// compact there) shrinks that magnitude from |y| S to the tile's radius times S,
+// and the drain adds c_J S exactly per tile.
+//
 // c adds a constant to every product: the score pass packs c = 15 * 2^-2e, so
 // S * 2^2e = log2(phi * 2^15) comes off the tensor core with the P' scale
 // (kPScaleExp) applied exactly inside the accumulation (one rounding fewer than

@@ -20,12 +20,21 @@
 //          (B = the same column tile, MN-major) -> sum_j phi y_hi_j,
 //          sum_j phi y_lo_j, sum_j phi  (TMEM, fp32; drained by the drain warps)
 // The n x n kernel matrix never leaves the SM; per column tile the SMEM
-// traffic is the 16 KiB B tile read by both GEMMs and the 16 KiB A tile.
+// traffic is the 12 KiB B tile read by both GEMMs and the 16 KiB A tile.
+//
+// Tile skipping (score pass on the spatial order, spatial_order.cuh): the score
+// pass carries phi' = phi 2^15 as fp16 hi + lo, so a pair with log2 phi' < -25
+// contributes exactly zero.  A CHECK pass (MODE kModeCheck: GEMM1 + an exact
+// max over the tile, no exps) visits the tile pairs a centroid predictor marked
+// (pred mask) and leaves in the skip mask those whose every pair is below
+// kSkipLog2; the SCORE pass then visits only the column tiles whose skip bit is
+// clear.  A skipped tile would have added exact zeros: the result is the same as
+// visiting it.
 //
 // Warp roles: warp 0 = bulk-copy producer, warp 1 = TMEM owner + GEMM1 issuer;
 // score pass: warp 2 = GEMM2 issuer, warps 4..7 = O drain warps (one per TMEM
-// lane quadrant), warps 8.. = epilogue; KDE: warps 2.. = epilogue.  Epilogue
-// warp w reads TMEM lane quadrant w%4 of every kNP-th tile.  Pipelines
+// lane quadrant), warps 8.. = epilogue; KDE / check: warps 2.. = epilogue.
+// Epilogue warp w reads TMEM lane quadrant w%4 of every kNP-th tile.  Pipelines
 // (mbarriers): A tiles x2, B tiles x kStages, S/P accumulators x kSBuf (TMEM),
 // O x2 (TMEM, score).
 #pragma once
@@ -42,44 +51,48 @@ enum PairMode : int {
     kModeScore = 0,     // stream_score_totals
     kModeGauss = 1,     // stream_kde_pass, PairTerm::Gaussian
     kModeLaplace = 2,   // two sums (phi, phi*log2 phi): LaplaceFused / LaplaceCorrection
+    kModeCheck = 3,     // score tile skipping: exact per-tile max of log2 phi' (no exps)
 };
 
 struct PairArgs {
     const uint8_t* opA;   // row tiles (A format), n_row_tiles * 16 KiB
-    const uint8_t* opB;   // column tiles (B format), n_col_tiles * 16 KiB
+    const uint8_t* opB;   // column tiles (B format), n_col_tiles * kColBytes
     int n_row_tiles;
     int n_col_tiles;
     int splits;           // column ranges per row tile
     const PassScalars* sc;
-    float* part0;         // KDE: [splits*2][rows_pad]
-    float* part1;         // Laplace: [splits*2][rows_pad]
+    float* part0;         // KDE: [splits*kNP][rows_pad]
+    float* part1;         // Laplace: [splits*kNP][rows_pad]
     double* dpart0;       // SCORE: S' [splits][rows_pad]   (fp64)
     double* dpart1;       // SCORE: T' [splits][rows_pad][16] (fp64)
-    int flush_log2;       // SCORE: O is drained every 2^flush_log2 column tiles (a sub-unit)
+    int flush_log2;       // SCORE: O is drained every 2^flush_log2 visited column tiles
     size_t rows_pad;
     // SCORE: column tile holding row tile 0's diagonal (rows and columns are
     // the same point set, row shard starting at global point diag_row0); the self pair
     // phi_ii = 1 is excluded from the tensor-core sums and added back exactly
     // in finalize_score, so that T - x S never cancels against the self term.
     long long diag_row0;  // -1: no diagonal
+    // tile masks, one bit per (row tile, column tile), rows of mask_words words:
+    //   SCORE: skip_mask (nullptr = visit every tile): visit tiles whose bit is 0
+    //   CHECK: pred_mask selects the tiles to check (bit 1); skip_mask starts as a
+    //          copy of it and loses the bit of every tile that is not skippable
+    const uint32_t* pred_mask;
+    uint32_t* skip_mask;
+    int mask_words;
+    unsigned long long* stats;   // CHECK (optional): [0] += tiles checked
+    // SCORE on the spatial order (nullptr otherwise): GEMM2's column operand centred
+    // per column tile (layout.cuh "B2") and the column-tile centroids the drain adds
+    // back (log2 units, unscaled); the drain then runs after every visited tile
+    const uint8_t* opB2;
+    const float* cenB;
     // debug (builds with -DFKDE_ENABLE_TRACE only): per-event clock64 trace of
     // block 0 (nullptr = off).  Layout [warp][event slot][tile] -> long long
     long long* trace;
-    // SCORE tile skipping (spatial_order.cuh): per-tile centroids (log2 units) of
-    // the row tiles (128) and column tiles (kNCol); a tile pair whose centroid
-    // half-distance^2 exceeds skip_pred is checked exactly (max log2 phi' over
-    // the tile) and, where every pair rounds to fp16 zero, its exps and (if all
-    // four lane quadrants agree) its GEMM2 are skipped.  nullptr = no skipping.
-    const float* cenA;
-    const float* cenB;
-    float skip_pred;
-    unsigned long long* stats;   // optional: [0] tiles checked (x4 quadrants),
-                                 // [1] quadrant-tiles skipped, [2] GEMM2 tiles skipped
 };
 // log2 phi' (S * dscale, with the 2^15 offset) below which both fp16 halves of
 // phi' are exactly zero (phi' < 2^-25 rounds to zero; one unit of margin for ex2.approx)
 constexpr float kSkipLog2 = -26.0f;
-constexpr uint32_t kCenBytes = kMaxDim * sizeof(float);   // one tile centroid
+
 #ifdef FKDE_ENABLE_TRACE
 #define FKDE_TRACE(slot, tile)                                                               \
     do {                                                                                     \
@@ -92,14 +105,62 @@ constexpr uint32_t kCenBytes = kMaxDim * sizeof(float);   // one tile centroid
     } while (0)
 #endif
 
-#ifndef FKDE_LO_SEPARATE
-#define FKDE_LO_SEPARATE 0
-#endif
+// Column tiles of one unit that a pass visits: [.., end) filtered by a mask row
+// (bit == want).  Every warp of the CTA walks the same sequence.  The walk keeps
+// the current mask word in a register, so a step costs a few integer ops and a
+// load only every 32 tiles (a load per step put an L1 round trip on every tile
+// of every warp's critical path).
+struct TileWalk {
+    const uint32_t* row;   // nullptr: every tile
+    int end;
+    uint32_t want;         // 0u: visit clear bits, ~0u: visit set bits
+    int w = 0;             // current word
+    uint32_t bits = 0;     // visited tiles of word w not yet returned
+    __device__ __forceinline__ uint32_t word(int i) const { return ~(row[i] ^ want); }
+    __device__ __forceinline__ int first(int from) {   // first visited tile >= from, or end
+        if (!row) {
+            w = from;
+            return from < end ? from : end;
+        }
+        if (from >= end) return end;
+        w = from >> 5;
+        bits = word(w) & (0xFFFFFFFFu << (from & 31));
+        return next();
+    }
+    __device__ __forceinline__ int next() {   // the following visited tile, or end
+        if (!row) {
+            ++w;
+            return w < end ? w : end;
+        }
+        while (!bits) {
+            if (((w + 1) << 5) >= end) return end;
+            bits = word(++w);
+        }
+        const int c = (w << 5) + __ffs(bits) - 1;
+        bits &= bits - 1u;
+        return c < end ? c : end;
+    }
+    __device__ __forceinline__ int count(int from) const {   // visited tiles in [from, end)
+        if (!row) return end > from ? end - from : 0;
+        int n = 0;
+        while (from < end) {
+            const int i = from >> 5;
+            uint32_t b = word(i) & (0xFFFFFFFFu << (from & 31));
+            const int top = end - (i << 5);
+            if (top < 32) b &= (1u << top) - 1u;
+            n += __popc(b);
+            from = (i + 1) << 5;
+        }
+        return n;
+    }
+};
 
 template <int MODE>
 struct TcConfig {
     static constexpr bool kScore = MODE == kModeScore;
-    // KDE: warps 0 producer, 1 GEMM1 issuer (+ TMEM owner), 2 .. 2+4*kNP-1
+    static constexpr bool kCheck = MODE == kModeCheck;
+    static constexpr bool kScoreTiling = kScore || kCheck;   // 96-column tiles
+    // KDE / CHECK: warps 0 producer, 1 GEMM1 issuer (+ TMEM owner), 2 .. 2+4*kNP-1
     // epilogue (kNP warps per TMEM lane quadrant, one per SM sub-partition each).
     // SCORE: warpgroup 0 = control (0 producer, 1 GEMM1 issuer + TMEM owner,
     // 2 GEMM2 issuer, 3 idle), warpgroups 1..kNP = epilogue.  tcgen05.mma issue
@@ -113,13 +174,25 @@ struct TcConfig {
 #ifndef FKDE_SCORE_NP
 #define FKDE_SCORE_NP 3
 #endif
+#ifndef FKDE_CHECK_NP
+#define FKDE_CHECK_NP 2
+#endif
 #ifndef FKDE_CTRL_REGS
 #define FKDE_CTRL_REGS 56
 #endif
-    static constexpr int kNP = kScore ? FKDE_SCORE_NP : FKDE_EPI_NP;   // epilogue warps per lane quadrant
+    static constexpr int kNP = kScore ? FKDE_SCORE_NP : (kCheck ? FKDE_CHECK_NP : FKDE_EPI_NP);
     // score: warpgroup 1 (warps 4..7) = the O drain warps, one per lane quadrant
-    static constexpr int kCtrlEnd = kScore ? 4 : 2;
-    static constexpr int kEpi0 = kScore ? 8 : 2;
+    // GEMM1 issuing warps: the check pass does little per tile, so its GEMM1 loop
+    // (two barrier waits + four blocking MMA issues, ~900 cycles a tile on one
+    // warp: trace_check.py) is the bottleneck; three issuers take turns by tile
+    // and overlap one another's waits with the MMAs in flight
+#ifndef FKDE_CHECK_ISSUERS
+#define FKDE_CHECK_ISSUERS 3
+#endif
+    static constexpr int kIssuers = kCheck ? FKDE_CHECK_ISSUERS : 1;
+    static constexpr int kCtrlEnd = kScore ? 4 : 1 + kIssuers;
+    static constexpr int kEpi0 = kScore ? 8 : (kCheck ? 4 : 2);
+    static_assert(kEpi0 >= kCtrlEnd, "control warps before the epilogue warps");
     static constexpr int kEpiEnd = kEpi0 + 4 * kNP;
     static constexpr int kG2Warp = kScore ? 2 : -1;
     static constexpr int kThreads = kEpiEnd * 32;
@@ -132,46 +205,36 @@ struct TcConfig {
         kScore ? (kLaunchRegs * kThreads - 128 * kCtrlRegs - 128 * kLaunchRegs) / (128 * kNP) / 8 * 8
                : 0;
     static_assert(!kScore || (kEpiRegs >= kLaunchRegs && kEpiRegs <= 256), "setmaxnreg split");
-    // B-stage ring: the score pass streams 12 KiB column tiles; with tile skipping a
-    // tile can be done in a fraction of its exp time, so the ring must cover the L2
-    // latency of many tiles in flight (ncu: GEMM1 waiting on b_full with 8 stages).
-    // Score stages are 13 KiB (tile + the centroid slot, 1 KiB aligned), KDE 16 KiB.
+    // B-stage ring: 96-column tiles are 12 KiB; the check pass finishes a tile in a
+    // fraction of the score pass's time, so its ring covers many tiles of L2 latency
 #ifndef FKDE_SCORE_STAGES
 #define FKDE_SCORE_STAGES 14
 #endif
-    static constexpr int kStages = kScore ? FKDE_SCORE_STAGES : 8;
+    // score stages hold the B tile and (spatial order) its centred B2 twin: 7 x 24 KiB
+    static constexpr int kStages = kScore ? 7 : (kCheck ? FKDE_SCORE_STAGES : 8);
     static constexpr uint32_t kOffA = 0;
     // column tile width: score 96 points (4 S/P buffers of 96 TMEM columns fit
     // beside the two O buffers; 3 of 128 made the S ring the bottleneck), KDE 128
 #ifndef FKDE_SCORE_NCOL
 #define FKDE_SCORE_NCOL 96
 #endif
-    static constexpr int kNCol = kScore ? FKDE_SCORE_NCOL : 128;
+    static constexpr int kNCol = kScoreTiling ? FKDE_SCORE_NCOL : 128;
     static constexpr uint32_t kColBytes = kNCol * kRowBytes;   // one B column tile
     static_assert(kNCol % 32 == 0 && kColBytes % 1024 == 0, "column tiles of whole SW128 atoms");
-    static constexpr uint32_t kBStride = kScore ? kColBytes + 1024 : kTileBytes;   // B stage stride
-    static_assert(kBStride % 1024 == 0 && (!kScore || kColBytes + 64 <= kBStride), "SW128 stages + centroid slot");
+    static constexpr uint32_t kBStride = kScore ? 2 * kColBytes : kColBytes;   // B (+ B2) per stage
     static constexpr uint32_t kOffB = 2 * kTileBytes;
-    static constexpr uint32_t kOffAcc = kOffB + kStages * kBStride;
-    static constexpr uint32_t kAccBytes = 0;
-    static constexpr uint32_t kOffBar = kOffAcc + kAccBytes;
+    static constexpr uint32_t kOffBar = kOffB + kStages * kBStride;
     // S accumulators in TMEM.  Score: 4 S/P buffers of 96 columns (a tile's S is
     // overwritten by its P; the buffer is free again once GEMM2 has read P) +
-    // O[2] at column 384.  KDE: 4 of 128 (freed as soon as S is loaded).
-    static constexpr int kSBuf = kScore ? 384 / kNCol : 4;
+    // O[2] at column 384.  KDE: 4 of 128, check: 5 of 96 (freed once S is loaded).
+    static constexpr int kSBuf = kScore ? 384 / kNCol : (kCheck ? 512 / kNCol : 4);
     static constexpr uint32_t kNumBars = 4 + 2 * kStages + 4 * kSBuf + 4;
     // + tmem slot, 1 KiB alignment slack
     static constexpr uint32_t kSmemBytes = kOffBar + kNumBars * 8 + 64 + 1024;
-    static_assert(4 * (1 + kSBuf + 2) <= 64, "tmem slot + skip flags + o_zero fit the 64 B tail");
     static constexpr uint32_t kTmemCols = 512;
     static constexpr uint32_t kTmemO = 384;   // score: O[2] (2 x 64 cols: T_hi, S, T_lo)
-    // FKDE_LO_SEPARATE: the P_lo half of GEMM2 accumulates into its own 32 columns
-    // (O_lo, next to O), so the main accumulator takes half the MMA steps per tile
-    // and P_lo's small products are not truncated against the large main sums;
-    // the 80 columns fit once, so O is single-buffered
-    static constexpr int kOBuf = FKDE_LO_SEPARATE ? 1 : 2;
-    static constexpr uint32_t kOStride = 64;
     static_assert(!kScore || kSBuf * kNCol <= kTmemO, "S/P buffers overlap O");
+    static_assert(kSBuf * kNCol <= kTmemCols, "S buffers fit TMEM");
     static constexpr uint32_t kN2 = 48;       // GEMM2 N
 };
 
@@ -188,12 +251,12 @@ struct TcConfig {
 #define FKDE_G2_LO_N 32
 #endif
 
-
 template <int MODE>
 __global__ void __launch_bounds__(TcConfig<MODE>::kThreads, 1)
 pairwise_tc_kernel(PairArgs args) {
     using Cfg = TcConfig<MODE>;
     constexpr bool kScore = Cfg::kScore;
+    constexpr bool kCheck = Cfg::kCheck;
     constexpr int kStages = Cfg::kStages;
 
     extern __shared__ uint8_t smem_raw[];
@@ -214,13 +277,6 @@ pairwise_tc_kernel(PairArgs args) {
     uint64_t* o_full = s_free + kSB;      // [2]
     uint64_t* o_empty = o_full + 2;       // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
-    // score: per S/P buffer, one byte per lane quadrant = "this quadrant's P is all zero"
-    // (written before p_full's arrive, read by the GEMM2 warp after its wait)
-    uint32_t* skipf = tmem_slot + 1;   // [kSBuf]
-    // score: O sub-unit produced no MMA (every tile of it skipped): one byte per
-    // drain warp, all set by the GEMM2 warp before its plain arrive on o_full, each
-    // cleared by its own drain warp before that warp releases the buffer (O = 0)
-    volatile uint32_t* o_zero = skipf + Cfg::kSBuf;   // [2] x 4 bytes
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -228,7 +284,7 @@ pairwise_tc_kernel(PairArgs args) {
     if (threadIdx.x == 0) {
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(&a_full[i], 1);
-            ptx::mbar_init(&a_empty[i], 1);
+            ptx::mbar_init(&a_empty[i], Cfg::kIssuers);   // one commit per GEMM1 issuer
         }
         for (int i = 0; i < kSB; ++i) {
             ptx::mbar_init(&s_full[i], 1);
@@ -244,8 +300,6 @@ pairwise_tc_kernel(PairArgs args) {
             ptx::mbar_init(&o_full[i], 1);
             ptx::mbar_init(&o_empty[i], 4);
         }
-        if constexpr (kScore) o_zero[0] = o_zero[1] = 0u;
-
         ptx::fence_barrier_init();
     }
     pdl_launch_dependents();
@@ -258,6 +312,15 @@ pairwise_tc_kernel(PairArgs args) {
     pdl_wait();
 
     const int n_units = args.n_row_tiles * args.splits;
+    // the column tiles a unit visits (score: clear skip bits; check: set pred bits)
+    auto walk_of = [&](int rt, int ct1) {
+        TileWalk w;
+        const uint32_t* m = kCheck ? args.pred_mask : (kScore ? args.skip_mask : nullptr);
+        w.row = m ? m + (size_t)rt * args.mask_words : nullptr;
+        w.end = ct1;
+        w.want = kCheck ? ~0u : 0u;
+        return w;
+    };
 
     // Control warps (producer, MMA issuers) and epilogue warps live in separate
     // warpgroups in the score pass; each side resizes its register file at the
@@ -277,6 +340,9 @@ pairwise_tc_kernel(PairArgs args) {
             const int sp = u / args.n_row_tiles, rt = u % args.n_row_tiles;
             const int ct0 = static_cast<int>((long long)sp * args.n_col_tiles / args.splits);
             const int ct1 = static_cast<int>((long long)(sp + 1) * args.n_col_tiles / args.splits);
+            TileWalk wk = walk_of(rt, ct1);
+            int ct = wk.first(ct0);
+            if (ct >= ct1) continue;   // nothing to visit: no A tile either
             const int ab = it_a & 1;
             ptx::mbar_wait(&a_empty[ab], ((it_a >> 1) & 1) ^ 1);
             if (ptx::elect_one()) {
@@ -286,25 +352,24 @@ pairwise_tc_kernel(PairArgs args) {
             }
             __syncwarp();
             ++it_a;
-            for (int ct = ct0; ct < ct1; ++ct) {
+            for (; ct < ct1; ct = wk.next()) {
                 const int st = it_b % kStages;
                 ptx::mbar_wait(&b_empty[st], ((it_b / kStages) & 1) ^ 1);
                 if (ptx::elect_one()) {
-                    // score tile skipping: the column tile's centroid (64 B) rides in the
-                    // stage's unused tail, on the same barrier
-                    const uint32_t extra = (kScore && args.cenB) ? kCenBytes : 0u;
-                    ptx::mbar_arrive_expect_tx(&b_full[st], Cfg::kColBytes + extra);
+                    const bool b2 = kScore && args.opB2;
+                    ptx::mbar_arrive_expect_tx(&b_full[st], Cfg::kColBytes * (b2 ? 2u : 1u));
                     ptx::bulk_g2s_hint(smB + st * Cfg::kBStride, args.opB + (size_t)ct * Cfg::kColBytes,
                                        Cfg::kColBytes, &b_full[st], pol_b);
-                    if (extra)
-                        ptx::bulk_g2s(smB + st * Cfg::kBStride + Cfg::kColBytes,
-                                      args.cenB + (size_t)ct * kMaxDim, kCenBytes, &b_full[st]);
+                    if (b2)
+                        ptx::bulk_g2s_hint(smB + st * Cfg::kBStride + Cfg::kColBytes,
+                                           args.opB2 + (size_t)ct * Cfg::kColBytes, Cfg::kColBytes,
+                                           &b_full[st], pol_b);
                 }
                 __syncwarp();
                 ++it_b;
             }
         }
-    } else if (warp == 1 || (kScore && warp == Cfg::kG2Warp)) {
+    } else if ((warp >= 1 && warp <= Cfg::kIssuers) || (kScore && warp == Cfg::kG2Warp)) {
         static_assert(Cfg::kNP <= Cfg::kSBuf, "each epilogue warp holds one S buffer");
         // ===================== MMA issuers =====================
         // Whole warp in the loop, one elected lane issues every tcgen05 op
@@ -316,42 +381,52 @@ pairwise_tc_kernel(PairArgs args) {
         constexpr uint32_t idesc2 = ptx::idesc_f16_f32(128, Cfg::kN2, false, true);
         // P_lo rows only need the y_hi and ones columns: P_lo . y_lo is 2^-22 of the
         // sum and is dropped, which takes 1/6 of GEMM2's MACs (and power) away
-        constexpr uint32_t idesc2_lo = ptx::idesc_f16_f32(128, FKDE_G2_LO_N > 0 ? FKDE_G2_LO_N : 32, false, true);
+        constexpr uint32_t idesc2_lo = ptx::idesc_f16_f32(128, FKDE_G2_LO_N, false, true);
         const uint64_t descA = ptx::smem_desc_sw128(ptx::smem_u32(smA), 16, 1024);
         const uint64_t descB = ptx::smem_desc_sw128(ptx::smem_u32(smB), 16, 1024);
-        const uint64_t descBmn = ptx::smem_desc_sw128(ptx::smem_u32(smB), kTileBytes, 1024);
+        // GEMM2's operand: the stage's B tile, or its centred B2 twin (spatial order)
+        const uint64_t descBmn = ptx::smem_desc_sw128(
+            ptx::smem_u32(smB) + ((kScore && args.opB2) ? Cfg::kColBytes : 0u), kTileBytes, 1024);
         uint32_t it_a = 0, it_b = 0, it_s = 0, it_u = 0;
-        bool o_started = false;   // GEMM2: an MMA has written the current O sub-unit
-        unsigned long long n_g2skip = 0;   // statistics: tiles whose GEMM2 was skipped
-        const bool g1 = warp == 1;
-        // GEMM2 (warp 10): O += P_hi.B + P_lo.B, P read from TMEM.  The
+        const bool g1 = warp >= 1 && warp <= Cfg::kIssuers;
+        const uint32_t my_turn = static_cast<uint32_t>(warp - 1);   // GEMM1: tiles it_s % kIssuers
+        // GEMM2 (warp 2): O += P_hi.B + P_lo.B, P read from TMEM.  The
         // epilogue stored, for each 32-column chunk c of S buffer sb, P_hi
         // (packed fp16 pairs) for K = 32c..32c+31 in the chunk's first 16
         // columns and P_lo in the next 16.  O is accumulated in TMEM over
-        // 2^flush_log2 column tiles (a "sub-unit"), then drained by the epilogue;
-        // two O buffers alternate so the drain overlaps the next sub-unit.  This
-        // bounds the tensor core's fp32 accumulation length (its truncation
-        // error grows with the accumulator magnitude x the number of steps).
+        // 2^flush_log2 visited column tiles (a "sub-unit"), then drained by the
+        // drain warps; two O buffers alternate so the drain overlaps the next
+        // sub-unit.  This bounds the tensor core's fp32 accumulation length (its
+        // truncation error grows with the accumulator magnitude x the number of steps).
         const int fmask = (1 << args.flush_log2) - 1;
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-            const int sp = u / args.n_row_tiles;
+            const int sp = u / args.n_row_tiles, rt = u % args.n_row_tiles;
             const int ct0 = static_cast<int>((long long)sp * args.n_col_tiles / args.splits);
             const int ct1 = static_cast<int>((long long)(sp + 1) * args.n_col_tiles / args.splits);
+            TileWalk wk = walk_of(rt, ct1);
+            int ct = wk.first(ct0);
+            if (ct >= ct1) continue;
+            const int len = (kScore && !g1) ? wk.count(ct0) : 0;   // GEMM2: sub-unit boundaries
             const int ab = it_a & 1;
             if (g1) {
                 ptx::mbar_wait(&a_full[ab], (it_a >> 1) & 1);
                 ptx::tc_fence_after();
             }
-            for (int ct = ct0; ct < ct1; ++ct) {
+            for (int rel = 0; ct < ct1; ct = wk.next(), ++rel) {
                 const uint32_t st = it_b % kStages;
                 const uint32_t sb = it_s % Cfg::kSBuf;
                 const uint32_t ph = (it_s / Cfg::kSBuf) & 1;
                 if (g1) {
+                    if (Cfg::kIssuers > 1 && it_s % Cfg::kIssuers != my_turn) {   // another issuer's tile
+                        ++it_b;
+                        ++it_s;
+                        continue;
+                    }
                     FKDE_TRACE(0, it_s);
                     ptx::mbar_wait(&b_full[st], (it_b / kStages) & 1);
                     FKDE_TRACE(1, it_s);
-                    // KDE: the epilogue frees S after loading it.  SCORE: GEMM2 of
-                    // the tile that last used this buffer has finished reading P.
+                    // KDE / check: the epilogue frees S after loading it.  SCORE: GEMM2
+                    // of the tile that last used this buffer has finished reading P.
                     if constexpr (!kScore) ptx::mbar_wait(&s_empty[sb], ph ^ 1);
                     else ptx::mbar_wait(&s_free[sb], ph ^ 1);
                     FKDE_TRACE(5, it_s);
@@ -362,8 +437,11 @@ pairwise_tc_kernel(PairArgs args) {
                         // K-step order: the half-norm chunk first, then y_hi.y_hi, so the
                         // large terms cancel inside one fused MMA step before the small
                         // hi/lo cross terms are added.
+                        // (the check pass needs only the norms and y_hi . y_hi: the hi/lo
+                        // cross terms are bounded by 2^-9 max|y|^2/2 and covered by the
+                        // margin of its threshold -- half the MMAs)
 #pragma unroll
-                        for (int kk = 0; kk < 4; ++kk) {
+                        for (int kk = 0; kk < (kCheck ? 2 : 4); ++kk) {
                             const int k = kk == 0 ? 1 : (kk == 1 ? 0 : kk);  // 1 (norms), 0, 2, 3
                             ptx::umma_f16(tmem_base + sb * Cfg::kNCol, da0 + ((k * 32) >> 4),
                                           db0 + ((k * 32) >> 4), idesc1, kk > 0 ? 1u : 0u);
@@ -374,57 +452,33 @@ pairwise_tc_kernel(PairArgs args) {
                     __syncwarp();
                     FKDE_TRACE(4, it_s);
                 } else if constexpr (kScore) {
-                    const int rel = ct - ct0;
                     const bool first = (rel & fmask) == 0;
-                    const bool last = (rel & fmask) == fmask || ct == ct1 - 1;
-                    const uint32_t ob = it_u % Cfg::kOBuf;
+                    const bool last = (rel & fmask) == fmask || rel == len - 1;
+                    const uint32_t ob = it_u & 1;
                     FKDE_TRACE(2, it_s);
                     ptx::mbar_wait(&p_full[sb], ph);
                     FKDE_TRACE(3, it_s);
-                    if (first) {
-                        ptx::mbar_wait(&o_empty[ob], ((it_u / Cfg::kOBuf) & 1) ^ 1);
-                        o_started = false;
-                    }
-                    // every lane quadrant's P of this tile is zero: no MMA needed,
-                    // unless the sub-unit would otherwise end with O never written
-                    const bool all_zero = *reinterpret_cast<volatile uint32_t*>(&skipf[sb]) == 0x01010101u;
-                    const bool issue = !all_zero;
+                    if (first) ptx::mbar_wait(&o_empty[ob], ((it_u >> 1) & 1) ^ 1);
                     ptx::tc_fence_after();
                     if (ptx::elect_one()) {
-                        if (issue) {
-                            const uint64_t db0 = descBmn + ((st * Cfg::kBStride) >> 4);
-                            const uint32_t ta0 = tmem_base + sb * Cfg::kNCol;
-                            const uint32_t to = tmem_base + Cfg::kTmemO + ob * Cfg::kOStride;
+                        const uint64_t db0 = descBmn + ((st * Cfg::kBStride) >> 4);
+                        const uint32_t ta0 = tmem_base + sb * Cfg::kNCol;
+                        const uint32_t to = tmem_base + Cfg::kTmemO + ob * 64;
 #pragma unroll
-                            for (int k = 0; k < Cfg::kNCol / 16; ++k) {
+                        for (int k = 0; k < Cfg::kNCol / 16; ++k) {
 #pragma unroll
-                                for (int part = 0; part < (FKDE_G2_LO_N > 0 ? 2 : 1); ++part) {
-                                    // one N=48 MMA per K step: columns 0-15 T_hi, 16 S, 32-47 T_lo
-                                    // (separate: P_lo into O_lo at +48, columns 0-15 T, 16 S)
-                                    const uint32_t dst = (FKDE_LO_SEPARATE && part) ? to + 48 : to;
-                                    const bool zero = FKDE_LO_SEPARATE ? (!o_started && k == 0)
-                                                                       : (!o_started && part == 0 && k == 0);
-                                    ptx::umma_f16_ts(dst, ta0 + (k >> 1) * 32 + part * 16 + (k & 1) * 8,
-                                                     db0 + ((k * 2048) >> 4), part ? idesc2_lo : idesc2,
-                                                     zero ? 0u : 1u);
-                                }
+                            for (int part = 0; part < 2; ++part) {
+                                // one N=48 MMA per K step: columns 0-15 T_hi, 16 S, 32-47 T_lo
+                                ptx::umma_f16_ts(to, ta0 + (k >> 1) * 32 + part * 16 + (k & 1) * 8,
+                                                 db0 + ((k * 2048) >> 4), part ? idesc2_lo : idesc2,
+                                                 (first && part == 0 && k == 0) ? 0u : 1u);
                             }
-                        } else {
-                            ++n_g2skip;
                         }
                         ptx::umma_commit(&b_empty[st]);
                         ptx::umma_commit(&s_free[sb]);
-                        if (last) {
-                            if (o_started || issue) {
-                                ptx::umma_commit(&o_full[ob]);
-                            } else {   // nothing written to O in this sub-unit
-                                o_zero[ob] = 0x01010101u;
-                                ptx::mbar_arrive(&o_full[ob]);
-                            }
-                        }
+                        if (last) ptx::umma_commit(&o_full[ob]);
                     }
                     __syncwarp();
-                    o_started = o_started || issue;
                     FKDE_TRACE(5, it_s);
                     if (last) ++it_u;
                 }
@@ -437,17 +491,16 @@ pairwise_tc_kernel(PairArgs args) {
             }
             ++it_a;
         }
-        if (kScore && !g1 && args.stats && n_g2skip && ptx::elect_one()) atomicAdd(&args.stats[2], n_g2skip);
     }
     } else if (warp < Cfg::kEpi0) {
         if constexpr (kScore) {
             // ===================== O drain warps (score) =====================
             // Warp 4+q drains lane quadrant q of every O sub-unit (2^flush_log2
-            // column tiles) in order: wait for GEMM2's commit, read T_hi, S, T_lo,
-            // release the buffer, fold into float-float sums (2Sum, ~48-bit
-            // significand) and write one fp64 partial per (split, row) at the
-            // unit's end.  Keeping this off the epilogue warps leaves them a
-            // uniform ld -> ex2 -> st stream with no waits on GEMM2.
+            // visited column tiles) in order: wait for GEMM2's commit, read T_hi,
+            // S, T_lo, release the buffer, fold into float-float sums (2Sum,
+            // ~48-bit significand) and write one fp64 partial per (split, row) at
+            // the unit's end (zero for a unit that visits no tile).  Keeping this
+            // off the epilogue warps leaves them a uniform ld -> ex2 -> st stream.
             const int q = warp & 3;
             const int r = q * 32 + lane;
             const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
@@ -458,53 +511,57 @@ pairwise_tc_kernel(PairArgs args) {
                 const int sp = u / args.n_row_tiles, rt = u % args.n_row_tiles;
                 const int ct0 = static_cast<int>((long long)sp * args.n_col_tiles / args.splits);
                 const int ct1 = static_cast<int>((long long)(sp + 1) * args.n_col_tiles / args.splits);
-                const int nsub = (ct1 - ct0 + fmask) >> lf;
+                TileWalk wk = walk_of(rt, ct1);
+                const int len = wk.count(ct0);
+                const int nsub = (len + fmask) >> lf;
                 float ahi[kMaxDim + 1], alo[kMaxDim + 1];
 #pragma unroll
                 for (int c = 0; c <= kMaxDim; ++c) ahi[c] = alo[c] = 0.f;
+                // centred GEMM2 (B2): one sub-unit per visited tile, whose centroid
+                // (scaled like the operands, 2^-e, exact) is added back as c_J * S
+                const bool centred = args.opB2 != nullptr;
+                // lane c < 16 holds coordinate c of the current tile's centroid; the
+                // next visited tile's is loaded one tile ahead (an L2 round trip per
+                // tile on the drain's critical path throttled GEMM2 through o_empty)
+                int cct = centred ? wk.first(ct0) : 0;
+                float cl = 0.f, cl_next = 0.f;
+                if (centred && lane < kMaxDim && cct < ct1) cl_next = __ldg(args.cenB + (size_t)cct * kMaxDim + lane);
 #pragma unroll 1
                 for (int j = 0; j < nsub; ++j, ++it_u) {
                     const uint32_t g = it_u;
-                    const uint32_t gb = g % Cfg::kOBuf, gph = (g / Cfg::kOBuf) & 1;
-                    const uint32_t to = lane_addr + Cfg::kTmemO + gb * Cfg::kOStride;
+                    const uint32_t to = lane_addr + Cfg::kTmemO + (g & 1) * 64;
                     uint32_t od[16], ol[16], os_;
-#if FKDE_LO_SEPARATE
-                    uint32_t oq[16], oqs;
-#endif
+                    if (centred) {
+                        cl = cl_next;
+                        cct = wk.next();
+                        cl_next = (lane < kMaxDim && cct < ct1) ? __ldg(args.cenB + (size_t)cct * kMaxDim + lane) : 0.f;
+                    }
                     FKDE_TRACE(4, g);
-                    ptx::mbar_wait(&o_full[gb], gph);
+                    ptx::mbar_wait(&o_full[g & 1], (g >> 1) & 1);
                     FKDE_TRACE(5, g);
                     ptx::tc_fence_after();
-                    volatile uint8_t* oz = reinterpret_cast<volatile uint8_t*>(&o_zero[gb]) + q;
-                    if (*oz) {   // every tile of this sub-unit was skipped: O = 0
-                        __syncwarp();
-                        if (lane == 0) {
-                            *oz = 0;
-                            ptx::mbar_arrive(&o_empty[gb]);
-                        }
-                        continue;
-                    }
                     ptx::tmem_ld16(to, od);
                     ptx::tmem_ld1(to + 16, os_);
                     ptx::tmem_ld16(to + 32, ol);
-#if FKDE_LO_SEPARATE
-                    ptx::tmem_ld16(to + 48, oq);
-                    ptx::tmem_ld1(to + 64, oqs);
-#endif
                     ptx::tmem_ld_wait();
                     ptx::tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(&o_empty[gb]);
+                    if (lane == 0) ptx::mbar_arrive(&o_empty[g & 1]);
+                    if (centred) {
+                        const float cls = ldexpf(cl, -args.sc->e);   // scaled like the operands (exact)
+#pragma unroll
+                        for (int c = 0; c < kMaxDim; ++c) {   // T = sum phi v + c_J S
+                            const float cc = __shfl_sync(0xffffffffu, cls, c);
+                            const float x = fmaf(cc, __uint_as_float(os_),
+                                                 __uint_as_float(od[c]) + __uint_as_float(ol[c]));
+                            od[c] = __float_as_uint(x);
+                            ol[c] = 0u;
+                        }
+                    }
 #pragma unroll
                     for (int c = 0; c <= kMaxDim; ++c) {
-#if FKDE_LO_SEPARATE
-                        const float x = c < kMaxDim ? __uint_as_float(od[c]) + (__uint_as_float(ol[c]) +
-                                                                                __uint_as_float(oq[c]))
-                                                    : __uint_as_float(os_) + __uint_as_float(oqs);
-#else
                         const float x = c < kMaxDim ? __uint_as_float(od[c]) + __uint_as_float(ol[c])
                                                     : __uint_as_float(os_);
-#endif
                         const float s2 = ahi[c] + x;           // 2Sum(ahi, x)
                         const float bb = s2 - ahi[c];
                         const float e = (ahi[c] - (s2 - bb)) + (x - bb);
@@ -524,41 +581,42 @@ pairwise_tc_kernel(PairArgs args) {
     } else if (warp < Cfg::kEpiEnd) {
         if constexpr (kScore) ptx::setmaxnreg_inc<Cfg::kEpiRegs>();
         // ===================== epilogue warps =====================
-        // Warp w reads TMEM lane quadrant w%4 and handles every kNP-th column
-        // tile (phase par = (w-kEpi0)/4), all its columns, in 32-column chunks.
-        // The kNP warps sharing an SM sub-partition (and a lane quadrant)
-        // therefore work on different tiles, out of phase: while one waits for
-        // its next S tile (GEMM1 of tile t + kNP can only start once GEMM2 of
-        // tile t has released the buffer) the others keep the MUFU pipe busy.
-        // The own-tile loop carries only a few integer ops of bookkeeping.
+        // Warp w reads TMEM lane quadrant w%4 and handles every kNP-th visited
+        // column tile (phase par = (w-kEpi0)/4), all its columns, in 32-column
+        // chunks.  The kNP warps sharing an SM sub-partition (and a lane
+        // quadrant) therefore work on different tiles, out of phase: while one
+        // waits for its next S tile (GEMM1 of tile t + kNP can only start once
+        // GEMM2 of tile t has released the buffer) the others keep the MUFU pipe
+        // busy.  The own-tile loop carries only a few integer ops of bookkeeping.
         constexpr int NP = Cfg::kNP;
         const int q = warp & 3;                      // TMEM lane quadrant
         const int par = (warp - Cfg::kEpi0) >> 2;    // tile phase handled by this warp
         const int r = q * 32 + lane;                 // row within the 128-row tile
         const float dsc = args.sc->dscale;
+        // check pass: S lacks the hi/lo cross terms y_hi.y_lo + y_lo.y_hi, each bounded
+        // by 2^-11 |y_i| |y_j| <= 2^-11 max|y|^2, so their sum by 2^-9 max|y|^2/2 (the
+        // bound prep_stats stored, log2 units): a tile is skippable when even the
+        // bound-raised maximum is below kSkipLog2
+        const float skip_below =
+            kSkipLog2 - (ldexpf(__uint_as_float(args.sc->max_half_norm_bits), -9) + 0.0625f);
         const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
-        uint32_t it_s = 0;                           // global tile counter (all phases)
-        unsigned long long n_checked = 0, n_skipped = 0;   // tile-skip statistics (lane-uniform)
+        uint32_t it_s = 0;                           // global visited-tile counter (all phases)
+        unsigned long long n_checked = 0;            // check statistics (quadrant 0 counts)
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
             const int sp = u / args.n_row_tiles, rt = u % args.n_row_tiles;
             const int ct0 = static_cast<int>((long long)sp * args.n_col_tiles / args.splits);
             const int ct1 = static_cast<int>((long long)(sp + 1) * args.n_col_tiles / args.splits);
-            const int len = ct1 - ct0;
+            TileWalk wk = walk_of(rt, ct1);
             float2 acc2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
             float2 accl2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-            // this warp's first own tile and its S buffer / phase
-            int rel = par - static_cast<int>(it_s % NP);
-            if (rel < 0) rel += NP;
-            const uint32_t sidx = it_s + rel;
-            uint32_t sb = sidx % Cfg::kSBuf, ph = (sidx / Cfg::kSBuf) & 1;
             // score: global index of this lane's row minus the unit's first
-            // column; the row's self pair sits at column jd - rel * kNCol of
-            // tile rel (masked where that lies in [0, kNCol))
+            // column; the row's self pair sits at column jd0 - (ct - ct0) * kNCol
+            // of column tile ct (masked where that lies in [0, kNCol))
             const long long jd0 = args.diag_row0 >= 0
                                       ? args.diag_row0 + (long long)rt * kTileRows + r - (long long)ct0 * Cfg::kNCol
                                       : -(1ll << 40);
-            // tiles of this unit the row tile's diagonal crosses: [drel_lo, drel_hi]
-            // (floor division; empty when the pass has no diagonal)
+            // column tiles (relative to ct0) the row tile's diagonal crosses:
+            // [drel_lo, drel_hi] (floor division; empty when the pass has no diagonal)
             const long long drow0 = jd0 - r;
             auto fdiv = [](long long a) {
                 return a >= 0 ? a / Cfg::kNCol : -((-a + Cfg::kNCol - 1) / Cfg::kNCol);
@@ -566,14 +624,15 @@ pairwise_tc_kernel(PairArgs args) {
             const bool has_diag = args.diag_row0 >= 0;
             const int drel_lo = has_diag ? static_cast<int>(fdiv(drow0)) : INT_MAX;
             const int drel_hi = has_diag ? static_cast<int>(fdiv(drow0 + kTileRows - 1)) : -1;
-            // tile skipping (score): this unit's row-tile centroid, one coordinate per
-            // lane (the column tile's centroid arrives with its B stage)
-            float ca_l = 0.f;
-            if (kScore && args.cenA && lane < kMaxDim) ca_l = __ldg(args.cenA + (size_t)rt * kMaxDim + lane);
-            for (; rel < len; rel += NP) {
-                FKDE_TRACE(0, it_s + rel);
+            uint32_t k = 0;   // visited tiles of this unit so far
+            for (int ct = wk.first(ct0); ct < ct1; ct = wk.next(), ++k) {
+                const uint32_t sidx = it_s + k;
+                if (static_cast<int>(sidx % NP) != par) continue;   // another phase's tile
+                const uint32_t sb = sidx % Cfg::kSBuf, ph = (sidx / Cfg::kSBuf) & 1;
+                const int rel = ct - ct0;
+                FKDE_TRACE(0, sidx);
                 ptx::mbar_wait(&s_full[sb], ph);
-                FKDE_TRACE(1, it_s + rel);
+                FKDE_TRACE(1, sidx);
                 ptx::tc_fence_after();
                 const uint32_t ts = lane_addr + sb * Cfg::kNCol;
                 const float2 dsc2 = make_float2(dsc, dsc);
@@ -583,62 +642,13 @@ pairwise_tc_kernel(PairArgs args) {
                                           : -1;   // this row's diagonal column (if in this tile)
                     const float2 neg1 = make_float2(-1.f, -1.f);
                     const float2 vk2 = make_float2(8193.f, 8193.f);   // 2^13 + 1
-                    // tile skipping: predicted from the tile centroids (warp-uniform),
-                    // then checked exactly on this quadrant's 32 rows
-                    bool skip = false;
-                    if (args.cenA) {
-                        // centroid half-distance^2: lane c < 16 holds coordinate c.  The
-                        // column centroid sits in this tile's B stage (that phase of
-                        // b_full is complete: GEMM1 waited on it, and the stage cannot
-                        // be refilled before this tile's P is consumed)
-                        const uint32_t gt = it_s + static_cast<uint32_t>(rel);
-                        const uint32_t bst = gt % kStages;
-                        ptx::mbar_wait(&b_full[bst], (gt / kStages) & 1);
-                        const float cb = lane < kMaxDim
-                            ? reinterpret_cast<const float*>(smB + bst * Cfg::kBStride + Cfg::kColBytes)[lane]
-                            : 0.f;
-                        const float df = ca_l - cb;
-                        float dd = df * df;
-#pragma unroll
-                        for (int o = 16; o > 0; o >>= 1) dd += __shfl_xor_sync(0xffffffffu, dd, o);
-                        if (0.5f * dd > args.skip_pred) {
-                            float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
+                    (void)vk2;
 #pragma unroll 1
-                            for (int ch = 0; ch < Cfg::kNCol / 32; ++ch) {
-                                uint32_t v[32];
-                                ptx::tmem_ld32(ts + ch * 32, v);
-                                ptx::tmem_ld_wait();
-#pragma unroll
-                                for (int c = 0; c < 32; c += 4) {
-                                    m0 = fmaxf(m0, __uint_as_float(v[c]));
-                                    m1 = fmaxf(m1, __uint_as_float(v[c + 1]));
-                                    m2 = fmaxf(m2, __uint_as_float(v[c + 2]));
-                                    m3 = fmaxf(m3, __uint_as_float(v[c + 3]));
-                                }
-                            }
-                            const float mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
-                            skip = __all_sync(0xffffffffu, mx * dsc < kSkipLog2);
-                            ++n_checked;
-                            n_skipped += skip ? 1u : 0u;
-                        }
-                    }
-                    if (skip) {   // P = 0 for this quadrant (GEMM2 may still read it)
-                        uint32_t z[16];
-#pragma unroll
-                        for (int w = 0; w < 16; ++w) z[w] = 0u;
-#pragma unroll
-                        for (int ch = 0; ch < Cfg::kNCol / 32; ++ch) {
-                            ptx::tmem_st16(ts + ch * 32, z);
-                            ptx::tmem_st16(ts + ch * 32 + 16, z);
-                        }
-                    }
-                    if (lane == 0) reinterpret_cast<volatile uint8_t*>(&skipf[sb])[q] = skip ? 1 : 0;
-#pragma unroll 1
-                    for (int ch = 0; ch < (skip ? 0 : Cfg::kNCol / 32); ++ch) {
+                    for (int ch = 0; ch < Cfg::kNCol / 32; ++ch) {
                         uint32_t v[32];
                         ptx::tmem_ld32(ts + ch * 32, v);
                         ptx::tmem_ld_wait();
-                        if (ch == 0) FKDE_TRACE(6, it_s + rel);
+                        if (ch == 0) FKDE_TRACE(6, sidx);
                         if (__any_sync(0xffffffffu, jdiag >= 0)) {
 #pragma unroll
                             for (int c = 0; c < 32; ++c)    // -inf -> phi = 0
@@ -676,12 +686,44 @@ pairwise_tc_kernel(PairArgs args) {
                         ptx::tmem_st16(ts + ch * 32, hi_w);
                         ptx::tmem_st16(ts + ch * 32 + 16, lo_w);
                     }
-                    FKDE_TRACE(7, it_s + rel);
+                    FKDE_TRACE(7, sidx);
                     ptx::tmem_st_wait();
                     ptx::tc_fence_before();
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(&p_full[sb]);
-                    FKDE_TRACE(2, it_s + rel);
+                    FKDE_TRACE(2, sidx);
+                } else if constexpr (kCheck) {
+                    // exact max of log2 phi' over this quadrant's 32 rows x 96 columns:
+                    // the three loads are in flight together, the buffer is released
+                    // as soon as they have landed
+                    uint32_t v0[32], v1[32], v2[32];
+                    ptx::tmem_ld32(ts, v0);
+                    ptx::tmem_ld32(ts + 32, v1);
+                    ptx::tmem_ld32(ts + 64, v2);
+                    ptx::tmem_ld_wait();
+                    FKDE_TRACE(6, sidx);
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&s_empty[sb]);
+                    float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
+#pragma unroll
+                    for (int c = 0; c < 32; c += 2) {
+                        m0 = fmaxf(m0, __uint_as_float(v0[c]));
+                        m1 = fmaxf(m1, __uint_as_float(v0[c + 1]));
+                        m2 = fmaxf(m2, __uint_as_float(v1[c]));
+                        m3 = fmaxf(m3, __uint_as_float(v1[c + 1]));
+                        m0 = fmaxf(m0, __uint_as_float(v2[c]));
+                        m1 = fmaxf(m1, __uint_as_float(v2[c + 1]));
+                    }
+                    const float mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
+                    const bool keep = __any_sync(0xffffffffu, !(mx * dsc < skip_below));
+                    if (lane == 0) {
+                        if (keep)   // some pair of this quadrant contributes: not skippable
+                            atomicAnd(args.skip_mask + (size_t)rt * args.mask_words + (ct >> 5),
+                                      ~(1u << (ct & 31)));
+                        if (q == 0) ++n_checked;
+                    }
+                    FKDE_TRACE(7, sidx);
                 } else {
                     // (phi <= 1 up to the expansion's rounding: no clamp needed)
 #pragma unroll 1
@@ -705,14 +747,8 @@ pairwise_tc_kernel(PairArgs args) {
                         }
                     }
                 }
-                // next own tile: buffer index advances by NP (mod kSBuf)
-                sb += NP;
-                if (sb >= Cfg::kSBuf) {
-                    sb -= Cfg::kSBuf;
-                    ph ^= 1;
-                }
             }
-            if constexpr (!kScore) {
+            if constexpr (!kScore && !kCheck) {
                 // the kNP phases hold disjoint column subsets of this unit
                 const size_t row = static_cast<size_t>(rt) * kTileRows + r;
                 const size_t idx = static_cast<size_t>(sp * NP + par) * args.rows_pad + row;
@@ -720,12 +756,10 @@ pairwise_tc_kernel(PairArgs args) {
                 if constexpr (MODE == kModeLaplace)
                     args.part1[idx] = (accl2[0].x + accl2[0].y) + (accl2[1].x + accl2[1].y);
             }
-            it_s += len;
+            it_s += k;
         }
-        if (kScore && args.stats && lane == 0 && n_checked) {
+        if (kCheck && args.stats && lane == 0 && q == 0 && n_checked)
             atomicAdd(&args.stats[0], n_checked);
-            atomicAdd(&args.stats[1], n_skipped);
-        }
     }
 
     ptx::tc_fence_before();

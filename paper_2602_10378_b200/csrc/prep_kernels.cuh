@@ -196,6 +196,8 @@ struct PackArgs {
     uint8_t* risk;           // A rows (optional): 1 where |y|^2/2 > risk_half_norm (the
                              // expanded norms' fp32 rounding is too coarse: direct_rows)
     double risk_half_norm;
+    const float* cen;        // format 2: per column-tile centroids (log2 units, unscaled)
+    int cen_tile;            // format 2: points per column tile
 };
 
 __device__ __forceinline__ uint32_t pack_h2(__half a, __half b) {
@@ -223,7 +225,51 @@ __global__ void pack_two(PackArgs a, PackArgs b, unsigned int blocks_a) {
     }
 }
 
+// format 2 (B2, score pass on the spatial order): the column operand of GEMM2 only,
+// y - c_J with c_J the row's column-tile centroid, so the tensor core accumulates
+// sum_j phi_ij (y_j - c_J) -- values of the tile's size, not of |y| -- and the
+// drain adds c_J * sum_j phi_ij in float-float (layout.cuh)
+__device__ __forceinline__ void pack_row_centred(const PackArgs& a, size_t i) {
+    uint32_t ch[8][4];
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+#pragma unroll
+        for (int w = 0; w < 4; ++w) ch[c][w] = 0u;
+    if (i < a.rows) {
+        const int e = a.sc->e;
+        const double ys = ldexp(a.k, -e);
+        const float* cj = a.cen + (i / a.cen_tile) * kMaxDim;
+        __half vh[kMaxDim], vl[kMaxDim];
+#pragma unroll
+        for (int c = 0; c < kMaxDim; ++c) {
+            double v = 0.0;
+            if (c < a.d)
+                v = (a.x[i * a.d + c] - a.sc->mu[c]) * ys - ldexp(static_cast<double>(cj[c]), -e);
+            vh[c] = __double2half(v);
+            vl[c] = __double2half(v - static_cast<double>(__half2float(vh[c])));
+        }
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+                const int k0 = c * 8 + 2 * w;
+                ch[c][w] = pack_h2(vh[k0], vh[k0 + 1]);
+                ch[4 + c][w] = pack_h2(vl[k0], vl[k0 + 1]);
+            }
+        ch[2][0] = pack_h2(__float2half(1.f), __float2half(0.f));   // column 16: the ones (S)
+    }
+    const size_t tile = i / kTileRows;
+    const int r = static_cast<int>(i % kTileRows);
+    uint4* base = a.out + tile * (kTileBytes / 16) + r * 8;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) base[c ^ (r & 7)] = make_uint4(ch[c][0], ch[c][1], ch[c][2], ch[c][3]);
+}
+
 __device__ __forceinline__ void pack_row(const PackArgs& a, size_t i) {
+    if (a.format == 2) {
+        pack_row_centred(a, i);
+        return;
+    }
     __half yh[kMaxDim], yl[kMaxDim];
     __half n1 = __float2half(0.f), n2 = n1, n3 = n1;
     const __half one = __float2half(1.f), zero = __float2half(0.f);

@@ -211,4 +211,35 @@ __global__ void __launch_bounds__(128) tile_centroids(const double* __restrict__
     }
 }
 
+// Skip predictor: one thread per (row tile, 32 column tiles): bit ct of the
+// row's mask words = centroid half-distance^2 > thresh (log2 units).  The bit
+// only selects the tile pair for the exact check (kModeCheck); pred and skip
+// masks start equal, the check clears skip bits of tiles that contribute.
+__global__ void tile_predict(const float* __restrict__ cenA, int row_tiles,
+                             const float* __restrict__ cenB, int col_tiles, int words, float thresh,
+                             uint32_t* __restrict__ pred, uint32_t* __restrict__ skip) {
+    pdl_launch_dependents();
+    pdl_wait();
+    const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (t >= static_cast<size_t>(row_tiles) * words) return;
+    const int rt = static_cast<int>(t / words), w = static_cast<int>(t % words);
+    float a[kMaxDim];
+#pragma unroll
+    for (int c = 0; c < kMaxDim; ++c) a[c] = cenA[(size_t)rt * kMaxDim + c];
+    uint32_t bits = 0;
+    for (int b = 0; b < 32; ++b) {
+        const int ct = w * 32 + b;
+        if (ct >= col_tiles) break;
+        float dd = 0.f;
+#pragma unroll
+        for (int c = 0; c < kMaxDim; ++c) {
+            const float df = a[c] - cenB[(size_t)ct * kMaxDim + c];
+            dd = fmaf(df, df, dd);
+        }
+        if (0.5f * dd > thresh) bits |= 1u << b;
+    }
+    pred[t] = bits;
+    skip[t] = bits;
+}
+
 }  // namespace fkde_b200

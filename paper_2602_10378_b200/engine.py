@@ -112,8 +112,8 @@ class Context:
         """Tile skipping of the last score pass (fkde_gpu_last_skip_stats)."""
         b = (ctypes.c_uint64 * 4)()
         self._lib.fkde_gpu_last_skip_stats(self._h, b)
-        return {"quadrant_tiles_checked": int(b[0]), "quadrant_tiles_skipped": int(b[1]),
-                "gemm2_tiles_skipped": int(b[2]), "spatial_order": bool(b[3])}
+        return {"tiles_checked": int(b[0]), "tiles_skipped": int(b[1]),
+                "tiles_total": int(b[2]), "spatial_order": bool(b[3])}
 
     def workspace_bytes(self) -> int:
         b = ctypes.c_size_t(0)
