@@ -194,7 +194,7 @@ struct Device {
     DevBuf qmax;                 // scale_two per-block maxima
     // spatial order of the score pass (spatial_order.cuh): sorted points, permutation,
     // keys, CUB scratch, axes, tile centroids, skip statistics, un-permuted outputs
-    DevBuf Xs, perm, keys, cubtmp, ordsc, cenA, cenB, skipstats, unperm0, unperm1, pmask, smask;
+    DevBuf Xs, perm, keys, cubtmp, ordsc, cenA, cenB, boxA, boxB, skipstats, unperm0, unperm1, pmask, smask;
     size_t mask_bytes = 0;       // skip mask of the last score pass (0: none)
     uint64_t tiles_total = 0;    // tile pairs of the last score pass
     bool ordered = false;        // last score pass ran on the spatial order
@@ -577,8 +577,9 @@ Status score_program(Device& D, const Options& o, const Job& J, const double* dX
     a.sc = sc;
     a.dpart0 = D.part0.as<double>();
     a.dpart1 = D.part1.as<double>();
-    // drain interval: the option, or by default ~256 columns (the accumulation
-    // length that keeps the tensor core's truncation error near 2e-4)
+    // drain interval: the option, or by default every 2 tiles (~192 columns: the
+    // accumulation length that keeps the tensor core's truncation error near 2e-4,
+    // DESIGN §4); the spatial order drains every tile (below)
     const int flush = o.flush_tiles > 0 ? o.flush_tiles
                                         : std::max<int>(1, 256 / static_cast<int>(kScoreNCol));
     a.flush_log2 = 0;
@@ -594,10 +595,14 @@ Status score_program(Device& D, const Options& o, const Job& J, const double* dX
         // column tile (B2, layout.cuh) with a drain after every visited tile
         STATUS_TRY(ensure(D.cenA, rt * kMaxDim * sizeof(float)));
         STATUS_TRY(ensure(D.cenB, ct * kMaxDim * sizeof(float)));
-        tile_centroids<<<static_cast<unsigned>(rt), 128, 0, D.stream>>>(
-            dX + sh.begin * d, sh.rows, d, sc, ks, kTileRows, D.cenA.as<float>());
-        tile_centroids<<<static_cast<unsigned>(ct), 128, 0, D.stream>>>(
-            dX, n, d, sc, ks, static_cast<int>(kScoreNCol), D.cenB.as<float>());
+        STATUS_TRY(ensure(D.boxA, rt * kBoxFloats * sizeof(float)));
+        STATUS_TRY(ensure(D.boxB, ct * kBoxFloats * sizeof(float)));
+        tile_summary<<<static_cast<unsigned>(rt), 128, 0, D.stream>>>(
+            dX + sh.begin * d, sh.rows, d, sc, D.ordsc.as<OrderScalars>(), ks, kTileRows,
+            D.cenA.as<float>(), D.boxA.as<float>());
+        tile_summary<<<static_cast<unsigned>(ct), 128, 0, D.stream>>>(
+            dX, n, d, sc, D.ordsc.as<OrderScalars>(), ks, static_cast<int>(kScoreNCol),
+            D.cenB.as<float>(), D.boxB.as<float>());
         size_t b2_pad = 0;
         PackArgs p2;
         STATUS_TRY(pack_args(D, dX, n, d, 2, true, ks, sc, D.opB2, &b2_pad, &p2, col_align));
@@ -623,9 +628,13 @@ Status score_program(Device& D, const Options& o, const Job& J, const double* dX
             const char* e = std::getenv("FKDE_SKIP_PRED");
             return e && *e ? static_cast<float>(std::atof(e)) : kSkipPredict;
         }();
+        // proven-zero threshold on the lower bound of r^2/2 (log2 units): every pair
+        // then has log2 phi' = 15 - r^2/2 < kSkipLog2 - 0.5 (float boxes' margin)
+        const float proven = 15.0f - kSkipLog2 + 0.5f;
         tile_predict<<<grid1(rt * words, 128), 128, 0, D.stream>>>(
-            D.cenA.as<float>(), static_cast<int>(rt), D.cenB.as<float>(), static_cast<int>(ct), words,
-            pred, D.pmask.as<uint32_t>(), D.smask.as<uint32_t>());
+            D.cenA.as<float>(), D.boxA.as<float>(), static_cast<int>(rt), D.cenB.as<float>(),
+            D.boxB.as<float>(), static_cast<int>(ct), words, pred, proven, D.pmask.as<uint32_t>(),
+            D.smask.as<uint32_t>());
         D.launches += 1;
         CUDA_TRY(cudaGetLastError());
         PairArgs c = a;
@@ -1186,7 +1195,7 @@ void fkde_gpu_destroy(fkde_gpu_ctx* ctx) {
                           &D.xsd,  &D.out,   &D.aux0, &D.aux1, &D.colpart, &D.scal,
                           &D.err,  &D.flags, &D.risk, &D.dpart, &D.ddone,
                           &D.Xs,   &D.perm,  &D.keys, &D.cubtmp, &D.ordsc, &D.cenA,
-                          &D.cenB, &D.skipstats, &D.unperm0, &D.unperm1, &D.pdone, &D.qmax, &D.pmask, &D.smask, &D.opB2};
+                          &D.cenB, &D.skipstats, &D.unperm0, &D.unperm1, &D.pdone, &D.qmax, &D.pmask, &D.smask, &D.opB2, &D.boxA, &D.boxB};
         for (DevBuf* b : bufs)
             if (b->p) cudaFree(b->p);
         for (auto& e : D.ev)
@@ -1288,7 +1297,7 @@ int fkde_gpu_workspace_bytes(const fkde_gpu_ctx* ctx, size_t* bytes) {
                                 &D.xsd,  &D.out,   &D.aux0, &D.aux1, &D.colpart, &D.scal,
                                 &D.err,  &D.flags, &D.risk, &D.dpart, &D.ddone,
                                 &D.Xs,   &D.perm,  &D.keys, &D.cubtmp, &D.ordsc, &D.cenA,
-                                &D.cenB, &D.skipstats, &D.unperm0, &D.unperm1, &D.pdone, &D.qmax, &D.pmask, &D.smask, &D.opB2};
+                                &D.cenB, &D.skipstats, &D.unperm0, &D.unperm1, &D.pdone, &D.qmax, &D.pmask, &D.smask, &D.opB2, &D.boxA, &D.boxB};
         for (const DevBuf* b : bufs) total += b->bytes;
     }
     *bytes = total;

@@ -624,10 +624,22 @@ pairwise_tc_kernel(PairArgs args) {
             const bool has_diag = args.diag_row0 >= 0;
             const int drel_lo = has_diag ? static_cast<int>(fdiv(drow0)) : INT_MAX;
             const int drel_hi = has_diag ? static_cast<int>(fdiv(drow0 + kTileRows - 1)) : -1;
-            uint32_t k = 0;   // visited tiles of this unit so far
-            for (int ct = wk.first(ct0); ct < ct1; ct = wk.next(), ++k) {
+            // visited tiles of this unit so far (k) and the current one (ct).  Without
+            // a mask every tile is visited and the walk jumps straight from one own
+            // tile to the next (the KDE pass keeps its original bookkeeping cost);
+            // with a mask it steps through the visited tiles, skipping other phases'.
+            const bool dense = wk.row == nullptr;
+            uint32_t k = 0;
+            int ct = wk.first(ct0);
+            if (dense) {
+                int first_own = par - static_cast<int>(it_s % NP);
+                if (first_own < 0) first_own += NP;
+                k = static_cast<uint32_t>(first_own);
+                ct = ct0 + first_own;
+            }
+            for (; ct < ct1; ct = dense ? ct + NP : wk.next(), k += dense ? NP : 1) {
                 const uint32_t sidx = it_s + k;
-                if (static_cast<int>(sidx % NP) != par) continue;   // another phase's tile
+                if (!dense && static_cast<int>(sidx % NP) != par) continue;   // another phase's tile
                 const uint32_t sb = sidx % Cfg::kSBuf, ph = (sidx / Cfg::kSBuf) & 1;
                 const int rel = ct - ct0;
                 FKDE_TRACE(0, sidx);
@@ -756,7 +768,7 @@ pairwise_tc_kernel(PairArgs args) {
                 if constexpr (MODE == kModeLaplace)
                     args.part1[idx] = (accl2[0].x + accl2[0].y) + (accl2[1].x + accl2[1].y);
             }
-            it_s += k;
+            it_s += dense ? static_cast<uint32_t>(ct1 - ct0) : k;
         }
         if (kCheck && args.stats && lane == 0 && q == 0 && n_checked)
             atomicAdd(&args.stats[0], n_checked);

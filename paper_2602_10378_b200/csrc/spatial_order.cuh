@@ -18,7 +18,8 @@
 //   morton_keys     project, quantise to 10 bits per axis, interleave -> 30-bit key
 //   (cub::DeviceRadixSort::SortPairs: keys + original indices -> permutation)
 //   gather_rows / scatter_rows   X -> X[perm], and outputs back to input order
-//   tile_centroids  per-tile centroid in log2 units (the skip predictor's input)
+//   tile_summary    per-tile centroid + coordinate / principal-axis boxes (log2 units)
+//   tile_predict    proven-zero tile pairs (box bound) and the pairs to check exactly
 #pragma once
 #include <cstdint>
 
@@ -56,79 +57,85 @@ __global__ void __launch_bounds__(256) cov_stage1(const double* __restrict__ x, 
 }
 
 // ---- covariance -> top principal axes (one block of 256 threads) -----------------------
+// Subspace iteration Q <- orth(C Q) on the 16 x 16 covariance, one warp: lane r < 16
+// owns row r of C and of Q, dot products are warp reductions (a single thread
+// running Gram-Schmidt took ~120 us).  The top-3 eigengap of clustered data is
+// large; for unclustered data any basis of the top subspace orders equally well.
+__device__ __forceinline__ double warp_sum16(double v) {
+    for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
 __global__ void __launch_bounds__(256) order_axes(const double* __restrict__ part, int nparts,
                                                   int d, OrderScalars* __restrict__ os) {
     __shared__ double C[kMaxDim][kMaxDim];
-    __shared__ double Q[kMaxDim][kOrderAxes], Z[kMaxDim][kOrderAxes];
     const int t = threadIdx.x;
     {
         double s = 0.0;
         for (int p = 0; p < nparts; ++p) s += part[p * 256 + t];
         C[t >> 4][t & 15] = s;
     }
-    if (t < kMaxDim * kOrderAxes) {   // start from the coordinate axes of largest variance order
-        const int r = t / kOrderAxes, k = t % kOrderAxes;
-        Q[r][k] = (r == k) ? 1.0 : 0.0;
-    }
     __syncthreads();
-    // subspace (orthogonal) iteration: Q <- orth(C Q); the top-3 eigengap of
-    // clustered data is large, and for unclustered data any basis of the top
-    // subspace orders equally well
-    for (int it = 0; it < 48; ++it) {
-        if (t < kMaxDim * kOrderAxes) {
-            const int r = t / kOrderAxes, k = t % kOrderAxes;
-            double s = 0.0;
-            for (int c = 0; c < kMaxDim; ++c) s = fma(C[r][c], Q[c][k], s);
-            Z[r][k] = s;
+    if (t >= 32) return;
+    const int r = t & 15;   // lanes 16..31 mirror 0..15 (the reductions stay within halves)
+    double q[kOrderAxes];
+#pragma unroll
+    for (int k = 0; k < kOrderAxes; ++k) q[k] = (r == k) ? 1.0 : 0.0;
+    double crow[kMaxDim];
+#pragma unroll
+    for (int c = 0; c < kMaxDim; ++c) crow[c] = C[r][c];
+    for (int it = 0; it < 24; ++it) {
+        double z[kOrderAxes];
+#pragma unroll
+        for (int k = 0; k < kOrderAxes; ++k) {   // z = C q (row r)
+            double acc = 0.0;
+#pragma unroll
+            for (int c = 0; c < kMaxDim; ++c) acc = fma(crow[c], __shfl_sync(0xffffffffu, q[k], c), acc);
+            z[k] = acc;
         }
-        __syncthreads();
-        if (t == 0) {   // modified Gram-Schmidt (3 vectors of 16)
-            for (int k = 0; k < kOrderAxes; ++k) {
+#pragma unroll
+        for (int k = 0; k < kOrderAxes; ++k) {   // modified Gram-Schmidt
+#pragma unroll
+            for (int j = 0; j < k; ++j) {
+                const double dp = warp_sum16(z[k] * z[j]);
+                z[k] -= dp * z[j];
+            }
+            double nn = warp_sum16(z[k] * z[k]);
+            if (!(nn > 1e-300)) {   // degenerate (d < 3, zero-variance subspace): a coordinate axis
+                z[k] = (r == k) ? 1.0 : 0.0;
+#pragma unroll
                 for (int j = 0; j < k; ++j) {
-                    double dp = 0.0;
-                    for (int r = 0; r < kMaxDim; ++r) dp += Z[r][k] * Z[r][j];
-                    for (int r = 0; r < kMaxDim; ++r) Z[r][k] -= dp * Z[r][j];
+                    const double dp = warp_sum16(z[k] * z[j]);
+                    z[k] -= dp * z[j];
                 }
-                double nn = 0.0;
-                for (int r = 0; r < kMaxDim; ++r) nn += Z[r][k] * Z[r][k];
-                if (nn > 1e-300) {
-                    const double inv = 1.0 / sqrt(nn);
-                    for (int r = 0; r < kMaxDim; ++r) Z[r][k] *= inv;
-                } else {   // degenerate (d < 3 or a zero-variance subspace): a spare coordinate axis
-                    for (int r = 0; r < kMaxDim; ++r) Z[r][k] = (r == k) ? 1.0 : 0.0;
-                    for (int j = 0; j < k; ++j) {
-                        double dp = 0.0;
-                        for (int r = 0; r < kMaxDim; ++r) dp += Z[r][k] * Z[r][j];
-                        for (int r = 0; r < kMaxDim; ++r) Z[r][k] -= dp * Z[r][j];
-                    }
-                    nn = 0.0;
-                    for (int r = 0; r < kMaxDim; ++r) nn += Z[r][k] * Z[r][k];
-                    const double inv = nn > 1e-300 ? 1.0 / sqrt(nn) : 0.0;
-                    for (int r = 0; r < kMaxDim; ++r) Z[r][k] *= inv;
-                }
+                nn = warp_sum16(z[k] * z[k]);
+            }
+            z[k] *= nn > 1e-300 ? 1.0 / sqrt(nn) : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < kOrderAxes; ++k) q[k] = z[k];
+    }
+#pragma unroll
+    for (int k = 0; k < kOrderAxes; ++k) {
+        // deterministic sign: largest-magnitude component positive (ties: lowest index)
+        double best = fabs(q[k]);
+        int am = r;
+        for (int o = 8; o > 0; o >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const int oa = __shfl_xor_sync(0xffffffffu, am, o);
+            if (ob > best || (ob == best && oa < am)) {
+                best = ob;
+                am = oa;
             }
         }
-        __syncthreads();
-        if (t < kMaxDim * kOrderAxes) Q[t / kOrderAxes][t % kOrderAxes] = Z[t / kOrderAxes][t % kOrderAxes];
-        __syncthreads();
-    }
-    if (t < kOrderAxes) {
-        const int k = t;
-        // deterministic sign: largest-magnitude component positive
-        int am = 0;
-        for (int r = 1; r < kMaxDim; ++r)
-            if (fabs(Q[r][k]) > fabs(Q[am][k])) am = r;
-        const double sg = Q[am][k] < 0.0 ? -1.0 : 1.0;
-        double lam = 0.0;
-        for (int r = 0; r < kMaxDim; ++r) {
-            double cq = 0.0;
-            for (int c = 0; c < kMaxDim; ++c) cq += C[r][c] * Q[c][k];
-            lam += Q[r][k] * cq;
-        }
-        for (int r = 0; r < kMaxDim; ++r) os->axis[k][r] = (r < d) ? sg * Q[r][k] : 0.0;
-        // covariance is a sum over n points, so lam / n is the variance (n folded
-        // into the scale by the caller's mean-free projection: use the ratio only)
-        os->inv_scale[k] = lam > 0.0 ? 1.0 / (4.0 * sqrt(lam)) : 0.0;
+        const double sg = __shfl_sync(0xffffffffu, q[k], am) < 0.0 ? -1.0 : 1.0;
+        double cq = 0.0;
+#pragma unroll
+        for (int c = 0; c < kMaxDim; ++c) cq = fma(crow[c], __shfl_sync(0xffffffffu, q[k], c), cq);
+        const double lam = warp_sum16(q[k] * cq);
+        if (t < 16) os->axis[k][r] = (r < d) ? sg * q[k] : 0.0;
+        // covariance is a sum over n points: lam / n is the variance (the caller's
+        // projection multiplies by sqrt(n))
+        if (t == 0) os->inv_scale[k] = lam > 0.0 ? 1.0 / (4.0 * sqrt(lam)) : 0.0;
     }
 }
 
@@ -188,58 +195,150 @@ __global__ void scatter_rows(const double* __restrict__ in, const uint32_t* __re
     out[static_cast<size_t>(perm[g]) * width + c] = in[t] + (add_mu ? add_mu->mu[c] : 0.0);
 }
 
-// centroid (log2 units: (x - mu) * sqrt(log2 e) / h) of each tile of `tile_w` rows of
-// x (rows beyond n are padding and ignored); one block of 128 threads per tile
-__global__ void __launch_bounds__(128) tile_centroids(const double* __restrict__ x, size_t n, int d,
-                                                      const PassScalars* __restrict__ sc, double k,
-                                                      int tile_w, float* __restrict__ out) {
-    __shared__ double part[8][kMaxDim];
+// Per-tile summaries (log2 units: y = (x - mu) sqrt(log2 e) / h), one block of
+// 128 threads (one point each) per tile of tile_w <= 128 points (rows beyond n
+// are padding and ignored):
+//   cen[tile][16]   centroid (the skip predictor's input)
+//   box[tile][38]   [0..15] / [16..31] per-coordinate min / max, [32..37] min / max
+//                   of the projections on the three principal axes -- two boxes
+//                   whose separation bounds every point distance from below
+constexpr int kBoxFloats = 38;
+__global__ void __launch_bounds__(128) tile_summary(const double* __restrict__ x, size_t n, int d,
+                                                    const PassScalars* __restrict__ sc,
+                                                    const OrderScalars* __restrict__ os, double k,
+                                                    int tile_w, float* __restrict__ cen,
+                                                    float* __restrict__ box) {
+    __shared__ float red[4][3][kMaxDim + kOrderAxes];   // per warp: sum, min, max
     const size_t r0 = static_cast<size_t>(blockIdx.x) * tile_w;
     const size_t r1 = r0 + tile_w < n ? r0 + tile_w : n;
-    const int c = threadIdx.x & 15, g = threadIdx.x >> 4;
-    double s = 0.0;
-    if (c < d)
-        for (size_t r = r0 + g; r < r1; r += 8) s += x[r * d + c] - sc->mu[c];
-    part[g][c] = s;
+    const size_t r = r0 + threadIdx.x;
+    const bool valid = threadIdx.x < tile_w && r < r1;
+    constexpr int V = kMaxDim + kOrderAxes;
+    float sum[V], lo[V], hi[V];
+    {
+        double y[kMaxDim];
+#pragma unroll
+        for (int c = 0; c < kMaxDim; ++c) y[c] = (valid && c < d) ? (x[r * d + c] - sc->mu[c]) * k : 0.0;
+#pragma unroll
+        for (int c = 0; c < kMaxDim; ++c) sum[c] = static_cast<float>(y[c]);
+#pragma unroll
+        for (int a = 0; a < kOrderAxes; ++a) {
+            double p = 0.0;
+#pragma unroll
+            for (int c = 0; c < kMaxDim; ++c) p = fma(y[c], os->axis[a][c], p);
+            sum[kMaxDim + a] = static_cast<float>(p);
+        }
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            lo[v] = valid ? sum[v] : INFINITY;
+            hi[v] = valid ? sum[v] : -INFINITY;
+            if (!valid) sum[v] = 0.f;
+        }
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+        for (int o = 16; o > 0; o >>= 1) {
+            sum[v] += __shfl_xor_sync(0xffffffffu, sum[v], o);
+            lo[v] = fminf(lo[v], __shfl_xor_sync(0xffffffffu, lo[v], o));
+            hi[v] = fmaxf(hi[v], __shfl_xor_sync(0xffffffffu, hi[v], o));
+        }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0)
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            red[w][0][v] = sum[v];
+            red[w][1][v] = lo[v];
+            red[w][2][v] = hi[v];
+        }
     __syncthreads();
-    if (threadIdx.x < kMaxDim) {
-        double t = 0.0;
-        for (int q = 0; q < 8; ++q) t += part[q][threadIdx.x];
-        const double cnt = r1 > r0 ? static_cast<double>(r1 - r0) : 1.0;
-        out[static_cast<size_t>(blockIdx.x) * kMaxDim + threadIdx.x] =
-            r1 > r0 ? static_cast<float>(t / cnt * k) : 1e18f;
+    if (threadIdx.x < V) {
+        const int v = threadIdx.x;
+        float s = 0.f, l = INFINITY, h = -INFINITY;
+        for (int q = 0; q < 4; ++q) {
+            s += red[q][0][v];
+            l = fminf(l, red[q][1][v]);
+            h = fmaxf(h, red[q][2][v]);
+        }
+        const float cnt = r1 > r0 ? static_cast<float>(r1 - r0) : 1.f;
+        if (v < kMaxDim) {
+            cen[static_cast<size_t>(blockIdx.x) * kMaxDim + v] = r1 > r0 ? s / cnt : 1e18f;
+            box[static_cast<size_t>(blockIdx.x) * kBoxFloats + v] = l;
+            box[static_cast<size_t>(blockIdx.x) * kBoxFloats + kMaxDim + v] = h;
+        } else {
+            const int a = v - kMaxDim;
+            box[static_cast<size_t>(blockIdx.x) * kBoxFloats + 2 * kMaxDim + 2 * a] = l;
+            box[static_cast<size_t>(blockIdx.x) * kBoxFloats + 2 * kMaxDim + 2 * a + 1] = h;
+        }
     }
 }
 
-// Skip predictor: one thread per (row tile, 32 column tiles): bit ct of the
-// row's mask words = centroid half-distance^2 > thresh (log2 units).  The bit
-// only selects the tile pair for the exact check (kModeCheck); pred and skip
-// masks start equal, the check clears skip bits of tiles that contribute.
-__global__ void tile_predict(const float* __restrict__ cenA, int row_tiles,
-                             const float* __restrict__ cenB, int col_tiles, int words, float thresh,
-                             uint32_t* __restrict__ pred, uint32_t* __restrict__ skip) {
+__device__ __forceinline__ float box_gap2(const float* a, const float* b, int n, int stride_hi) {
+    float g2 = 0.f;
+    for (int v = 0; v < n; ++v) {
+        const float alo = a[v], ahi = a[v + stride_hi], blo = b[v], bhi = b[v + stride_hi];
+        const float g = fmaxf(0.f, fmaxf(blo - ahi, alo - bhi));
+        g2 = fmaf(g, g, g2);
+    }
+    return g2;
+}
+
+// Skip predictor: one thread per (row tile, 32 column tiles).  Per tile pair:
+//   * proven: the box separation (coordinates, or the principal-axis projections;
+//     projections never lengthen a distance) bounds every pair's r^2 from below;
+//     if even that pair has log2 phi' = 15 - r^2/2 below kSkipLog2 (with a margin
+//     for the float boxes), the tile is skipped without a check (pred 0, skip 1);
+//   * predicted: centroid half-distance^2 > thresh -> checked exactly by the
+//     check pass (pred 1, skip 1 until the check clears it);
+//   * otherwise computed (pred 0, skip 0).
+__global__ void tile_predict(const float* __restrict__ cenA, const float* __restrict__ boxA,
+                             int row_tiles, const float* __restrict__ cenB,
+                             const float* __restrict__ boxB, int col_tiles, int words, float thresh,
+                             float proven_half_r2, uint32_t* __restrict__ pred,
+                             uint32_t* __restrict__ skip) {
     pdl_launch_dependents();
     pdl_wait();
     const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
     if (t >= static_cast<size_t>(row_tiles) * words) return;
     const int rt = static_cast<int>(t / words), w = static_cast<int>(t % words);
-    float a[kMaxDim];
+    float a[kMaxDim], ab[kBoxFloats];
 #pragma unroll
     for (int c = 0; c < kMaxDim; ++c) a[c] = cenA[(size_t)rt * kMaxDim + c];
-    uint32_t bits = 0;
+#pragma unroll
+    for (int c = 0; c < kBoxFloats; ++c) ab[c] = boxA[(size_t)rt * kBoxFloats + c];
+    uint32_t pbits = 0, sbits = 0;
     for (int b = 0; b < 32; ++b) {
         const int ct = w * 32 + b;
         if (ct >= col_tiles) break;
+        const float* bb = boxB + (size_t)ct * kBoxFloats;
+        float bx[kBoxFloats];
+#pragma unroll
+        for (int c = 0; c < kBoxFloats; ++c) bx[c] = bb[c];
+        float lbp = 0.f;   // principal-axis boxes (lo, hi interleaved per axis)
+#pragma unroll
+        for (int q = 0; q < kOrderAxes; ++q) {
+            const float alo = ab[2 * kMaxDim + 2 * q], ahi = ab[2 * kMaxDim + 2 * q + 1];
+            const float blo = bx[2 * kMaxDim + 2 * q], bhi = bx[2 * kMaxDim + 2 * q + 1];
+            const float g = fmaxf(0.f, fmaxf(blo - ahi, alo - bhi));
+            lbp = fmaf(g, g, lbp);
+        }
+        const float lower = fmaxf(box_gap2(ab, bx, kMaxDim, kMaxDim), lbp);
+        if (0.5f * lower > proven_half_r2) {
+            sbits |= 1u << b;
+            continue;
+        }
         float dd = 0.f;
 #pragma unroll
         for (int c = 0; c < kMaxDim; ++c) {
             const float df = a[c] - cenB[(size_t)ct * kMaxDim + c];
             dd = fmaf(df, df, dd);
         }
-        if (0.5f * dd > thresh) bits |= 1u << b;
+        if (0.5f * dd > thresh) {
+            pbits |= 1u << b;
+            sbits |= 1u << b;
+        }
     }
-    pred[t] = bits;
-    skip[t] = bits;
+    pred[t] = pbits;
+    skip[t] = sbits;
 }
 
 }  // namespace fkde_b200

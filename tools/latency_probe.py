@@ -20,6 +20,8 @@ def main():
     reps = int(sys.argv[1]) if len(sys.argv) > 1 else 50
     lib = N.load()
     ctx = fk.Context([0])
+    if os.environ.get("SPATIAL"):
+        ctx.set_option(N.OPT_SPATIAL, int(os.environ["SPATIAL"]))
     stream = torch.cuda.ExternalStream(ctx.stream())
     cases = [("config1 sdkde", "sdkde", 4096, 4096), ("config2 sdkde", "sdkde", 32768, 32768),
              ("paper sdkde 32k/4k", "sdkde", 32768, 4096), ("config3 kde", "kde", 32768, 32768),
