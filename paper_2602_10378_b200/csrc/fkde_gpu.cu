@@ -631,7 +631,8 @@ Status score_program(Device& D, const Options& o, const Job& J, const double* dX
         // proven-zero threshold on the lower bound of r^2/2 (log2 units): every pair
         // then has log2 phi' = 15 - r^2/2 < kSkipLog2 - 0.5 (float boxes' margin)
         const float proven = 15.0f - kSkipLog2 + 0.5f;
-        tile_predict<<<grid1(rt * words, 128), 128, 0, D.stream>>>(
+        tile_predict<<<dim3(grid1(rt, 128), static_cast<unsigned>((words + kPredWords - 1) / kPredWords)),
+                       128, 0, D.stream>>>(
             D.cenA.as<float>(), D.boxA.as<float>(), static_cast<int>(rt), D.cenB.as<float>(),
             D.boxB.as<float>(), static_cast<int>(ct), words, pred, proven, D.pmask.as<uint32_t>(),
             D.smask.as<uint32_t>());

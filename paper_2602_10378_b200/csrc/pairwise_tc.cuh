@@ -229,8 +229,8 @@ struct TcConfig {
     // O[2] at column 384.  KDE: 4 of 128, check: 5 of 96 (freed once S is loaded).
     static constexpr int kSBuf = kScore ? 384 / kNCol : (kCheck ? 512 / kNCol : 4);
     static constexpr uint32_t kNumBars = 4 + 2 * kStages + 4 * kSBuf + 4;
-    // + tmem slot, 1 KiB alignment slack
-    static constexpr uint32_t kSmemBytes = kOffBar + kNumBars * 8 + 64 + 1024;
+    // + tmem slot + stage column table, 1 KiB alignment slack
+    static constexpr uint32_t kSmemBytes = kOffBar + kNumBars * 8 + 16 + 4 * kStages + 1024;
     static constexpr uint32_t kTmemCols = 512;
     static constexpr uint32_t kTmemO = 384;   // score: O[2] (2 x 64 cols: T_hi, S, T_lo)
     static_assert(!kScore || kSBuf * kNCol <= kTmemO, "S/P buffers overlap O");
@@ -277,6 +277,9 @@ pairwise_tc_kernel(PairArgs args) {
     uint64_t* o_full = s_free + kSB;      // [2]
     uint64_t* o_empty = o_full + 2;       // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
+    // the column tile each B stage holds (written by the producer before the stage's
+    // b_full arrive): the other warps look it up instead of walking the tile mask
+    int* stage_ct = reinterpret_cast<int*>(tmem_slot + 1);   // [kStages]
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -294,7 +297,9 @@ pairwise_tc_kernel(PairArgs args) {
         }
         for (int i = 0; i < kStages; ++i) {
             ptx::mbar_init(&b_full[i], 1);
-            ptx::mbar_init(&b_empty[i], 1);
+            // check pass: the four quadrant warps release a stage once they have read
+            // its column index (stage_ct) and the tile's S; elsewhere an MMA commit
+            ptx::mbar_init(&b_empty[i], kCheck ? 4 : 1);
         }
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(&o_full[i], 1);
@@ -356,6 +361,7 @@ pairwise_tc_kernel(PairArgs args) {
                 const int st = it_b % kStages;
                 ptx::mbar_wait(&b_empty[st], ((it_b / kStages) & 1) ^ 1);
                 if (ptx::elect_one()) {
+                    stage_ct[st] = ct;   // (ordered before the arrive below: release)
                     const bool b2 = kScore && args.opB2;
                     ptx::mbar_arrive_expect_tx(&b_full[st], Cfg::kColBytes * (b2 ? 2u : 1u));
                     ptx::bulk_g2s_hint(smB + st * Cfg::kBStride, args.opB + (size_t)ct * Cfg::kColBytes,
@@ -403,16 +409,15 @@ pairwise_tc_kernel(PairArgs args) {
             const int sp = u / args.n_row_tiles, rt = u % args.n_row_tiles;
             const int ct0 = static_cast<int>((long long)sp * args.n_col_tiles / args.splits);
             const int ct1 = static_cast<int>((long long)(sp + 1) * args.n_col_tiles / args.splits);
-            TileWalk wk = walk_of(rt, ct1);
-            int ct = wk.first(ct0);
-            if (ct >= ct1) continue;
-            const int len = (kScore && !g1) ? wk.count(ct0) : 0;   // GEMM2: sub-unit boundaries
+            // (the issuers only need how many tiles the unit visits, not which)
+            const int len = walk_of(rt, ct1).count(ct0);
+            if (len == 0) continue;
             const int ab = it_a & 1;
             if (g1) {
                 ptx::mbar_wait(&a_full[ab], (it_a >> 1) & 1);
                 ptx::tc_fence_after();
             }
-            for (int rel = 0; ct < ct1; ct = wk.next(), ++rel) {
+            for (int rel = 0; rel < len; ++rel) {
                 const uint32_t st = it_b % kStages;
                 const uint32_t sb = it_s % Cfg::kSBuf;
                 const uint32_t ph = (it_s / Cfg::kSBuf) & 1;
@@ -447,7 +452,7 @@ pairwise_tc_kernel(PairArgs args) {
                                           db0 + ((k * 32) >> 4), idesc1, kk > 0 ? 1u : 0u);
                         }
                         ptx::umma_commit(&s_full[sb]);
-                        if constexpr (!kScore) ptx::umma_commit(&b_empty[st]);
+                        if constexpr (!kScore && !kCheck) ptx::umma_commit(&b_empty[st]);
                     }
                     __syncwarp();
                     FKDE_TRACE(4, it_s);
@@ -547,26 +552,38 @@ pairwise_tc_kernel(PairArgs args) {
                     ptx::tc_fence_before();
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(&o_empty[g & 1]);
-                    if (centred) {
-                        const float cls = ldexpf(cl, -args.sc->e);   // scaled like the operands (exact)
+                    // x = T_hi + T_lo (+ c_J S when centred), then 2Sum into the
+                    // float-float sums -- all in packed f32x2 pairs (with a drain per
+                    // tile the drain's instruction count is not negligible on the
+                    // epilogue's sub-partitions)
+                    const float sv = __uint_as_float(os_);
+                    const float cls = centred ? ldexpf(cl, -args.sc->e) : 0.f;   // scaled like the operands
 #pragma unroll
-                        for (int c = 0; c < kMaxDim; ++c) {   // T = sum phi v + c_J S
-                            const float cc = __shfl_sync(0xffffffffu, cls, c);
-                            const float x = fmaf(cc, __uint_as_float(os_),
-                                                 __uint_as_float(od[c]) + __uint_as_float(ol[c]));
-                            od[c] = __float_as_uint(x);
-                            ol[c] = 0u;
-                        }
+                    for (int c = 0; c < kMaxDim; c += 2) {
+                        float2 x = ptx::fadd2(make_float2(__uint_as_float(od[c]), __uint_as_float(od[c + 1])),
+                                              make_float2(__uint_as_float(ol[c]), __uint_as_float(ol[c + 1])));
+                        if (centred)   // T = sum phi v + c_J S
+                            x = ptx::ffma2(make_float2(__shfl_sync(0xffffffffu, cls, c),
+                                                       __shfl_sync(0xffffffffu, cls, c + 1)),
+                                           make_float2(sv, sv), x);
+                        // 2Sum(ahi, x); a - b as fma(b, -1, a) (exact negation, one rounding)
+                        const float2 m1 = make_float2(-1.f, -1.f);
+                        const float2 a2 = make_float2(ahi[c], ahi[c + 1]);
+                        const float2 s2 = ptx::fadd2(a2, x);
+                        const float2 bb = ptx::ffma2(a2, m1, s2);                 // s - a
+                        const float2 e = ptx::fadd2(ptx::ffma2(ptx::ffma2(bb, m1, s2), m1, a2),   // a - (s - bb)
+                                                    ptx::ffma2(bb, m1, x));                        // + (x - bb)
+                        ahi[c] = s2.x;
+                        ahi[c + 1] = s2.y;
+                        const float2 l2 = ptx::fadd2(make_float2(alo[c], alo[c + 1]), e);
+                        alo[c] = l2.x;
+                        alo[c + 1] = l2.y;
                     }
-#pragma unroll
-                    for (int c = 0; c <= kMaxDim; ++c) {
-                        const float x = c < kMaxDim ? __uint_as_float(od[c]) + __uint_as_float(ol[c])
-                                                    : __uint_as_float(os_);
-                        const float s2 = ahi[c] + x;           // 2Sum(ahi, x)
-                        const float bb = s2 - ahi[c];
-                        const float e = (ahi[c] - (s2 - bb)) + (x - bb);
-                        ahi[c] = s2;
-                        alo[c] += e;
+                    {   // S
+                        const float s2 = ahi[kMaxDim] + sv;
+                        const float bb = s2 - ahi[kMaxDim];
+                        alo[kMaxDim] += (ahi[kMaxDim] - (s2 - bb)) + (sv - bb);
+                        ahi[kMaxDim] = s2;
                     }
                 }
                 const size_t idx = static_cast<size_t>(sp) * args.rows_pad + static_cast<size_t>(rt) * kTileRows + r;
@@ -629,18 +646,18 @@ pairwise_tc_kernel(PairArgs args) {
             // tile to the next (the KDE pass keeps its original bookkeeping cost);
             // with a mask it steps through the visited tiles, skipping other phases'.
             const bool dense = wk.row == nullptr;
-            uint32_t k = 0;
-            int ct = wk.first(ct0);
-            if (dense) {
-                int first_own = par - static_cast<int>(it_s % NP);
-                if (first_own < 0) first_own += NP;
-                k = static_cast<uint32_t>(first_own);
-                ct = ct0 + first_own;
-            }
-            for (; ct < ct1; ct = dense ? ct + NP : wk.next(), k += dense ? NP : 1) {
+            const int len = wk.count(ct0);
+            int first_own = par - static_cast<int>(it_s % NP);
+            if (first_own < 0) first_own += NP;
+            for (int k = first_own; k < len; k += NP) {
                 const uint32_t sidx = it_s + k;
-                if (!dense && static_cast<int>(sidx % NP) != par) continue;   // another phase's tile
                 const uint32_t sb = sidx % Cfg::kSBuf, ph = (sidx / Cfg::kSBuf) & 1;
+                int ct = ct0 + k;
+                if (!dense) {   // the visited tile's column index, from its B stage
+                    const uint32_t st = sidx % kStages;
+                    ptx::mbar_wait(&b_full[st], (sidx / kStages) & 1);   // (complete: GEMM1 used it)
+                    ct = *reinterpret_cast<volatile int*>(&stage_ct[st]);
+                }
                 const int rel = ct - ct0;
                 FKDE_TRACE(0, sidx);
                 ptx::mbar_wait(&s_full[sb], ph);
@@ -716,7 +733,10 @@ pairwise_tc_kernel(PairArgs args) {
                     FKDE_TRACE(6, sidx);
                     ptx::tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(&s_empty[sb]);
+                    if (lane == 0) {
+                        ptx::mbar_arrive(&s_empty[sb]);
+                        ptx::mbar_arrive(&b_empty[sidx % kStages]);   // (stage_ct read above)
+                    }
                     float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
 #pragma unroll
                     for (int c = 0; c < 32; c += 2) {
@@ -768,7 +788,7 @@ pairwise_tc_kernel(PairArgs args) {
                 if constexpr (MODE == kModeLaplace)
                     args.part1[idx] = (accl2[0].x + accl2[0].y) + (accl2[1].x + accl2[1].y);
             }
-            it_s += dense ? static_cast<uint32_t>(ct1 - ct0) : k;
+            it_s += static_cast<uint32_t>(len);
         }
         if (kCheck && args.stats && lane == 0 && q == 0 && n_checked)
             atomicAdd(&args.stats[0], n_checked);

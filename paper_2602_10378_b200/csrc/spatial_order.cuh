@@ -272,17 +272,8 @@ __global__ void __launch_bounds__(128) tile_summary(const double* __restrict__ x
     }
 }
 
-__device__ __forceinline__ float box_gap2(const float* a, const float* b, int n, int stride_hi) {
-    float g2 = 0.f;
-    for (int v = 0; v < n; ++v) {
-        const float alo = a[v], ahi = a[v + stride_hi], blo = b[v], bhi = b[v + stride_hi];
-        const float g = fmaxf(0.f, fmaxf(blo - ahi, alo - bhi));
-        g2 = fmaf(g, g, g2);
-    }
-    return g2;
-}
 
-// Skip predictor: one thread per (row tile, 32 column tiles).  Per tile pair:
+// Skip predictor.  Per tile pair:
 //   * proven: the box separation (coordinates, or the principal-axis projections;
 //     projections never lengthen a distance) bounds every pair's r^2 from below;
 //     if even that pair has log2 phi' = 15 - r^2/2 below kSkipLog2 (with a margin
@@ -290,55 +281,78 @@ __device__ __forceinline__ float box_gap2(const float* a, const float* b, int n,
 //   * predicted: centroid half-distance^2 > thresh -> checked exactly by the
 //     check pass (pred 1, skip 1 until the check clears it);
 //   * otherwise computed (pred 0, skip 0).
-__global__ void tile_predict(const float* __restrict__ cenA, const float* __restrict__ boxA,
-                             int row_tiles, const float* __restrict__ cenB,
-                             const float* __restrict__ boxB, int col_tiles, int words, float thresh,
-                             float proven_half_r2, uint32_t* __restrict__ pred,
-                             uint32_t* __restrict__ skip) {
+// Block = 128 row tiles (one per thread) x kPredWords mask words (32 column tiles
+// each): the column tiles' summaries are staged once in shared memory, so each
+// summary is read from global memory once per 128 row tiles (a thread per (row
+// tile, word) re-reading its 32 column summaries moved ~14 GB at n = 2^20).
+constexpr int kPredWords = 4;
+constexpr int kSumFloats = kMaxDim + kBoxFloats;   // centroid + boxes
+__global__ void __launch_bounds__(128) tile_predict(const float* __restrict__ cenA,
+                                                    const float* __restrict__ boxA, int row_tiles,
+                                                    const float* __restrict__ cenB,
+                                                    const float* __restrict__ boxB, int col_tiles,
+                                                    int words, float thresh, float proven_half_r2,
+                                                    uint32_t* __restrict__ pred,
+                                                    uint32_t* __restrict__ skip) {
     pdl_launch_dependents();
     pdl_wait();
-    const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-    if (t >= static_cast<size_t>(row_tiles) * words) return;
-    const int rt = static_cast<int>(t / words), w = static_cast<int>(t % words);
+    __shared__ float colsum[kPredWords * 32][kSumFloats];
+    const int w0 = blockIdx.y * kPredWords;
+    const int ct0 = w0 * 32;
+    const int nct = min(kPredWords * 32, col_tiles - ct0);
+    for (int e = threadIdx.x; e < nct * kSumFloats; e += blockDim.x) {
+        const int j = e / kSumFloats, v = e % kSumFloats;
+        colsum[j][v] = v < kMaxDim ? cenB[(size_t)(ct0 + j) * kMaxDim + v]
+                                   : boxB[(size_t)(ct0 + j) * kBoxFloats + (v - kMaxDim)];
+    }
+    __syncthreads();
+    const int rt = blockIdx.x * blockDim.x + threadIdx.x;
+    if (rt >= row_tiles) return;
     float a[kMaxDim], ab[kBoxFloats];
 #pragma unroll
     for (int c = 0; c < kMaxDim; ++c) a[c] = cenA[(size_t)rt * kMaxDim + c];
 #pragma unroll
     for (int c = 0; c < kBoxFloats; ++c) ab[c] = boxA[(size_t)rt * kBoxFloats + c];
-    uint32_t pbits = 0, sbits = 0;
-    for (int b = 0; b < 32; ++b) {
-        const int ct = w * 32 + b;
-        if (ct >= col_tiles) break;
-        const float* bb = boxB + (size_t)ct * kBoxFloats;
-        float bx[kBoxFloats];
+    for (int wi = 0; wi < kPredWords && w0 + wi < words; ++wi) {
+        uint32_t pbits = 0, sbits = 0;
+        for (int b = 0; b < 32; ++b) {
+            const int j = wi * 32 + b;
+            if (j >= nct) break;
+            const float* cs = colsum[j];   // (all threads read the same address: broadcast)
+            float lower = 0.f;
 #pragma unroll
-        for (int c = 0; c < kBoxFloats; ++c) bx[c] = bb[c];
-        float lbp = 0.f;   // principal-axis boxes (lo, hi interleaved per axis)
+            for (int c = 0; c < kMaxDim; ++c) {   // coordinate boxes
+                const float g = fmaxf(0.f, fmaxf(cs[kMaxDim + c] - ab[kMaxDim + c],
+                                                 ab[c] - cs[2 * kMaxDim + c]));
+                lower = fmaf(g, g, lower);
+            }
+            float lbp = 0.f;
 #pragma unroll
-        for (int q = 0; q < kOrderAxes; ++q) {
-            const float alo = ab[2 * kMaxDim + 2 * q], ahi = ab[2 * kMaxDim + 2 * q + 1];
-            const float blo = bx[2 * kMaxDim + 2 * q], bhi = bx[2 * kMaxDim + 2 * q + 1];
-            const float g = fmaxf(0.f, fmaxf(blo - ahi, alo - bhi));
-            lbp = fmaf(g, g, lbp);
-        }
-        const float lower = fmaxf(box_gap2(ab, bx, kMaxDim, kMaxDim), lbp);
-        if (0.5f * lower > proven_half_r2) {
-            sbits |= 1u << b;
-            continue;
-        }
-        float dd = 0.f;
+            for (int q = 0; q < kOrderAxes; ++q) {   // principal-axis boxes
+                const float alo = ab[2 * kMaxDim + 2 * q], ahi = ab[2 * kMaxDim + 2 * q + 1];
+                const float blo = cs[3 * kMaxDim + 2 * q], bhi = cs[3 * kMaxDim + 2 * q + 1];
+                const float g = fmaxf(0.f, fmaxf(blo - ahi, alo - bhi));
+                lbp = fmaf(g, g, lbp);
+            }
+            if (0.5f * fmaxf(lower, lbp) > proven_half_r2) {
+                sbits |= 1u << b;
+                continue;
+            }
+            float dd = 0.f;
 #pragma unroll
-        for (int c = 0; c < kMaxDim; ++c) {
-            const float df = a[c] - cenB[(size_t)ct * kMaxDim + c];
-            dd = fmaf(df, df, dd);
+            for (int c = 0; c < kMaxDim; ++c) {
+                const float df = a[c] - cs[c];
+                dd = fmaf(df, df, dd);
+            }
+            if (0.5f * dd > thresh) {
+                pbits |= 1u << b;
+                sbits |= 1u << b;
+            }
         }
-        if (0.5f * dd > thresh) {
-            pbits |= 1u << b;
-            sbits |= 1u << b;
-        }
+        const size_t t = (size_t)rt * words + w0 + wi;
+        pred[t] = pbits;
+        skip[t] = sbits;
     }
-    pred[t] = pbits;
-    skip[t] = sbits;
 }
 
 }  // namespace fkde_b200
