@@ -122,11 +122,18 @@ void* fkde_gpu_stream(fkde_gpu_ctx* ctx);
 int fkde_gpu_last_timing(const fkde_gpu_ctx* ctx, float* ms, int n);
 /* number of kernels this library launched during the last call (this rank) */
 int64_t fkde_gpu_last_launch_count(const fkde_gpu_ctx* ctx);
-/* score-pass tile skipping of the last call on device 0 (synchronises):
- * out[0] = (row tile, column tile) pairs checked exactly, out[1] = pairs
- * skipped (every pair of points in them contributes exactly zero), out[2] =
- * pairs in the pass, out[3] = 1 if the pass ran on the spatial order */
-int fkde_gpu_last_skip_stats(fkde_gpu_ctx* ctx, uint64_t* out4);
+/* tile skipping of the last call on device 0 (synchronises); fills
+ * min(n, FKDE_SKIP_STATS_COUNT) entries:
+ *   [0] score pass: (row tile, column tile) pairs checked exactly
+ *   [1] score pass: pairs skipped (every pair of points in them contributes
+ *       exactly zero to the fp16 P sums)
+ *   [2] score pass: pairs in the pass       [3] 1 if it ran on the spatial order
+ *   [4] density pass: pairs skipped (box bound: every kernel value < 2^-44.5)
+ *   [5] density pass: pairs in the pass     [6] 1 if it ran on the spatial order
+ *   [7] density pass: query rows recomputed by direct differences
+ *   [8] score pass: rows recomputed by direct differences */
+#define FKDE_SKIP_STATS_COUNT 9
+int fkde_gpu_last_skip_stats(fkde_gpu_ctx* ctx, uint64_t* out, size_t n);
 /* device workspace currently held by the context (all devices), bytes: the
  * analogue of the reference's transient-allocation accounting
  * (alloc_stats, test_engine.cpp:218-243) -- linear in n + m, never n x m */

@@ -30,6 +30,7 @@ METHOD_KDE, METHOD_SDKDE, METHOD_LAPLACE = 0, 1, 2
 
 OPT_ENGINE, OPT_SPLITS, OPT_TIMING, OPT_MAX_CTAS, OPT_FLUSH_TILES = 1, 2, 3, 4, 5
 OPT_SPATIAL = 7
+SKIP_STATS_COUNT = 9   # FKDE_SKIP_STATS_COUNT
 OPT_PDL = 8
 ENGINE_TC = 0
 
@@ -85,7 +86,7 @@ def _declare(lib):
     lib.fkde_gpu_last_launch_count.argtypes = [_vp]
     lib.fkde_gpu_last_launch_count.restype = ctypes.c_int64
     lib.fkde_gpu_workspace_bytes.argtypes = [_vp, _szp]
-    lib.fkde_gpu_last_skip_stats.argtypes = [_vp, ctypes.POINTER(ctypes.c_uint64)]
+    lib.fkde_gpu_last_skip_stats.argtypes = [_vp, ctypes.POINTER(ctypes.c_uint64), ctypes.c_size_t]
     lib.fkde_gpu_score.argtypes = [_vp, _dp, _sz, _sz, ctypes.c_double, _dp, _szp]
     lib.fkde_gpu_score_accumulate.argtypes = [_vp, _dp, _sz, _sz, ctypes.c_double, _dp, _dp]
     lib.fkde_gpu_kde.argtypes = [_vp, _dp, _sz, _dp, _sz, _sz, ctypes.c_double, ctypes.c_int,

@@ -16,7 +16,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libfkde_b200.so")
 SOURCES = ["fkde_gpu.cu", "host_fixtures.cpp", "host_io.cpp"]
-HEADERS = ["ptx.cuh", "layout.cuh", "pairwise_tc.cuh", "prep_kernels.cuh", "direct_rows.cuh"]
+HEADERS = ["ptx.cuh", "layout.cuh", "pairwise_tc.cuh", "prep_kernels.cuh", "direct_rows.cuh",
+           "spatial_order.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

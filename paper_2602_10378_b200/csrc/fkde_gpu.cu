@@ -198,6 +198,12 @@ struct Device {
     size_t mask_bytes = 0;       // skip mask of the last score pass (0: none)
     uint64_t tiles_total = 0;    // tile pairs of the last score pass
     bool ordered = false;        // last score pass ran on the spatial order
+    // density pass on the spatial order: sorted queries, their permutation, keys + CUB
+    // scratch, skipped tiles per query tile, densities back in the caller's order
+    DevBuf Qs, qperm, qkeys, qcubtmp, qskip, qout;
+    bool qordered = false;       // last density pass ran on the spatial order (D.qout)
+    uint64_t dtiles_total = 0;   // tile pairs of the last density pass
+    size_t dtiles_rows = 0;      // query tiles of the last skipping density pass (0: none)
     cudaEvent_t ev[FKDE_T_COUNT + 1] = {};
     int64_t launches = 0;
     // device-resident API: the call's whole device program as a CUDA graph,
@@ -209,6 +215,13 @@ struct Device {
     uint64_t graph_epoch = 0;   // g_alloc_epoch when the graph was captured
     float timing[FKDE_T_COUNT] = {};
     Status last;
+    std::vector<DevBuf*> buffers() {   // every device workspace (free / size accounting)
+        return {&X,     &Y,     &opA,  &opB,    &opB2,  &part0, &part1,     &xsd,     &out,
+                &aux0,  &aux1,  &colpart, &scal, &err,  &flags, &risk,      &dpart,   &ddone,
+                &pdone, &qmax,  &Xs,   &perm,   &keys,  &cubtmp, &ordsc,    &cenA,    &cenB,
+                &boxA,  &boxB,  &skipstats, &unperm0, &unperm1, &pmask, &smask, &Qs, &qperm,
+                &qkeys, &qcubtmp, &qskip, &qout};
+    }
 };
 
 }  // namespace
@@ -409,7 +422,8 @@ Status pack2(Device& D, bool pdl, const PackArgs& a, const PackArgs& b) {
 
 // one pairwise pass over (row operand x column operand) with density partials
 Status density_pass(Device& D, const Options& o, int mode, size_t rows_pad, size_t n_cols,
-                    const PassScalars* sc, int* nparts_out) {
+                    const PassScalars* sc, int* nparts_out, const uint32_t* skip_mask = nullptr,
+                    int mask_words = 0) {
     const size_t rt = rows_pad / kTileRows;
     const size_t ct = round_up(n_cols, kTileRows) / kTileRows;
     const int splits =
@@ -431,6 +445,8 @@ Status density_pass(Device& D, const Options& o, int mode, size_t rows_pad, size
     a.flush_log2 = 0;
     a.rows_pad = rows_pad;
     a.diag_row0 = -1;
+    a.skip_mask = const_cast<uint32_t*>(skip_mask);
+    a.mask_words = mask_words;
     if (mode == kModeGauss)
         STATUS_TRY(launch_pairwise<kModeGauss>(D, o, a, n_cols));
     else
@@ -530,6 +546,46 @@ Status spatial_order(Device& D, const double* dX, size_t n, int d, const PassSca
     return {};
 }
 
+// Density pass on the spatial order: a tile pair is skipped when the box bound
+// proves every pair's log2 phi < -(kDensitySkipHalfR2 - 0.5) (0.5: margin for the
+// float boxes).  The skipped contribution of a row is then below skipped_tiles *
+// 128 * 2^-44.5 (Gaussian terms phi) or that times (1 + d/2 + ln2 * 44.5)
+// (Laplace-fused terms phi (1 + d/2 - u); phi |log2 phi| decreases below 1/e), and a
+// row whose term mass (|ca| s0 + |cb| |s1|: the scale of the fp32 sums' own
+// rounding of that row) is not at least 2^24 times that bound is recomputed by
+// direct differences (reduce_density flags it).  The skip therefore changes no
+// row by more than 2^-24 of its term mass.
+constexpr float kDensitySkipHalfR2 = 45.0f;
+inline double density_skip_flag(int kernel, int d) {   // per skipped tile, x 2^24
+    const double per_pair = kernel == FKDE_KERNEL_GAUSSIAN ? 0x1p-44 : 0x1p-44 * (1.0 + 0.5 * d + 31.0);
+    return 128.0 * per_pair * 0x1p24;
+}
+
+// Queries sorted on the training order's axes (D.ordsc; sc: the training mean,
+// n_cov: the count the covariance was summed over): D.Qs = Q[qperm]
+Status order_queries(Device& D, const double* dQ, size_t m, int d, size_t n_cov,
+                     const PassScalars* sc) {
+    STATUS_TRY(ensure(D.qkeys, 2 * m * sizeof(uint32_t)));
+    STATUS_TRY(ensure(D.qperm, 2 * m * sizeof(uint32_t)));
+    uint32_t* kin = D.qkeys.as<uint32_t>();
+    uint32_t* kout = kin + m;
+    uint32_t* iin = D.qperm.as<uint32_t>() + m;
+    uint32_t* perm = D.qperm.as<uint32_t>();
+    morton_keys<<<grid1(m, 256), 256, 0, D.stream>>>(dQ, m, d, std::sqrt(static_cast<double>(n_cov)), sc,
+                                                      D.ordsc.as<OrderScalars>(), kin, iin);
+    size_t tmp = 0;
+    CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin, kout, iin, perm, static_cast<int>(m), 0,
+                                             kOrderAxes * kMortonBits, D.stream));
+    STATUS_TRY(ensure(D.qcubtmp, tmp));
+    CUDA_TRY(cub::DeviceRadixSort::SortPairs(D.qcubtmp.p, tmp, kin, kout, iin, perm, static_cast<int>(m),
+                                             0, kOrderAxes * kMortonBits, D.stream));
+    STATUS_TRY(ensure(D.Qs, m * d * sizeof(double)));
+    gather_rows<<<grid1(m * d, 256), 256, 0, D.stream>>>(dQ, perm, m, d, D.Qs.as<double>());
+    D.launches += 2;
+    CUDA_TRY(cudaGetLastError());
+    return {};
+}
+
 // Score pass on this rank's row shard; leaves the requested per-row outputs in
 // D.aux0 / D.aux1 / D.xsd in global row layout (gathered when world > 1).  With
 // the spatial order (D.ordered) that layout is the sorted one: unpermute_score()
@@ -598,10 +654,10 @@ Status score_program(Device& D, const Options& o, const Job& J, const double* dX
         STATUS_TRY(ensure(D.boxA, rt * kBoxFloats * sizeof(float)));
         STATUS_TRY(ensure(D.boxB, ct * kBoxFloats * sizeof(float)));
         tile_summary<<<static_cast<unsigned>(rt), 128, 0, D.stream>>>(
-            dX + sh.begin * d, sh.rows, d, sc, D.ordsc.as<OrderScalars>(), ks, kTileRows,
+            dX + sh.begin * d, sh.rows, d, sc, D.ordsc.as<OrderScalars>(), ks, kTileRows, 0,
             D.cenA.as<float>(), D.boxA.as<float>());
         tile_summary<<<static_cast<unsigned>(ct), 128, 0, D.stream>>>(
-            dX, n, d, sc, D.ordsc.as<OrderScalars>(), ks, static_cast<int>(kScoreNCol),
+            dX, n, d, sc, D.ordsc.as<OrderScalars>(), ks, static_cast<int>(kScoreNCol), 0,
             D.cenB.as<float>(), D.boxB.as<float>());
         size_t b2_pad = 0;
         PackArgs p2;
@@ -635,7 +691,7 @@ Status score_program(Device& D, const Options& o, const Job& J, const double* dX
                        128, 0, D.stream>>>(
             D.cenA.as<float>(), D.boxA.as<float>(), static_cast<int>(rt), D.cenB.as<float>(),
             D.boxB.as<float>(), static_cast<int>(ct), words, pred, proven, D.pmask.as<uint32_t>(),
-            D.smask.as<uint32_t>());
+            D.smask.as<uint32_t>(), nullptr);
         D.launches += 1;
         CUDA_TRY(cudaGetLastError());
         PairArgs c = a;
@@ -714,6 +770,9 @@ Status score_program(Device& D, const Options& o, const Job& J, const double* dX
         e.phi_sum = f.phi_sum;
         e.weighted = f.weighted;
         STATUS_TRY(launch_direct(D, o.pdl, e, sh.rows));
+        // (statistics: the score pass's directly recomputed row count, skipstats[1])
+        CUDA_TRY(cudaMemcpyAsync(D.skipstats.as<unsigned long long>() + 1, f.flag_count, sizeof(unsigned int),
+                                 cudaMemcpyDeviceToDevice, D.stream));
     }
     record(D, o, FKDE_T_GATHER);
     if (J.kind == Job::kScore) STATUS_TRY(allgather(D, D.aux0.p, sh.chunk * d, ncclFloat64));
@@ -773,6 +832,16 @@ Status query_program(Device& D, const Options& o, const Job& J, const double* dC
         ++D.launches;
         CUDA_TRY(cudaGetLastError());
     }
+    // spatial order (the columns were sorted by the score pass / spatial_order): the
+    // queries sorted on the same axes, and -- Gaussian and Laplace-fused passes --
+    // tile pairs skipped on the box bound (kDensitySkipHalfR2)
+    D.qordered = D.ordered;
+    D.dtiles_rows = 0;
+    if (D.qordered) {
+        STATUS_TRY(order_queries(D, dQ, m, d, n, sc_q));
+        dQ = D.Qs.as<double>();
+    }
+    const bool skipping = D.qordered && o.spatial != 3 && (kernel == FKDE_KERNEL_GAUSSIAN || fused);
     const Shard sh = shard_of(m, D.world, D.rank);
     size_t rows_pad = 0, cols_pad = 0;
     PackArgs pa, pb;
@@ -780,6 +849,38 @@ Status query_program(Device& D, const Options& o, const Job& J, const double* dC
     STATUS_TRY(pack_args(D, dCols, n, d, 1, !cols_centred, kh, sc_q, D.opB, &cols_pad, &pb));
     STATUS_TRY(pack2(D, o.pdl, pa, pb));
     record(D, o, FKDE_T_QUERY);
+    const uint32_t* dmask = nullptr;
+    int dwords = 0;
+    const size_t q_rt = rows_pad / kTileRows, q_ct = cols_pad / kTileRows;
+    D.dtiles_total = static_cast<uint64_t>(q_rt) * q_ct;
+    if (skipping) {
+        dwords = static_cast<int>((q_ct + 31) / 32);
+        STATUS_TRY(ensure(D.cenA, q_rt * kMaxDim * sizeof(float)));
+        STATUS_TRY(ensure(D.cenB, q_ct * kMaxDim * sizeof(float)));
+        STATUS_TRY(ensure(D.boxA, q_rt * kBoxFloats * sizeof(float)));
+        STATUS_TRY(ensure(D.boxB, q_ct * kBoxFloats * sizeof(float)));
+        STATUS_TRY(ensure(D.pmask, q_rt * dwords * sizeof(uint32_t)));
+        STATUS_TRY(ensure(D.smask, q_rt * dwords * sizeof(uint32_t)));
+        STATUS_TRY(ensure(D.qskip, q_rt * sizeof(unsigned int)));
+        CUDA_TRY(cudaMemsetAsync(D.qskip.p, 0, q_rt * sizeof(unsigned int), D.stream));
+        if (sh.rows)
+            tile_summary<<<static_cast<unsigned>(q_rt), 128, 0, D.stream>>>(
+                dQ + sh.begin * d, sh.rows, d, sc_q, D.ordsc.as<OrderScalars>(), kh, kTileRows, 0,
+                D.cenA.as<float>(), D.boxA.as<float>());
+        tile_summary<<<static_cast<unsigned>(q_ct), 128, 0, D.stream>>>(
+            dCols, n, d, sc_q, D.ordsc.as<OrderScalars>(), kh, kTileRows, cols_centred ? 1 : 0,
+            D.cenB.as<float>(), D.boxB.as<float>());
+        // (no predicted pairs: thresh = inf; only the proven bound skips)
+        tile_predict<<<dim3(grid1(q_rt, 128), static_cast<unsigned>((dwords + kPredWords - 1) / kPredWords)),
+                       128, 0, D.stream>>>(
+            D.cenA.as<float>(), D.boxA.as<float>(), static_cast<int>(q_rt), D.cenB.as<float>(),
+            D.boxB.as<float>(), static_cast<int>(q_ct), dwords, INFINITY, kDensitySkipHalfR2,
+            D.pmask.as<uint32_t>(), D.smask.as<uint32_t>(), D.qskip.as<unsigned int>());
+        D.launches += 3;
+        CUDA_TRY(cudaGetLastError());
+        dmask = D.smask.as<uint32_t>();
+        D.dtiles_rows = q_rt;
+    }
 
     const double norm = std::pow(2.0 * M_PI, -0.5 * d) * std::pow(J.h, -static_cast<double>(d)) /
                         static_cast<double>(n);  // gaussian_norm_const(h,d)/n, kernels.cpp:26-29
@@ -793,7 +894,7 @@ Status query_program(Device& D, const Options& o, const Job& J, const double* dC
     unsigned int* flag_count = D.flags.as<unsigned int>();
     int nparts = 0;
     if (kernel == FKDE_KERNEL_GAUSSIAN) {
-        STATUS_TRY(density_pass(D, o, kModeGauss, rows_pad, n, sc_q, &nparts));
+        STATUS_TRY(density_pass(D, o, kModeGauss, rows_pad, n, sc_q, &nparts, dmask, dwords));
         record(D, o, FKDE_T_REDUCE);
         r.part0 = D.part0.as<float>();
         r.nparts = nparts;
@@ -803,11 +904,13 @@ Status query_program(Device& D, const Options& o, const Job& J, const double* dC
         r.flag_count = flag_count;
         r.flag_rows = flag_count + 1;
         r.risk = D.risk.as<uint8_t>();
+        r.skip_tiles = dmask ? D.qskip.as<unsigned int>() : nullptr;
+        r.skip_flag_mass = density_skip_flag(FKDE_KERNEL_GAUSSIAN, d);
         if (sh.rows) CUDA_TRY(launch_chain(o.pdl, reduce_density, dim3(grid1(sh.rows, 256)), dim3(256), 0, D.stream, r));
         ++D.launches;
     } else if (fused) {
         // LaplaceFused: phi (1 + d/2 - u) = (1 + d/2) phi + ln2 * phi * log2(phi)
-        STATUS_TRY(density_pass(D, o, kModeLaplace, rows_pad, n, sc_q, &nparts));
+        STATUS_TRY(density_pass(D, o, kModeLaplace, rows_pad, n, sc_q, &nparts, dmask, dwords));
         record(D, o, FKDE_T_REDUCE);
         r.part0 = D.part0.as<float>();
         r.part1 = D.part1.as<float>();
@@ -818,6 +921,8 @@ Status query_program(Device& D, const Options& o, const Job& J, const double* dC
         r.flag_count = flag_count;
         r.flag_rows = flag_count + 1;
         r.risk = D.risk.as<uint8_t>();
+        r.skip_tiles = dmask ? D.qskip.as<unsigned int>() : nullptr;
+        r.skip_flag_mass = density_skip_flag(FKDE_KERNEL_LAPLACE_CORRECTED, d);
         if (sh.rows) CUDA_TRY(launch_chain(o.pdl, reduce_density, dim3(grid1(sh.rows, 256)), dim3(256), 0, D.stream, r));
         ++D.launches;
     } else {
@@ -865,6 +970,13 @@ Status query_program(Device& D, const Options& o, const Job& J, const double* dC
         STATUS_TRY(launch_direct(D, o.pdl, e, sh.rows));
     }
     STATUS_TRY(allgather(D, D.out.p, sh.chunk, ncclFloat64));
+    if (D.qordered) {   // densities back to the caller's query order
+        STATUS_TRY(ensure(D.qout, m * sizeof(double)));
+        scatter_rows<<<grid1(m, 256), 256, 0, D.stream>>>(D.out.as<double>(), D.qperm.as<uint32_t>(), m, 1,
+                                                          nullptr, D.qout.as<double>());
+        ++D.launches;
+        CUDA_TRY(cudaGetLastError());
+    }
     return {};
 }
 
@@ -952,6 +1064,13 @@ Status run_job(Device& D, const Options& o, const Job& J) {
         }
         case Job::kKde: {
             STATUS_TRY(prep(D, o.pdl, dX, J.n, d, 0.0, sc_q, false));   // the mean only
+            // large point sets: training points and queries on the spatial order, so
+            // the density pass skips tile pairs too (query_program)
+            D.ordered = use_spatial(o, J.n);
+            if (D.ordered) {
+                STATUS_TRY(spatial_order(D, dX, J.n, d, sc_q));
+                dX = D.Xs.as<double>();
+            }
             record(D, o, FKDE_T_SCORE);
             record(D, o, FKDE_T_FINALIZE);
             record(D, o, FKDE_T_GATHER);
@@ -965,12 +1084,13 @@ Status run_job(Device& D, const Options& o, const Job& J) {
     // outputs
     const size_t nd = J.n * d;
     if (J.kind == Job::kSdkde || J.kind == Job::kKde) {
+        const void* dens = D.qordered ? D.qout.p : D.out.p;
         if (J.d_out) {
-            CUDA_TRY(cudaMemcpyAsync(J.d_out, D.out.p, J.m * sizeof(double),
-                                     cudaMemcpyDeviceToDevice, D.stream));
+            CUDA_TRY(cudaMemcpyAsync(J.d_out, dens, J.m * sizeof(double), cudaMemcpyDeviceToDevice,
+                                     D.stream));
         }
         if (J.out) {
-            CUDA_TRY(cudaMemcpyAsync(J.out, D.out.p, J.m * sizeof(double), cudaMemcpyDeviceToHost,
+            CUDA_TRY(cudaMemcpyAsync(J.out, dens, J.m * sizeof(double), cudaMemcpyDeviceToHost,
                                      D.stream));
         }
         if (J.kind == Job::kSdkde && J.out2)   // the side-stream copy joins the main stream
@@ -1192,12 +1312,7 @@ void fkde_gpu_destroy(fkde_gpu_ctx* ctx) {
         cudaSetDevice(D.dev);
         if (D.stream) cudaStreamSynchronize(D.stream);
         if (D.comm && nccl().loaded) nccl().CommDestroy(D.comm);
-        DevBuf* bufs[] = {&D.X,    &D.Y,     &D.opA,  &D.opB, &D.part0, &D.part1,
-                          &D.xsd,  &D.out,   &D.aux0, &D.aux1, &D.colpart, &D.scal,
-                          &D.err,  &D.flags, &D.risk, &D.dpart, &D.ddone,
-                          &D.Xs,   &D.perm,  &D.keys, &D.cubtmp, &D.ordsc, &D.cenA,
-                          &D.cenB, &D.skipstats, &D.unperm0, &D.unperm1, &D.pdone, &D.qmax, &D.pmask, &D.smask, &D.opB2, &D.boxA, &D.boxB};
-        for (DevBuf* b : bufs)
+        for (DevBuf* b : D.buffers())
             if (b->p) cudaFree(b->p);
         for (auto& e : D.ev)
             if (e) cudaEventDestroy(e);
@@ -1294,38 +1409,51 @@ int fkde_gpu_workspace_bytes(const fkde_gpu_ctx* ctx, size_t* bytes) {
     if (!ctx || !bytes) return FKDE_INVALID_ARGUMENT;
     size_t total = 0;
     for (const Device& D : ctx->devs) {
-        const DevBuf* bufs[] = {&D.X,    &D.Y,     &D.opA,  &D.opB,  &D.part0,   &D.part1,
-                                &D.xsd,  &D.out,   &D.aux0, &D.aux1, &D.colpart, &D.scal,
-                                &D.err,  &D.flags, &D.risk, &D.dpart, &D.ddone,
-                                &D.Xs,   &D.perm,  &D.keys, &D.cubtmp, &D.ordsc, &D.cenA,
-                                &D.cenB, &D.skipstats, &D.unperm0, &D.unperm1, &D.pdone, &D.qmax, &D.pmask, &D.smask, &D.opB2, &D.boxA, &D.boxB};
-        for (const DevBuf* b : bufs) total += b->bytes;
+        for (const DevBuf* b : const_cast<Device&>(D).buffers()) total += b->bytes;
     }
     *bytes = total;
     return FKDE_OK;
 }
 
-int fkde_gpu_last_skip_stats(fkde_gpu_ctx* ctx, uint64_t* out4) {
-    if (!ctx || !out4) return FKDE_INVALID_ARGUMENT;
+int fkde_gpu_last_skip_stats(fkde_gpu_ctx* ctx, uint64_t* out, size_t n) {
+    if (!ctx || (!out && n)) return FKDE_INVALID_ARGUMENT;
     const Device& D = ctx->devs[0];
-    for (int i = 0; i < 4; ++i) out4[i] = 0;
-    if (!D.skipstats.p) return FKDE_OK;
-    cudaSetDevice(D.dev);
-    if (cudaStreamSynchronize(D.stream) != cudaSuccess) return FKDE_CUDA_ERROR;
-    unsigned long long h[1] = {0};
-    if (cudaMemcpy(h, D.skipstats.p, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess)
-        return FKDE_CUDA_ERROR;
-    uint64_t skipped = 0;
-    if (D.mask_bytes) {   // popcount of the skip mask
-        std::vector<uint32_t> m(D.mask_bytes / sizeof(uint32_t));
-        if (cudaMemcpy(m.data(), D.smask.p, D.mask_bytes, cudaMemcpyDeviceToHost) != cudaSuccess)
+    uint64_t v[FKDE_SKIP_STATS_COUNT] = {};
+    if (D.skipstats.p) {
+        cudaSetDevice(D.dev);
+        if (cudaStreamSynchronize(D.stream) != cudaSuccess) return FKDE_CUDA_ERROR;
+        unsigned long long h[2] = {0, 0};
+        if (cudaMemcpy(h, D.skipstats.p, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess)
             return FKDE_CUDA_ERROR;
-        for (uint32_t w : m) skipped += static_cast<uint64_t>(__builtin_popcount(w));
+        uint64_t skipped = 0;
+        if (D.mask_bytes) {   // popcount of the score pass's skip mask
+            std::vector<uint32_t> m(D.mask_bytes / sizeof(uint32_t));
+            if (cudaMemcpy(m.data(), D.smask.p, D.mask_bytes, cudaMemcpyDeviceToHost) != cudaSuccess)
+                return FKDE_CUDA_ERROR;
+            for (uint32_t w : m) skipped += static_cast<uint64_t>(__builtin_popcount(w));
+        }
+        uint64_t dskipped = 0;
+        if (D.dtiles_rows) {   // the density pass's per-query-tile skip counts
+            std::vector<unsigned int> c(D.dtiles_rows);
+            if (cudaMemcpy(c.data(), D.qskip.p, c.size() * sizeof(unsigned int), cudaMemcpyDeviceToHost) !=
+                cudaSuccess)
+                return FKDE_CUDA_ERROR;
+            for (unsigned int x : c) dskipped += x;
+        }
+        unsigned int dflag = 0;
+        if (D.flags.p && cudaMemcpy(&dflag, D.flags.p, sizeof(dflag), cudaMemcpyDeviceToHost) != cudaSuccess)
+            return FKDE_CUDA_ERROR;
+        v[0] = h[0];
+        v[1] = skipped;
+        v[2] = D.tiles_total;
+        v[3] = D.ordered ? 1 : 0;
+        v[4] = dskipped;
+        v[5] = D.dtiles_total;
+        v[6] = D.qordered ? 1 : 0;
+        v[7] = dflag;
+        v[8] = h[1] & 0xFFFFFFFFull;
     }
-    out4[0] = h[0];
-    out4[1] = skipped;
-    out4[2] = D.tiles_total;
-    out4[3] = D.ordered ? 1 : 0;
+    for (size_t i = 0; i < n && i < FKDE_SKIP_STATS_COUNT; ++i) out[i] = v[i];
     return FKDE_OK;
 }
 

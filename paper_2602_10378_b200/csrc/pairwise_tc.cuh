@@ -73,7 +73,7 @@ struct PairArgs {
     // in finalize_score, so that T - x S never cancels against the self term.
     long long diag_row0;  // -1: no diagonal
     // tile masks, one bit per (row tile, column tile), rows of mask_words words:
-    //   SCORE: skip_mask (nullptr = visit every tile): visit tiles whose bit is 0
+    //   SCORE / KDE: skip_mask (nullptr = visit every tile): visit tiles whose bit is 0
     //   CHECK: pred_mask selects the tiles to check (bit 1); skip_mask starts as a
     //          copy of it and loses the bit of every tile that is not skippable
     const uint32_t* pred_mask;
@@ -197,14 +197,17 @@ struct TcConfig {
     static constexpr int kG2Warp = kScore ? 2 : -1;
     static constexpr int kThreads = kEpiEnd * 32;
     // score register split: launch at kLaunchRegs (x kThreads <= 64K, multiple of 8),
-    // control warpgroup down to kCtrlRegs, drain warpgroup stays at kLaunchRegs,
-    // epilogue warpgroups up to kEpiRegs (the pool is what the launch allocated)
+    // control warpgroup down to kCtrlRegs, drain warpgroup up to kDrainRegs (its
+    // float-float sums + one tile's O + the tile centroid), epilogue warpgroups up to
+    // kEpiRegs (the pool is what the launch allocated)
     static constexpr int kLaunchRegs = kScore ? (65536 / kThreads) / 8 * 8 : 128;
     static constexpr int kCtrlRegs = FKDE_CTRL_REGS;
+    static constexpr int kDrainRegs = kScore ? 112 : 0;
     static constexpr int kEpiRegs =
-        kScore ? (kLaunchRegs * kThreads - 128 * kCtrlRegs - 128 * kLaunchRegs) / (128 * kNP) / 8 * 8
+        kScore ? (kLaunchRegs * kThreads - 128 * kCtrlRegs - 128 * kDrainRegs) / (128 * kNP) / 8 * 8
                : 0;
-    static_assert(!kScore || (kEpiRegs >= kLaunchRegs && kEpiRegs <= 256), "setmaxnreg split");
+    static_assert(!kScore || (kEpiRegs >= kLaunchRegs && kEpiRegs <= 256 && kDrainRegs >= kLaunchRegs),
+                  "setmaxnreg split");
     // B-stage ring: 96-column tiles are 12 KiB; the check pass finishes a tile in a
     // fraction of the score pass's time, so its ring covers many tiles of L2 latency
 #ifndef FKDE_SCORE_STAGES
@@ -320,7 +323,7 @@ pairwise_tc_kernel(PairArgs args) {
     // the column tiles a unit visits (score: clear skip bits; check: set pred bits)
     auto walk_of = [&](int rt, int ct1) {
         TileWalk w;
-        const uint32_t* m = kCheck ? args.pred_mask : (kScore ? args.skip_mask : nullptr);
+        const uint32_t* m = kCheck ? args.pred_mask : args.skip_mask;
         w.row = m ? m + (size_t)rt * args.mask_words : nullptr;
         w.end = ct1;
         w.want = kCheck ? ~0u : 0u;
@@ -499,6 +502,7 @@ pairwise_tc_kernel(PairArgs args) {
     }
     } else if (warp < Cfg::kEpi0) {
         if constexpr (kScore) {
+            ptx::setmaxnreg_inc<Cfg::kDrainRegs>();
             // ===================== O drain warps (score) =====================
             // Warp 4+q drains lane quadrant q of every O sub-unit (2^flush_log2
             // visited column tiles) in order: wait for GEMM2's commit, read T_hi,
@@ -511,6 +515,7 @@ pairwise_tc_kernel(PairArgs args) {
             const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
             const int lf = args.flush_log2;
             const int fmask = (1 << lf) - 1;
+            const float escale = exp2f(static_cast<float>(-args.sc->e));   // 2^-e (exact)
             uint32_t it_u = 0;
             for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
                 const int sp = u / args.n_row_tiles, rt = u % args.n_row_tiles;
@@ -523,23 +528,23 @@ pairwise_tc_kernel(PairArgs args) {
 #pragma unroll
                 for (int c = 0; c <= kMaxDim; ++c) ahi[c] = alo[c] = 0.f;
                 // centred GEMM2 (B2): one sub-unit per visited tile, whose centroid
-                // (scaled like the operands, 2^-e, exact) is added back as c_J * S
+                // (scaled like the operands, 2^-e, exact) is added back as c_J * S.
+                // The centroid is warp-uniform: every lane loads the same 16 floats
+                // (broadcast loads, issued before the o_full wait so the L2 round
+                // trip overlaps it) -- no shuffles on the drain's critical path.
                 const bool centred = args.opB2 != nullptr;
-                // lane c < 16 holds coordinate c of the current tile's centroid; the
-                // next visited tile's is loaded one tile ahead (an L2 round trip per
-                // tile on the drain's critical path throttled GEMM2 through o_empty)
                 int cct = centred ? wk.first(ct0) : 0;
-                float cl = 0.f, cl_next = 0.f;
-                if (centred && lane < kMaxDim && cct < ct1) cl_next = __ldg(args.cenB + (size_t)cct * kMaxDim + lane);
 #pragma unroll 1
                 for (int j = 0; j < nsub; ++j, ++it_u) {
                     const uint32_t g = it_u;
                     const uint32_t to = lane_addr + Cfg::kTmemO + (g & 1) * 64;
                     uint32_t od[16], ol[16], os_;
+                    float4 cj[4];
                     if (centred) {
-                        cl = cl_next;
+                        const float4* cp = reinterpret_cast<const float4*>(args.cenB + (size_t)cct * kMaxDim);
+#pragma unroll
+                        for (int w = 0; w < 4; ++w) cj[w] = __ldg(cp + w);
                         cct = wk.next();
-                        cl_next = (lane < kMaxDim && cct < ct1) ? __ldg(args.cenB + (size_t)cct * kMaxDim + lane) : 0.f;
                     }
                     FKDE_TRACE(4, g);
                     ptx::mbar_wait(&o_full[g & 1], (g >> 1) & 1);
@@ -557,15 +562,16 @@ pairwise_tc_kernel(PairArgs args) {
                     // tile the drain's instruction count is not negligible on the
                     // epilogue's sub-partitions)
                     const float sv = __uint_as_float(os_);
-                    const float cls = centred ? ldexpf(cl, -args.sc->e) : 0.f;   // scaled like the operands
+                    const float svs = sv * escale;   // S 2^-e: c_J (log2 units) -> operand scale
 #pragma unroll
                     for (int c = 0; c < kMaxDim; c += 2) {
                         float2 x = ptx::fadd2(make_float2(__uint_as_float(od[c]), __uint_as_float(od[c + 1])),
                                               make_float2(__uint_as_float(ol[c]), __uint_as_float(ol[c + 1])));
-                        if (centred)   // T = sum phi v + c_J S
-                            x = ptx::ffma2(make_float2(__shfl_sync(0xffffffffu, cls, c),
-                                                       __shfl_sync(0xffffffffu, cls, c + 1)),
-                                           make_float2(sv, sv), x);
+                        if (centred) {   // T = sum phi v + c_J S
+                            const float4 q = cj[c >> 2];
+                            x = ptx::ffma2((c & 2) ? make_float2(q.z, q.w) : make_float2(q.x, q.y),
+                                           make_float2(svs, svs), x);
+                        }
                         // 2Sum(ahi, x); a - b as fma(b, -1, a) (exact negation, one rounding)
                         const float2 m1 = make_float2(-1.f, -1.f);
                         const float2 a2 = make_float2(ahi[c], ahi[c + 1]);
@@ -653,7 +659,8 @@ pairwise_tc_kernel(PairArgs args) {
                 const uint32_t sidx = it_s + k;
                 const uint32_t sb = sidx % Cfg::kSBuf, ph = (sidx / Cfg::kSBuf) & 1;
                 int ct = ct0 + k;
-                if (!dense) {   // the visited tile's column index, from its B stage
+                if (Cfg::kScoreTiling && !dense) {   // the visited tile's column index, from its B stage
+                    // (the density passes never need it)
                     const uint32_t st = sidx % kStages;
                     ptx::mbar_wait(&b_full[st], (sidx / kStages) & 1);   // (complete: GEMM1 used it)
                     ct = *reinterpret_cast<volatile int*>(&stage_ct[st]);

@@ -439,6 +439,11 @@ struct ReduceArgs {
     unsigned int* flag_count;   // rows whose Gaussian mass underflows fp32 ranges
     unsigned int* flag_rows;
     const uint8_t* risk;        // pack's spread flags (local rows) or nullptr
+    // density tile skipping (nullptr: none): skipped tiles per 128-row tile; a row
+    // whose term mass |ca| s0 + |cb| |s1| (the scale of the fp32 sums' own rounding
+    // of the row) is below skip_tiles * skip_flag_mass is flagged
+    const unsigned int* skip_tiles;
+    double skip_flag_mass;
 };
 
 __global__ void reduce_density(ReduceArgs a) {
@@ -450,7 +455,10 @@ __global__ void reduce_density(ReduceArgs a) {
     for (int p = 0; p < a.nparts; ++p) s0 += static_cast<double>(a.part0[p * a.rows_pad + j]);
     if (a.part1)
         for (int p = 0; p < a.nparts; ++p) s1 += static_cast<double>(a.part1[p * a.rows_pad + j]);
-    if (a.flag_rows && (s0 < kDensityFlagMass || (a.risk && a.risk[j]))) {
+    const bool skipped_mass =
+        a.skip_tiles && fabs(a.ca) * s0 + fabs(a.cb * s1) <
+                            static_cast<double>(a.skip_tiles[j / kTileRows]) * a.skip_flag_mass;
+    if (a.flag_rows && (s0 < kDensityFlagMass || (a.risk && a.risk[j]) || skipped_mass)) {
         a.flag_rows[atomicAdd(a.flag_count, 1u)] = static_cast<unsigned int>(j);
         return;
     }

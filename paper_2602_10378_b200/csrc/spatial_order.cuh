@@ -206,7 +206,7 @@ constexpr int kBoxFloats = 38;
 __global__ void __launch_bounds__(128) tile_summary(const double* __restrict__ x, size_t n, int d,
                                                     const PassScalars* __restrict__ sc,
                                                     const OrderScalars* __restrict__ os, double k,
-                                                    int tile_w, float* __restrict__ cen,
+                                                    int tile_w, int centred, float* __restrict__ cen,
                                                     float* __restrict__ box) {
     __shared__ float red[4][3][kMaxDim + kOrderAxes];   // per warp: sum, min, max
     const size_t r0 = static_cast<size_t>(blockIdx.x) * tile_w;
@@ -218,7 +218,8 @@ __global__ void __launch_bounds__(128) tile_summary(const double* __restrict__ x
     {
         double y[kMaxDim];
 #pragma unroll
-        for (int c = 0; c < kMaxDim; ++c) y[c] = (valid && c < d) ? (x[r * d + c] - sc->mu[c]) * k : 0.0;
+        for (int c = 0; c < kMaxDim; ++c)
+            y[c] = (valid && c < d) ? (x[r * d + c] - (centred ? 0.0 : sc->mu[c])) * k : 0.0;
 #pragma unroll
         for (int c = 0; c < kMaxDim; ++c) sum[c] = static_cast<float>(y[c]);
 #pragma unroll
@@ -281,6 +282,7 @@ __global__ void __launch_bounds__(128) tile_summary(const double* __restrict__ x
 //   * predicted: centroid half-distance^2 > thresh -> checked exactly by the
 //     check pass (pred 1, skip 1 until the check clears it);
 //   * otherwise computed (pred 0, skip 0).
+// skip_count (optional, zeroed by the caller): += skipped tiles per row tile.
 // Block = 128 row tiles (one per thread) x kPredWords mask words (32 column tiles
 // each): the column tiles' summaries are staged once in shared memory, so each
 // summary is read from global memory once per 128 row tiles (a thread per (row
@@ -293,7 +295,8 @@ __global__ void __launch_bounds__(128) tile_predict(const float* __restrict__ ce
                                                     const float* __restrict__ boxB, int col_tiles,
                                                     int words, float thresh, float proven_half_r2,
                                                     uint32_t* __restrict__ pred,
-                                                    uint32_t* __restrict__ skip) {
+                                                    uint32_t* __restrict__ skip,
+                                                    unsigned int* __restrict__ skip_count) {
     pdl_launch_dependents();
     pdl_wait();
     __shared__ float colsum[kPredWords * 32][kSumFloats];
@@ -313,6 +316,7 @@ __global__ void __launch_bounds__(128) tile_predict(const float* __restrict__ ce
     for (int c = 0; c < kMaxDim; ++c) a[c] = cenA[(size_t)rt * kMaxDim + c];
 #pragma unroll
     for (int c = 0; c < kBoxFloats; ++c) ab[c] = boxA[(size_t)rt * kBoxFloats + c];
+    unsigned int nskip = 0;
     for (int wi = 0; wi < kPredWords && w0 + wi < words; ++wi) {
         uint32_t pbits = 0, sbits = 0;
         for (int b = 0; b < 32; ++b) {
@@ -352,7 +356,9 @@ __global__ void __launch_bounds__(128) tile_predict(const float* __restrict__ ce
         const size_t t = (size_t)rt * words + w0 + wi;
         pred[t] = pbits;
         skip[t] = sbits;
+        nskip += __popc(sbits);
     }
+    if (skip_count && nskip) atomicAdd(skip_count + rt, nskip);
 }
 
 }  // namespace fkde_b200

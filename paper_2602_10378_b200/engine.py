@@ -109,11 +109,15 @@ class Context:
         return int(self._lib.fkde_gpu_last_launch_count(self._h))
 
     def skip_stats(self) -> dict:
-        """Tile skipping of the last score pass (fkde_gpu_last_skip_stats)."""
-        b = (ctypes.c_uint64 * 4)()
-        self._lib.fkde_gpu_last_skip_stats(self._h, b)
+        """Tile skipping of the last call's score pass (and, under "density",
+        its density pass) -- fkde_gpu_last_skip_stats."""
+        b = (ctypes.c_uint64 * N.SKIP_STATS_COUNT)()
+        self._lib.fkde_gpu_last_skip_stats(self._h, b, N.SKIP_STATS_COUNT)
         return {"tiles_checked": int(b[0]), "tiles_skipped": int(b[1]),
-                "tiles_total": int(b[2]), "spatial_order": bool(b[3])}
+                "tiles_total": int(b[2]), "spatial_order": bool(b[3]),
+                "direct_rows": int(b[8]),
+                "density": {"tiles_skipped": int(b[4]), "tiles_total": int(b[5]),
+                            "spatial_order": bool(b[6]), "direct_rows": int(b[7])}}
 
     def workspace_bytes(self) -> int:
         b = ctypes.c_size_t(0)
