@@ -447,6 +447,9 @@ Status density_pass(Device& D, const Options& o, int mode, size_t rows_pad, size
     a.diag_row0 = -1;
     a.skip_mask = const_cast<uint32_t*>(skip_mask);
     a.mask_words = mask_words;
+#ifdef FKDE_CTA_TIMES
+    a.trace = o.trace;
+#endif
     if (mode == kModeGauss)
         STATUS_TRY(launch_pairwise<kModeGauss>(D, o, a, n_cols));
     else
@@ -697,6 +700,11 @@ Status score_program(Device& D, const Options& o, const Job& J, const double* dX
         PairArgs c = a;
         c.opB2 = nullptr;
         c.cenB = nullptr;
+#ifdef FKDE_CTA_TIMES
+        if (true) {
+            c.trace = a.trace;   // (regions per MODE)
+        } else
+#endif
         if (std::getenv("FKDE_TRACE_CHECK")) {   // debug: trace the check pass, not the score pass
             c.trace = a.trace;
             a.trace = nullptr;

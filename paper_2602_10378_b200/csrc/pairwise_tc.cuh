@@ -318,6 +318,11 @@ pairwise_tc_kernel(PairArgs args) {
     const uint32_t tmem_base = *tmem_slot;
     // (barriers and TMEM are set up while the previous kernel of the chain drains)
     pdl_wait();
+#ifdef FKDE_CTA_TIMES
+    // debug build (tools/cta_balance.py): per-CTA start / end globaltimer and the
+    // number of tiles the CTA visited, region MODE * 4096 of args.trace
+    if (args.trace && threadIdx.x == 0) args.trace[MODE * 4096 + 2 * blockIdx.x] = ptx::globaltimer();
+#endif
 
     const int n_units = args.n_row_tiles * args.splits;
     // the column tiles a unit visits (score: clear skip bits; check: set pred bits)
@@ -797,12 +802,18 @@ pairwise_tc_kernel(PairArgs args) {
             }
             it_s += static_cast<uint32_t>(len);
         }
+#ifdef FKDE_CTA_TIMES
+        if (args.trace && warp == Cfg::kEpi0 && lane == 0) args.trace[MODE * 4096 + 2048 + blockIdx.x] = it_s;
+#endif
         if (kCheck && args.stats && lane == 0 && q == 0 && n_checked)
             atomicAdd(&args.stats[0], n_checked);
     }
 
     ptx::tc_fence_before();
     __syncthreads();
+#ifdef FKDE_CTA_TIMES
+    if (args.trace && threadIdx.x == 0) args.trace[MODE * 4096 + 2 * blockIdx.x + 1] = ptx::globaltimer();
+#endif
     if (warp == 1) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc<Cfg::kTmemCols>(tmem_base);
