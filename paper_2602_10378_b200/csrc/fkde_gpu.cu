@@ -191,6 +191,7 @@ struct Device {
     DevBuf X, Y, opA, opB, opB2, part0, part1, xsd, out, aux0, aux1, colpart, scal, err, flags;
     DevBuf risk, dpart, ddone;   // direct_rows_kernel: spread flags, partials, counters
     DevBuf pdone;                // prep_stats / scale_two completion counters (self-resetting)
+    DevBuf sched;                // pairwise kernels' unit schedulers, 2 per mode (self-resetting)
     DevBuf qmax;                 // scale_two per-block maxima
     // spatial order of the score pass (spatial_order.cuh): sorted points, permutation,
     // keys, CUB scratch, axes, tile centroids, skip statistics, un-permuted outputs
@@ -218,7 +219,7 @@ struct Device {
     std::vector<DevBuf*> buffers() {   // every device workspace (free / size accounting)
         return {&X,     &Y,     &opA,  &opB,    &opB2,  &part0, &part1,     &xsd,     &out,
                 &aux0,  &aux1,  &colpart, &scal, &err,  &flags, &risk,      &dpart,   &ddone,
-                &pdone, &qmax,  &Xs,   &perm,   &keys,  &cubtmp, &ordsc,    &cenA,    &cenB,
+                &pdone, &sched, &qmax,  &Xs,   &perm,   &keys,  &cubtmp, &ordsc,    &cenA,    &cenB,
                 &boxA,  &boxB,  &skipstats, &unperm0, &unperm1, &pmask, &smask, &Qs, &qperm,
                 &qkeys, &qcubtmp, &qskip, &qout};
     }
@@ -331,8 +332,10 @@ Status launch_pairwise(Device& D, const Options& o, const PairArgs& a, size_t n_
         const int units = a.n_row_tiles * a.splits;
         int grid = std::min(units, D.num_sms);
         if (o.max_ctas > 0) grid = std::min(grid, o.max_ctas);
+        PairArgs b = a;
+        b.sched = D.sched.as<unsigned int>() + 2 * MODE;   // (ensure_call_scratch)
         CUDA_TRY(launch_chain(o.pdl, pairwise_tc_kernel<MODE>, dim3(grid), dim3(Cfg::kThreads),
-                              Cfg::kSmemBytes, D.stream, a));
+                              Cfg::kSmemBytes, D.stream, b));
     }
     ++D.launches;
     CUDA_TRY(cudaGetLastError());
@@ -357,6 +360,10 @@ Status ensure_call_scratch(Device& D, size_t flag_rows) {
     if (!D.pdone.p) {   // counters start at zero and reset themselves
         STATUS_TRY(ensure(D.pdone, 4 * sizeof(unsigned int)));
         CUDA_TRY(cudaMemsetAsync(D.pdone.p, 0, D.pdone.bytes, D.stream));
+    }
+    if (!D.sched.p) {
+        STATUS_TRY(ensure(D.sched, 8 * sizeof(unsigned int)));
+        CUDA_TRY(cudaMemsetAsync(D.sched.p, 0, D.sched.bytes, D.stream));
     }
     return {};
 }
@@ -515,6 +522,9 @@ constexpr size_t kSpatialMinN = 32768;
 // centroid half-distance^2 (log2 units) above which a tile pair is checked for
 // skipping: skipping needs max log2 phi' < -26, i.e. r^2/2 > 41 for every pair
 constexpr float kSkipPredict = 40.0f;
+// score pass on the spatial order: O is drained at every change of the B2 tile group
+// (kB2GroupLog2 column tiles, pairwise_tc.cuh) or after kCentredFlush visited tiles
+constexpr int kCentredFlush = 4;
 
 bool use_spatial(const Options& o, size_t n) {
     return o.spatial == 1 || o.spatial == 3 || (o.spatial == 0 && n >= kSpatialMinN);
@@ -667,6 +677,7 @@ Status score_program(Device& D, const Options& o, const Job& J, const double* dX
         STATUS_TRY(pack_args(D, dX, n, d, 2, true, ks, sc, D.opB2, &b2_pad, &p2, col_align));
         p2.cen = D.cenB.as<float>();
         p2.cen_tile = static_cast<int>(kScoreNCol);
+        p2.ones_mask = (1 << kB2GroupLog2) - 1;
         pack_operands<<<grid1(b2_pad, 128), 128, 0, D.stream>>>(p2);
         D.launches += 3;
         CUDA_TRY(cudaGetLastError());
@@ -674,7 +685,9 @@ Status score_program(Device& D, const Options& o, const Job& J, const double* dX
         if (!no_b2) {
             a.opB2 = D.opB2.as<uint8_t>();
             a.cenB = D.cenB.as<float>();
+            const int fl = o.flush_tiles > 0 ? o.flush_tiles : kCentredFlush;
             a.flush_log2 = 0;
+            while ((2 << a.flush_log2) <= fl) ++a.flush_log2;
         }
     }
     if (D.ordered && o.spatial != 3) {

@@ -80,9 +80,16 @@ struct PairArgs {
     uint32_t* skip_mask;
     int mask_words;
     unsigned long long* stats;   // CHECK (optional): [0] += tiles checked
+    // dynamic unit scheduler: [0] next unit (atomic fetch-and-add by each CTA's
+    // producer), [1] CTAs finished; both zero at launch, reset by the last CTA
+    unsigned int* sched;
     // SCORE on the spatial order (nullptr otherwise): GEMM2's column operand centred
     // per column tile (layout.cuh "B2") and the column-tile centroids the drain adds
-    // back (log2 units, unscaled); the drain then runs after every visited tile
+    // back (log2 units, unscaled).  Tiles are grouped by 2^kB2GroupLog2 consecutive
+    // column tiles; tile J's ones column is 16 + (J mod 2^kB2GroupLog2), so an O
+    // sub-unit may hold several tiles of one group and still give each tile's own
+    // S_J for its centroid term c_J S_J.  A sub-unit never spans two groups: it ends
+    // at a group change or after 2^flush_log2 visited tiles.
     const uint8_t* opB2;
     const float* cenB;
     // debug (builds with -DFKDE_ENABLE_TRACE only): per-event clock64 trace of
@@ -92,6 +99,8 @@ struct PairArgs {
 // log2 phi' (S * dscale, with the 2^15 offset) below which both fp16 halves of
 // phi' are exactly zero (phi' < 2^-25 rounds to zero; one unit of margin for ex2.approx)
 constexpr float kSkipLog2 = -26.0f;
+// score pass on the spatial order: column tiles per B2 group (ones columns 16..19)
+constexpr int kB2GroupLog2 = 2;
 
 #ifdef FKDE_ENABLE_TRACE
 #define FKDE_TRACE(slot, tile)                                                               \
@@ -226,14 +235,20 @@ struct TcConfig {
     static_assert(kNCol % 32 == 0 && kColBytes % 1024 == 0, "column tiles of whole SW128 atoms");
     static constexpr uint32_t kBStride = kScore ? 2 * kColBytes : kColBytes;   // B (+ B2) per stage
     static constexpr uint32_t kOffB = 2 * kTileBytes;
-    static constexpr uint32_t kOffBar = kOffB + kStages * kBStride;
+    static constexpr uint32_t kOffCen = kOffB + kStages * kBStride;   // score: drain centroid ring
+    static constexpr uint32_t kCenBytes = kScore ? 4 * (1u << kB2GroupLog2) * kMaxDim * 4 : 0;
+    static constexpr uint32_t kOffBar = kOffCen + kCenBytes;
     // S accumulators in TMEM.  Score: 4 S/P buffers of 96 columns (a tile's S is
     // overwritten by its P; the buffer is free again once GEMM2 has read P) +
     // O[2] at column 384.  KDE: 4 of 128, check: 5 of 96 (freed once S is loaded).
     static constexpr int kSBuf = kScore ? 384 / kNCol : (kCheck ? 512 / kNCol : 4);
-    static constexpr uint32_t kNumBars = 4 + 2 * kStages + 4 * kSBuf + 4;
+    // unit queue: the producer fetches units (dynamic scheduling) and hands them to
+    // the other warps through kQ shared slots
+    static constexpr int kQ = 4;
+    static constexpr int kConsumers = (kEpiEnd - 1) - (kScore ? 1 : 0);   // warps taking units
+    static constexpr uint32_t kNumBars = 4 + 2 * kStages + 4 * kSBuf + 4 + 2 * kQ;
     // + tmem slot + stage column table, 1 KiB alignment slack
-    static constexpr uint32_t kSmemBytes = kOffBar + kNumBars * 8 + 16 + 4 * kStages + 1024;
+    static constexpr uint32_t kSmemBytes = kOffBar + kNumBars * 8 + 16 + 4 * kStages + 4 * kQ + 1024;
     static constexpr uint32_t kTmemCols = 512;
     static constexpr uint32_t kTmemO = 384;   // score: O[2] (2 x 64 cols: T_hi, S, T_lo)
     static_assert(!kScore || kSBuf * kNCol <= kTmemO, "S/P buffers overlap O");
@@ -249,6 +264,11 @@ struct TcConfig {
 #ifndef FKDE_SPLIT
 #define FKDE_SPLIT 0
 #endif
+// score drain: per-row sums of the O sub-units in fp64 (1: F2F + DADD per value) or
+// float-float (0: 2Sum in packed f32x2)
+#ifndef FKDE_DRAIN_F64
+#define FKDE_DRAIN_F64 0
+#endif
 // GEMM2 N for the P_lo half: 32 (y_hi + the ones block; P_lo . y_lo dropped) or 48
 #ifndef FKDE_G2_LO_N
 #define FKDE_G2_LO_N 32
@@ -263,8 +283,8 @@ pairwise_tc_kernel(PairArgs args) {
     constexpr int kStages = Cfg::kStages;
 
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                               ~static_cast<uintptr_t>(1023));
+    const uint32_t smem_s = ptx::smem_u32(smem_raw);
+    uint8_t* smem = smem_raw + (((smem_s + 1023u) & ~1023u) - smem_s);
     uint8_t* smA = smem + Cfg::kOffA;
     uint8_t* smB = smem + Cfg::kOffB;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::kOffBar);
@@ -279,10 +299,13 @@ pairwise_tc_kernel(PairArgs args) {
     uint64_t* s_free = p_full + kSB;      // [kSB] score: GEMM2 done reading P (S buffer reusable)
     uint64_t* o_full = s_free + kSB;      // [2]
     uint64_t* o_empty = o_full + 2;       // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
+    uint64_t* uq_full = o_empty + 2;      // [kQ] unit queue
+    uint64_t* uq_empty = uq_full + Cfg::kQ;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(uq_empty + Cfg::kQ);
     // the column tile each B stage holds (written by the producer before the stage's
     // b_full arrive): the other warps look it up instead of walking the tile mask
     int* stage_ct = reinterpret_cast<int*>(tmem_slot + 1);   // [kStages]
+    int* uq_slot = stage_ct + kStages;                        // [kQ]
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -308,6 +331,10 @@ pairwise_tc_kernel(PairArgs args) {
             ptx::mbar_init(&o_full[i], 1);
             ptx::mbar_init(&o_empty[i], 4);
         }
+        for (int i = 0; i < Cfg::kQ; ++i) {
+            ptx::mbar_init(&uq_full[i], 1);
+            ptx::mbar_init(&uq_empty[i], Cfg::kConsumers);
+        }
         ptx::fence_barrier_init();
     }
     pdl_launch_dependents();
@@ -325,6 +352,34 @@ pairwise_tc_kernel(PairArgs args) {
 #endif
 
     const int n_units = args.n_row_tiles * args.splits;
+    // Dynamic scheduling: the producer warp fetches the next unit from a global
+    // counter when it is ready to stream it (units stay in chunk-major order, so the
+    // CTAs running at any time still share one column chunk in L2) and publishes it
+    // in the unit queue; every other role takes the units from the queue in the
+    // same order (-1 ends the kernel).  A CTA that drew short units simply draws
+    // more: the per-CTA work no longer depends on which rows sit where.
+    auto publish_unit = [&](uint32_t qi) -> int {
+        const uint32_t sl = qi % Cfg::kQ;
+        int u = 0;
+        if (lane == 0) u = static_cast<int>(atomicAdd(args.sched, 1u));
+        u = __shfl_sync(0xffffffffu, u, 0);
+        if (u >= n_units) u = -1;
+        ptx::mbar_wait(&uq_empty[sl], ((qi / Cfg::kQ) & 1) ^ 1);
+        if (lane == 0) {
+            uq_slot[sl] = u;
+            ptx::mbar_arrive(&uq_full[sl]);   // (release: the slot write)
+        }
+        __syncwarp();
+        return u;
+    };
+    auto take_unit = [&](uint32_t qi) -> int {
+        const uint32_t sl = qi % Cfg::kQ;
+        ptx::mbar_wait(&uq_full[sl], (qi / Cfg::kQ) & 1);
+        const int u = *reinterpret_cast<volatile int*>(&uq_slot[sl]);
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&uq_empty[sl]);
+        return u;
+    };
     // the column tiles a unit visits (score: clear skip bits; check: set pred bits)
     auto walk_of = [&](int rt, int ct1) {
         TileWalk w;
@@ -347,7 +402,9 @@ pairwise_tc_kernel(PairArgs args) {
         // loops around the uniform-register operands); one elected lane issues.
         const uint64_t pol_b = ptx::policy_evict_last();
         uint32_t it_a = 0, it_b = 0;
-        for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        for (uint32_t qi = 0;; ++qi) {
+            const int u = publish_unit(qi);
+            if (u < 0) break;
             // chunk-major unit order: CTAs running concurrently share one column
             // chunk, which therefore stays L2-resident while they stream it
             const int sp = u / args.n_row_tiles, rt = u % args.n_row_tiles;
@@ -412,14 +469,27 @@ pairwise_tc_kernel(PairArgs args) {
         // drain warps; two O buffers alternate so the drain overlaps the next
         // sub-unit.  This bounds the tensor core's fp32 accumulation length (its
         // truncation error grows with the accumulator magnitude x the number of steps).
-        const int fmask = (1 << args.flush_log2) - 1;
-        for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        // sub-unit boundaries (identical in the drain warps): a new sub-unit starts at
+        // the unit's first visited tile, when the column-tile group changes (centred
+        // B2) and after 2^flush_log2 tiles.  The GEMM2 warp walks the tile mask itself
+        // (it knows the next tile's group without waiting for its stage), so the
+        // sub-unit's o_full commit follows its last MMAs at once: the drain, and
+        // with it the O buffer's release, is not held back by the next tile's p_full.
+        const int fcap = 1 << args.flush_log2;
+        const bool grouped = kScore && args.opB2 != nullptr;
+        constexpr int glog = kB2GroupLog2;
+        for (uint32_t qi = 0;; ++qi) {
+            const int u = take_unit(qi);
+            if (u < 0) break;
             const int sp = u / args.n_row_tiles, rt = u % args.n_row_tiles;
             const int ct0 = static_cast<int>((long long)sp * args.n_col_tiles / args.splits);
             const int ct1 = static_cast<int>((long long)(sp + 1) * args.n_col_tiles / args.splits);
-            // (the issuers only need how many tiles the unit visits, not which)
-            const int len = walk_of(rt, ct1).count(ct0);
+            // (GEMM1 only needs how many tiles the unit visits, not which)
+            TileWalk wk2 = walk_of(rt, ct1);
+            const int len = wk2.count(ct0);
             if (len == 0) continue;
+            int sub_cnt = 0;
+            int cur_ct = (kScore && !g1) ? wk2.first(ct0) : 0;
             const int ab = it_a & 1;
             if (g1) {
                 ptx::mbar_wait(&a_full[ab], (it_a >> 1) & 1);
@@ -465,18 +535,23 @@ pairwise_tc_kernel(PairArgs args) {
                     __syncwarp();
                     FKDE_TRACE(4, it_s);
                 } else if constexpr (kScore) {
-                    const bool first = (rel & fmask) == 0;
-                    const bool last = (rel & fmask) == fmask || rel == len - 1;
-                    const uint32_t ob = it_u & 1;
+                    const int next_ct = wk2.next();
+                    const bool first = sub_cnt == 0;
+                    ++sub_cnt;
+                    const bool last = rel == len - 1 || sub_cnt == fcap ||
+                                      (grouped && (next_ct >> glog) != (cur_ct >> glog));
+                    cur_ct = next_ct;
                     FKDE_TRACE(2, it_s);
                     ptx::mbar_wait(&p_full[sb], ph);
                     FKDE_TRACE(3, it_s);
+                    const uint32_t ob = it_u & 1;
                     if (first) ptx::mbar_wait(&o_empty[ob], ((it_u >> 1) & 1) ^ 1);
                     ptx::tc_fence_after();
                     if (ptx::elect_one()) {
                         const uint64_t db0 = descBmn + ((st * Cfg::kBStride) >> 4);
                         const uint32_t ta0 = tmem_base + sb * Cfg::kNCol;
                         const uint32_t to = tmem_base + Cfg::kTmemO + ob * 64;
+#ifndef FKDE_DBG_NO_G2MMA
 #pragma unroll
                         for (int k = 0; k < Cfg::kNCol / 16; ++k) {
 #pragma unroll
@@ -487,13 +562,17 @@ pairwise_tc_kernel(PairArgs args) {
                                                  (first && part == 0 && k == 0) ? 0u : 1u);
                             }
                         }
+#endif
                         ptx::umma_commit(&b_empty[st]);
                         ptx::umma_commit(&s_free[sb]);
                         if (last) ptx::umma_commit(&o_full[ob]);
                     }
                     __syncwarp();
                     FKDE_TRACE(5, it_s);
-                    if (last) ++it_u;
+                    if (last) {
+                        ++it_u;
+                        sub_cnt = 0;
+                    }
                 }
                 ++it_b;
                 ++it_s;
@@ -502,6 +581,7 @@ pairwise_tc_kernel(PairArgs args) {
                 if (ptx::elect_one()) ptx::umma_commit(&a_empty[ab]);
                 __syncwarp();
             }
+
             ++it_a;
         }
     }
@@ -518,65 +598,102 @@ pairwise_tc_kernel(PairArgs args) {
             const int q = warp & 3;
             const int r = q * 32 + lane;
             const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
-            const int lf = args.flush_log2;
-            const int fmask = (1 << lf) - 1;
+            const int fcap = 1 << args.flush_log2;
+            constexpr int glog = kB2GroupLog2;
+            constexpr int gmask = (1 << glog) - 1;
             const float escale = exp2f(static_cast<float>(-args.sc->e));   // 2^-e (exact)
+            // centred GEMM2 (B2): each tile J of a sub-unit adds c_J S_J (c_J scaled
+            // like the operands, 2^-e, exact; S_J from J's own ones column).  The
+            // centroids are copied into this warp's shared-memory ring (cp.async,
+            // slot J mod 2^glog) when the tile joins the sub-unit, a tile or more
+            // before the drain reads them (broadcast) -- no L2 round trip on the path
+            // that releases O to GEMM2, and no registers held for them.
+            const bool centred = args.opB2 != nullptr;
+            const uint32_t cring = ptx::smem_u32(smem + Cfg::kOffCen) + q * ((1u << glog) * kMaxDim * 4);
+            const float* cring_p = reinterpret_cast<const float*>(smem + Cfg::kOffCen) + q * (1 << glog) * kMaxDim;
             uint32_t it_u = 0;
-            for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+            for (uint32_t qi = 0;; ++qi) {
+            const int u = take_unit(qi);
+            if (u < 0) break;
                 const int sp = u / args.n_row_tiles, rt = u % args.n_row_tiles;
                 const int ct0 = static_cast<int>((long long)sp * args.n_col_tiles / args.splits);
                 const int ct1 = static_cast<int>((long long)(sp + 1) * args.n_col_tiles / args.splits);
                 TileWalk wk = walk_of(rt, ct1);
                 const int len = wk.count(ct0);
-                const int nsub = (len + fmask) >> lf;
+#if FKDE_DRAIN_F64
+                double acc[kMaxDim + 1];
+#pragma unroll
+                for (int c = 0; c <= kMaxDim; ++c) acc[c] = 0.0;
+#else
                 float ahi[kMaxDim + 1], alo[kMaxDim + 1];
 #pragma unroll
                 for (int c = 0; c <= kMaxDim; ++c) ahi[c] = alo[c] = 0.f;
-                // centred GEMM2 (B2): one sub-unit per visited tile, whose centroid
-                // (scaled like the operands, 2^-e, exact) is added back as c_J * S.
-                // The centroid is warp-uniform: every lane loads the same 16 floats
-                // (broadcast loads, issued before the o_full wait so the L2 round
-                // trip overlaps it) -- no shuffles on the drain's critical path.
-                const bool centred = args.opB2 != nullptr;
-                int cct = centred ? wk.first(ct0) : 0;
+#endif
+                int pend = 0, cur_grp = -1;
+                uint32_t pmask = 0;   // ring slots (tiles) of the pending sub-unit
+                int ct = len > 0 ? wk.first(ct0) : ct1;
+                // the sub-unit schedule of the GEMM2 issuer, replayed from the tile walk;
+                // k == len drains the last sub-unit
 #pragma unroll 1
-                for (int j = 0; j < nsub; ++j, ++it_u) {
-                    const uint32_t g = it_u;
+                for (int k = 0; k <= len; ++k) {
+                    const int grp = (k < len && centred) ? (ct >> glog) : 0;
+                    if (pend > 0 && (k == len || grp != cur_grp || pend == fcap)) {
+                    const uint32_t g = it_u++;
+                    pend = 0;
                     const uint32_t to = lane_addr + Cfg::kTmemO + (g & 1) * 64;
-                    uint32_t od[16], ol[16], os_;
-                    float4 cj[4];
-                    if (centred) {
-                        const float4* cp = reinterpret_cast<const float4*>(args.cenB + (size_t)cct * kMaxDim);
-#pragma unroll
-                        for (int w = 0; w < 4; ++w) cj[w] = __ldg(cp + w);
-                        cct = wk.next();
-                    }
+                    uint32_t od[16], ol[16], os4[4];
                     FKDE_TRACE(4, g);
                     ptx::mbar_wait(&o_full[g & 1], (g >> 1) & 1);
                     FKDE_TRACE(5, g);
                     ptx::tc_fence_after();
                     ptx::tmem_ld16(to, od);
-                    ptx::tmem_ld1(to + 16, os_);
+                    ptx::tmem_ld4(to + 16, os4);   // S_J per ring slot (non-centred: 16-18 = S)
                     ptx::tmem_ld16(to + 32, ol);
                     ptx::tmem_ld_wait();
                     ptx::tc_fence_before();
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(&o_empty[g & 1]);
-                    // x = T_hi + T_lo (+ c_J S when centred), then 2Sum into the
-                    // float-float sums -- all in packed f32x2 pairs (with a drain per
-                    // tile the drain's instruction count is not negligible on the
-                    // epilogue's sub-partitions)
-                    const float sv = __uint_as_float(os_);
-                    const float svs = sv * escale;   // S 2^-e: c_J (log2 units) -> operand scale
+                    // x = T_hi + T_lo (+ sum_J c_J S_J when centred), then 2Sum into the
+                    // float-float sums -- all in packed f32x2 pairs
+                    float sv = __uint_as_float(os4[0]);
+                    float2 xs[kMaxDim / 2];
+#pragma unroll
+                    for (int c = 0; c < kMaxDim; c += 2)
+                        xs[c >> 1] = ptx::fadd2(make_float2(__uint_as_float(od[c]), __uint_as_float(od[c + 1])),
+                                                make_float2(__uint_as_float(ol[c]), __uint_as_float(ol[c + 1])));
+                    if (centred) {
+                        ptx::cp_async_wait_all();
+                        __syncwarp();
+                        sv = 0.f;
+#pragma unroll
+                        for (int sl = 0; sl <= gmask; ++sl) {
+                            if (!(pmask & (1u << sl))) continue;   // (warp-uniform)
+                            const float sj = __uint_as_float(os4[sl]);
+                            sv += sj;
+                            const float sjs = sj * escale;   // S_J 2^-e: c_J (log2 units) -> operand scale
+                            const float4* cp = reinterpret_cast<const float4*>(cring_p + sl * kMaxDim);
+#pragma unroll
+                            for (int w = 0; w < 4; ++w) {
+                                const float4 cq = cp[w];
+                                xs[2 * w] = ptx::ffma2(make_float2(cq.x, cq.y), make_float2(sjs, sjs), xs[2 * w]);
+                                xs[2 * w + 1] = ptx::ffma2(make_float2(cq.z, cq.w), make_float2(sjs, sjs), xs[2 * w + 1]);
+                            }
+                        }
+                    }
+                    pmask = 0;
+#ifdef FKDE_DBG_NO_DRAIN_MATH
+                    if (xs[0].x == 12345.f) ahi[0] += sv;   // (keeps the loads alive)
+#elif FKDE_DRAIN_F64
 #pragma unroll
                     for (int c = 0; c < kMaxDim; c += 2) {
-                        float2 x = ptx::fadd2(make_float2(__uint_as_float(od[c]), __uint_as_float(od[c + 1])),
-                                              make_float2(__uint_as_float(ol[c]), __uint_as_float(ol[c + 1])));
-                        if (centred) {   // T = sum phi v + c_J S
-                            const float4 q = cj[c >> 2];
-                            x = ptx::ffma2((c & 2) ? make_float2(q.z, q.w) : make_float2(q.x, q.y),
-                                           make_float2(svs, svs), x);
-                        }
+                        acc[c] += static_cast<double>(xs[c >> 1].x);
+                        acc[c + 1] += static_cast<double>(xs[c >> 1].y);
+                    }
+                    acc[kMaxDim] += static_cast<double>(sv);
+#else
+#pragma unroll
+                    for (int c = 0; c < kMaxDim; c += 2) {
+                        const float2 x = xs[c >> 1];
                         // 2Sum(ahi, x); a - b as fma(b, -1, a) (exact negation, one rounding)
                         const float2 m1 = make_float2(-1.f, -1.f);
                         const float2 a2 = make_float2(ahi[c], ahi[c + 1]);
@@ -596,14 +713,34 @@ pairwise_tc_kernel(PairArgs args) {
                         alo[kMaxDim] += (ahi[kMaxDim] - (s2 - bb)) + (sv - bb);
                         ahi[kMaxDim] = s2;
                     }
+#endif
+                    }
+                    if (k == len) break;
+                    if (pend == 0) cur_grp = grp;   // a new sub-unit
+                    if (centred) {   // tile ct joins it: its centroid into ring slot ct mod 2^glog
+                        const int sl = ct & gmask;
+                        if (lane < 4)
+                            ptx::cp_async16(cring + (sl * kMaxDim + lane * 4) * 4,
+                                            args.cenB + (size_t)ct * kMaxDim + lane * 4);
+                        ptx::cp_async_commit();
+                        pmask |= 1u << sl;
+                    }
+                    ++pend;
+                    ct = wk.next();
                 }
                 const size_t idx = static_cast<size_t>(sp) * args.rows_pad + static_cast<size_t>(rt) * kTileRows + r;
-                args.dpart0[idx] = static_cast<double>(ahi[kMaxDim]) + static_cast<double>(alo[kMaxDim]);
                 double2* t = reinterpret_cast<double2*>(args.dpart1 + idx * kMaxDim);
+#if FKDE_DRAIN_F64
+                args.dpart0[idx] = acc[kMaxDim];
+#pragma unroll
+                for (int w = 0; w < kMaxDim / 2; ++w) t[w] = make_double2(acc[2 * w], acc[2 * w + 1]);
+#else
+                args.dpart0[idx] = static_cast<double>(ahi[kMaxDim]) + static_cast<double>(alo[kMaxDim]);
 #pragma unroll
                 for (int w = 0; w < kMaxDim / 2; ++w)
                     t[w] = make_double2(static_cast<double>(ahi[2 * w]) + static_cast<double>(alo[2 * w]),
                                         static_cast<double>(ahi[2 * w + 1]) + static_cast<double>(alo[2 * w + 1]));
+#endif
             }
         }
     } else if (warp < Cfg::kEpiEnd) {
@@ -630,7 +767,9 @@ pairwise_tc_kernel(PairArgs args) {
         const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
         uint32_t it_s = 0;                           // global visited-tile counter (all phases)
         unsigned long long n_checked = 0;            // check statistics (quadrant 0 counts)
-        for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        for (uint32_t qi = 0;; ++qi) {
+            const int u = take_unit(qi);
+            if (u < 0) break;
             const int sp = u / args.n_row_tiles, rt = u % args.n_row_tiles;
             const int ct0 = static_cast<int>((long long)sp * args.n_col_tiles / args.splits);
             const int ct1 = static_cast<int>((long long)(sp + 1) * args.n_col_tiles / args.splits);
@@ -658,18 +797,34 @@ pairwise_tc_kernel(PairArgs args) {
             // with a mask it steps through the visited tiles, skipping other phases'.
             const bool dense = wk.row == nullptr;
             const int len = wk.count(ct0);
+            // score with a mask: the visited-tile indices (within the unit) of the
+            // column tiles the diagonal crosses, so that a tile's column index is never
+            // needed (no b_full wait / stage_ct load per tile on the epilogue's path)
+            int kd_lo = -1, kd_hi = -1;
+            if (kScore && !dense && has_diag) {
+                auto vidx = [&](int rel) {
+                    const int c = ct0 + rel;
+                    if (rel < 0 || c >= ct1 || !((wk.word(c >> 5) >> (c & 31)) & 1u)) return -1;
+                    TileWalk w2 = wk;
+                    w2.end = c;
+                    return w2.count(ct0);
+                };
+                kd_lo = vidx(drel_lo);
+                kd_hi = drel_hi != drel_lo ? vidx(drel_hi) : -1;
+            }
             int first_own = par - static_cast<int>(it_s % NP);
             if (first_own < 0) first_own += NP;
             for (int k = first_own; k < len; k += NP) {
                 const uint32_t sidx = it_s + k;
                 const uint32_t sb = sidx % Cfg::kSBuf, ph = (sidx / Cfg::kSBuf) & 1;
                 int ct = ct0 + k;
-                if (Cfg::kScoreTiling && !dense) {   // the visited tile's column index, from its B stage
-                    // (the density passes never need it)
+                if (kCheck && !dense) {   // the visited tile's column index, from its B stage
                     const uint32_t st = sidx % kStages;
                     ptx::mbar_wait(&b_full[st], (sidx / kStages) & 1);   // (complete: GEMM1 used it)
                     ct = *reinterpret_cast<volatile int*>(&stage_ct[st]);
                 }
+                if (kScore && !dense)   // only the diagonal's tiles need their column index
+                    ct = k == kd_lo ? ct0 + drel_lo : (k == kd_hi ? ct0 + drel_hi : INT_MIN / 2);
                 const int rel = ct - ct0;
                 FKDE_TRACE(0, sidx);
                 ptx::mbar_wait(&s_full[sb], ph);
@@ -811,6 +966,14 @@ pairwise_tc_kernel(PairArgs args) {
 
     ptx::tc_fence_before();
     __syncthreads();
+    if (threadIdx.x == 0) {   // the last CTA to finish resets the scheduler for the next launch
+        __threadfence();
+        if (atomicAdd(args.sched + 1, 1u) == gridDim.x - 1) {
+            args.sched[0] = 0;
+            args.sched[1] = 0;
+            __threadfence();
+        }
+    }
 #ifdef FKDE_CTA_TIMES
     if (args.trace && threadIdx.x == 0) args.trace[MODE * 4096 + 2 * blockIdx.x + 1] = ptx::globaltimer();
 #endif

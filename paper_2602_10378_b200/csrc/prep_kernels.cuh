@@ -198,6 +198,7 @@ struct PackArgs {
     double risk_half_norm;
     const float* cen;        // format 2: per column-tile centroids (log2 units, unscaled)
     int cen_tile;            // format 2: points per column tile
+    int ones_mask;           // format 2: tile J's ones column is 16 + (J & ones_mask)
 };
 
 __device__ __forceinline__ uint32_t pack_h2(__half a, __half b) {
@@ -256,7 +257,10 @@ __device__ __forceinline__ void pack_row_centred(const PackArgs& a, size_t i) {
                 ch[c][w] = pack_h2(vh[k0], vh[k0 + 1]);
                 ch[4 + c][w] = pack_h2(vl[k0], vl[k0 + 1]);
             }
-        ch[2][0] = pack_h2(__float2half(1.f), __float2half(0.f));   // column 16: the ones (S)
+        // the ones (S_J) in column 16 + (J mod group): chunk-2 word slot/2, half slot%2
+        const int slot = static_cast<int>(i / a.cen_tile) & a.ones_mask;
+        ch[2][slot >> 1] = (slot & 1) ? pack_h2(__float2half(0.f), __float2half(1.f))
+                                      : pack_h2(__float2half(1.f), __float2half(0.f));
     }
     const size_t tile = i / kTileRows;
     const int r = static_cast<int>(i % kTileRows);

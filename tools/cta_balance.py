@@ -51,6 +51,10 @@ def main():
               f"(max/mean {dur.max() / dur.mean():.3f}) | start spread {(st.max() - t0) / 1e3:.1f} us | "
               f"tiles min {tiles.min()} med {int(np.median(tiles))} max {tiles.max()} "
               f"(max/mean {tiles.max() / tiles.mean():.3f}) | us/tile {np.sum(dur) / max(tiles.sum(), 1):.4f}")
+        if mode == 0:
+            zc = b[mode, 3072:3072 + 1024][ok].sum()
+            print(f"           all-zero 32x32 sub-blocks: {zc} of {tiles.sum() * 12} "
+                  f"({zc / max(tiles.sum() * 12, 1) * 100:.1f}%)")
     ctx.close()
 
 
