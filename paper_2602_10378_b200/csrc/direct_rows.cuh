@@ -20,9 +20,14 @@
 // Schedule: one thread per flagged row, 128 rows per block, column range
 // split so that (row blocks x splits) fills the GPU whatever the (device-side)
 // flagged count is; column tiles are staged centred in fp32 in shared memory
-// and broadcast to the 128 rows.  Per-(row, split) partials are merged by the
-// last block to finish a row block (threadfence + counter), so the whole
-// recompute is one launch that exits at once when nothing is flagged.
+// and broadcast to the 128 rows.  Few flagged rows (<= kDirFewRows, the usual
+// case: a handful of outliers) would leave most threads of such a block idle
+// and each active thread walking a long column range alone, so there the block
+// works on ONE row instead, its 128 threads striding over the columns, with a
+// block reduction (online maximum, then rescaled sums).  Either way the
+// per-(row, split) partials are merged by the last block to finish (threadfence
+// + counter), so the whole recompute is one launch that exits at once when
+// nothing is flagged.
 #pragma once
 #include <cstdint>
 
@@ -42,6 +47,7 @@ constexpr int kDirTileCols = 128;    // columns per shared-memory tile
 constexpr int kDirTargetItems = 4 * 148;
 constexpr int kDirMaxSplits = 256;
 constexpr int kDirPart = 20;         // doubles per (row, split) partial: m, S, L, T[16], pad
+constexpr int kDirFewRows = 64;      // up to this many flagged rows: one row per block
 
 struct DirectArgs {
     int mode;                    // kExactScore / kExactGauss / kExactLaplace
@@ -112,6 +118,141 @@ __device__ __forceinline__ void direct_finish_row(const DirectArgs& a, size_t i,
     }
 }
 
+// Block-wide merge of per-thread (m, v[kMaxDim + 2]) = scaled sums sum 2^(t - m):
+// returns (in every thread) the block maximum M and v rescaled to it and summed.
+__device__ __forceinline__ float direct_block_merge(float m, double (&v)[kMaxDim + 2]) {
+    __shared__ double red[kDirRows / 32][kMaxDim + 2];
+    __shared__ float redm[kDirRows / 32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    float M = m;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    if (lane == 0) redm[w] = M;
+    __syncthreads();
+    M = redm[0];
+#pragma unroll
+    for (int q = 1; q < kDirRows / 32; ++q) M = fmaxf(M, redm[q]);
+    const double f = m == -INFINITY ? 0.0 : exp2(static_cast<double>(m) - static_cast<double>(M));
+#pragma unroll
+    for (int k = 0; k < kMaxDim + 2; ++k) {
+        v[k] *= f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+    }
+    if (lane == 0)
+#pragma unroll
+        for (int k = 0; k < kMaxDim + 2; ++k) red[w][k] = v[k];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kMaxDim + 2; ++k) {
+        v[k] = red[0][k];
+        for (int q = 1; q < kDirRows / 32; ++q) v[k] += red[q][k];
+    }
+    __syncthreads();   // (red / redm reused by the next call)
+    return M;
+}
+
+// Few flagged rows: block = (row, column split), threads stride over the columns.
+__device__ __forceinline__ void direct_few_rows(const DirectArgs& a, unsigned int count) {
+    __shared__ int s_last;
+    const int d = a.d;
+    int S = (kDirTargetItems + static_cast<int>(count) - 1) / static_cast<int>(count);
+    const size_t max_by_cols = (a.n + kDirTileCols - 1) / kDirTileCols;
+    if (static_cast<size_t>(S) > max_by_cols) S = static_cast<int>(max_by_cols);
+    if (S < 1) S = 1;
+    const int items = static_cast<int>(count) * S;
+    const float k2 = static_cast<float>(1.4426950408889634 / (2.0 * a.h * a.h));
+    const double ln2 = 0.69314718055994530942;
+    for (int it = blockIdx.x; it < items; it += gridDim.x) {
+        const int ridx = it / S, sp = it % S;
+        const size_t i = a.rows[ridx];
+        float u[kMaxDim];
+#pragma unroll
+        for (int c = 0; c < kMaxDim; ++c)
+            u[c] = c < d ? static_cast<float>(a.rowpts[i * d + c] - (a.center_rows ? a.sc->mu[c] : 0.0)) : 0.f;
+        const size_t self = a.mode == kExactScore ? a.row0 + i : ~static_cast<size_t>(0);
+        const size_t j0 = a.n * sp / S, j1 = a.n * (sp + 1) / S;
+        float m = -INFINITY;
+        double S64 = 0.0, L64 = 0.0, T64[kMaxDim];
+#pragma unroll
+        for (int c = 0; c < kMaxDim; ++c) T64[c] = 0.0;
+        for (size_t j = j0 + threadIdx.x; j < j1; j += kDirRows) {
+            float df[kMaxDim];
+            float r2 = 0.f;
+#pragma unroll
+            for (int c = 0; c < kMaxDim; ++c) {
+                const float v = c < d ? static_cast<float>(a.cols[j * d + c] - (a.center_cols ? a.sc->mu[c] : 0.0)) : 0.f;
+                df[c] = v - u[c];
+                r2 = fmaf(df[c], df[c], r2);
+            }
+            if (j == self) continue;   // phi_ii = 1 is added back in fp64
+            const float t = -r2 * k2;
+            if (t > m) {
+                const double f64 = exp2(static_cast<double>(m) - static_cast<double>(t));
+                S64 *= f64;
+                L64 *= f64;
+#pragma unroll
+                for (int c = 0; c < kMaxDim; ++c) T64[c] *= f64;
+                m = t;
+            }
+            const float p = dir_ex2(t - m);
+            S64 += p;
+            if (a.mode == kExactLaplace) L64 += static_cast<double>(p) * static_cast<double>(-t);
+            if (a.mode == kExactScore) {
+#pragma unroll
+                for (int c = 0; c < kMaxDim; ++c) T64[c] += static_cast<double>(p * df[c]);
+            }
+        }
+        // block reduction: maximum, then the sums rescaled to it
+        double v[kMaxDim + 2];
+        v[0] = S64;
+        v[1] = L64;
+#pragma unroll
+        for (int c = 0; c < kMaxDim; ++c) v[2 + c] = T64[c];
+        const float M = direct_block_merge(m, v);
+        if (threadIdx.x == 0) {
+            if (S == 1) {
+                direct_finish_row(a, i, M, v[0], v[1] * ln2, v + 2);
+            } else {
+                double* p = a.part + (static_cast<size_t>(ridx) * S + sp) * kDirPart;
+                p[0] = static_cast<double>(M);
+                p[1] = v[0];
+                p[2] = v[1] * ln2;
+#pragma unroll
+                for (int c = 0; c < kMaxDim; ++c) p[3 + c] = v[2 + c];
+                __threadfence();
+                s_last = atomicAdd(&a.done[ridx], 1u) == static_cast<unsigned int>(S - 1);
+            }
+        }
+        __syncthreads();
+        if (S > 1 && s_last) {
+            // last split of this row to finish: merge the S partials across the block
+            // (thread t takes splits t, t + 128, ...; a fixed order, so deterministic)
+            __threadfence();
+            const double* p = a.part + static_cast<size_t>(ridx) * S * kDirPart;
+            float mt = -INFINITY;
+            for (int s = threadIdx.x; s < S; s += kDirRows) mt = fmaxf(mt, static_cast<float>(__ldcg(p + s * kDirPart)));
+            double w[kMaxDim + 2];
+#pragma unroll
+            for (int k = 0; k < kMaxDim + 2; ++k) w[k] = 0.0;
+            for (int s = threadIdx.x; s < S; s += kDirRows) {
+                const double* q = p + s * kDirPart;
+                const float ms = static_cast<float>(__ldcg(q));
+                if (ms == -INFINITY) continue;
+                const double fs = exp2(static_cast<double>(ms) - static_cast<double>(mt));
+#pragma unroll
+                for (int k = 0; k < kMaxDim + 2; ++k) w[k] += fs * __ldcg(q + 1 + k);
+            }
+            const float Mm = direct_block_merge(mt, w);
+            if (threadIdx.x == 0) {
+                direct_finish_row(a, i, Mm, w[0], w[1], w + 2);
+                a.done[ridx] = 0u;   // ready for the next call
+            }
+        }
+        __syncthreads();   // (s_last reused by the next item)
+    }
+}
+
 __global__ void __launch_bounds__(kDirRows) direct_rows_kernel(DirectArgs a) {
     pdl_launch_dependents();
     pdl_wait();
@@ -119,6 +260,10 @@ __global__ void __launch_bounds__(kDirRows) direct_rows_kernel(DirectArgs a) {
     __shared__ int s_last;
     const unsigned int count = *a.count;
     if (count == 0) return;
+    if (count <= static_cast<unsigned int>(kDirFewRows)) {
+        direct_few_rows(a, count);
+        return;
+    }
     const int nblk = static_cast<int>((count + kDirRows - 1) / kDirRows);
     const int S = direct_splits(count, a.n);
     const int items = nblk * S;

@@ -201,7 +201,7 @@ struct Device {
     bool ordered = false;        // last score pass ran on the spatial order
     // density pass on the spatial order: sorted queries, their permutation, keys + CUB
     // scratch, skipped tiles per query tile, densities back in the caller's order
-    DevBuf Qs, qperm, qkeys, qcubtmp, qskip, qout;
+    DevBuf Qs, qperm, qkeys, qcubtmp, qskip, qmass, qout;
     bool qordered = false;       // last density pass ran on the spatial order (D.qout)
     uint64_t dtiles_total = 0;   // tile pairs of the last density pass
     size_t dtiles_rows = 0;      // query tiles of the last skipping density pass (0: none)
@@ -221,7 +221,7 @@ struct Device {
                 &aux0,  &aux1,  &colpart, &scal, &err,  &flags, &risk,      &dpart,   &ddone,
                 &pdone, &sched, &qmax,  &Xs,   &perm,   &keys,  &cubtmp, &ordsc,    &cenA,    &cenB,
                 &boxA,  &boxB,  &skipstats, &unperm0, &unperm1, &pmask, &smask, &Qs, &qperm,
-                &qkeys, &qcubtmp, &qskip, &qout};
+                &qkeys, &qcubtmp, &qskip, &qmass, &qout};
     }
 };
 
@@ -474,7 +474,8 @@ Status launch_direct(Device& D, bool pdl, DirectArgs& e, size_t rows) {
     // partials: at most (row blocks x splits) < 2 * kDirTargetItems items of 128 rows
     STATUS_TRY(ensure(D.dpart, static_cast<size_t>(2 * kDirTargetItems) * kDirRows * kDirPart *
                                    sizeof(double)));
-    const size_t blocks = (rows + kDirRows - 1) / kDirRows + 1;
+    // completion counters: one per row block, or per row when few rows are flagged
+    const size_t blocks = std::max<size_t>((rows + kDirRows - 1) / kDirRows + 1, kDirFewRows);
     if (D.ddone.bytes < blocks * sizeof(unsigned int)) {   // counters start at zero, then self-reset
         STATUS_TRY(ensure(D.ddone, blocks * sizeof(unsigned int)));
         CUDA_TRY(cudaMemsetAsync(D.ddone.p, 0, D.ddone.bytes, D.stream));
@@ -561,18 +562,14 @@ Status spatial_order(Device& D, const double* dX, size_t n, int d, const PassSca
 
 // Density pass on the spatial order: a tile pair is skipped when the box bound
 // proves every pair's log2 phi < -(kDensitySkipHalfR2 - 0.5) (0.5: margin for the
-// float boxes).  The skipped contribution of a row is then below skipped_tiles *
-// 128 * 2^-44.5 (Gaussian terms phi) or that times (1 + d/2 + ln2 * 44.5)
-// (Laplace-fused terms phi (1 + d/2 - u); phi |log2 phi| decreases below 1/e), and a
-// row whose term mass (|ca| s0 + |cb| |s1|: the scale of the fp32 sums' own
-// rounding of that row) is not at least 2^24 times that bound is recomputed by
-// direct differences (reduce_density flags it).  The skip therefore changes no
-// row by more than 2^-24 of its term mass.
+// float boxes).  tile_predict sums, per query tile, the bound on what one row loses
+// to its skipped tiles (128 columns x the largest phi the box bound allows, times
+// 1 + d/2 + ln2 |log2 phi| for the Laplace-fused terms phi (1 + d/2 - u)), and a row
+// whose term mass (|ca| s0 + |cb| |s1|: the scale of the fp32 sums' own rounding of
+// that row) is not at least 2^24 times that bound is recomputed by direct
+// differences (reduce_density flags it).  The skip therefore changes no row by more
+// than 2^-24 of its term mass.
 constexpr float kDensitySkipHalfR2 = 45.0f;
-inline double density_skip_flag(int kernel, int d) {   // per skipped tile, x 2^24
-    const double per_pair = kernel == FKDE_KERNEL_GAUSSIAN ? 0x1p-44 : 0x1p-44 * (1.0 + 0.5 * d + 31.0);
-    return 128.0 * per_pair * 0x1p24;
-}
 
 // Queries sorted on the training order's axes (D.ordsc; sc: the training mean,
 // n_cov: the count the covariance was summed over): D.Qs = Q[qperm]
@@ -883,7 +880,9 @@ Status query_program(Device& D, const Options& o, const Job& J, const double* dC
         STATUS_TRY(ensure(D.pmask, q_rt * dwords * sizeof(uint32_t)));
         STATUS_TRY(ensure(D.smask, q_rt * dwords * sizeof(uint32_t)));
         STATUS_TRY(ensure(D.qskip, q_rt * sizeof(unsigned int)));
+        STATUS_TRY(ensure(D.qmass, q_rt * sizeof(float)));
         CUDA_TRY(cudaMemsetAsync(D.qskip.p, 0, q_rt * sizeof(unsigned int), D.stream));
+        CUDA_TRY(cudaMemsetAsync(D.qmass.p, 0, q_rt * sizeof(float), D.stream));
         if (sh.rows)
             tile_summary<<<static_cast<unsigned>(q_rt), 128, 0, D.stream>>>(
                 dQ + sh.begin * d, sh.rows, d, sc_q, D.ordsc.as<OrderScalars>(), kh, kTileRows, 0,
@@ -896,7 +895,8 @@ Status query_program(Device& D, const Options& o, const Job& J, const double* dC
                        128, 0, D.stream>>>(
             D.cenA.as<float>(), D.boxA.as<float>(), static_cast<int>(q_rt), D.cenB.as<float>(),
             D.boxB.as<float>(), static_cast<int>(q_ct), dwords, INFINITY, kDensitySkipHalfR2,
-            D.pmask.as<uint32_t>(), D.smask.as<uint32_t>(), D.qskip.as<unsigned int>());
+            D.pmask.as<uint32_t>(), D.smask.as<uint32_t>(), D.qskip.as<unsigned int>(), D.qmass.as<float>(),
+            kernel == FKDE_KERNEL_GAUSSIAN ? -1 : d, static_cast<float>(kTileRows));
         D.launches += 3;
         CUDA_TRY(cudaGetLastError());
         dmask = D.smask.as<uint32_t>();
@@ -925,8 +925,7 @@ Status query_program(Device& D, const Options& o, const Job& J, const double* dC
         r.flag_count = flag_count;
         r.flag_rows = flag_count + 1;
         r.risk = D.risk.as<uint8_t>();
-        r.skip_tiles = dmask ? D.qskip.as<unsigned int>() : nullptr;
-        r.skip_flag_mass = density_skip_flag(FKDE_KERNEL_GAUSSIAN, d);
+        r.skip_mass = dmask ? D.qmass.as<float>() : nullptr;
         if (sh.rows) CUDA_TRY(launch_chain(o.pdl, reduce_density, dim3(grid1(sh.rows, 256)), dim3(256), 0, D.stream, r));
         ++D.launches;
     } else if (fused) {
@@ -942,8 +941,7 @@ Status query_program(Device& D, const Options& o, const Job& J, const double* dC
         r.flag_count = flag_count;
         r.flag_rows = flag_count + 1;
         r.risk = D.risk.as<uint8_t>();
-        r.skip_tiles = dmask ? D.qskip.as<unsigned int>() : nullptr;
-        r.skip_flag_mass = density_skip_flag(FKDE_KERNEL_LAPLACE_CORRECTED, d);
+        r.skip_mass = dmask ? D.qmass.as<float>() : nullptr;
         if (sh.rows) CUDA_TRY(launch_chain(o.pdl, reduce_density, dim3(grid1(sh.rows, 256)), dim3(256), 0, D.stream, r));
         ++D.launches;
     } else {

@@ -443,11 +443,11 @@ struct ReduceArgs {
     unsigned int* flag_count;   // rows whose Gaussian mass underflows fp32 ranges
     unsigned int* flag_rows;
     const uint8_t* risk;        // pack's spread flags (local rows) or nullptr
-    // density tile skipping (nullptr: none): skipped tiles per 128-row tile; a row
-    // whose term mass |ca| s0 + |cb| |s1| (the scale of the fp32 sums' own rounding
-    // of the row) is below skip_tiles * skip_flag_mass is flagged
-    const unsigned int* skip_tiles;
-    double skip_flag_mass;
+    // density tile skipping (nullptr: none): per 128-row tile, the bound on the
+    // term mass one row loses to the skipped tiles (tile_predict); a row whose term
+    // mass |ca| s0 + |cb| |s1| (the scale of the fp32 sums' own rounding of the row)
+    // is below 2^24 times that bound is flagged
+    const float* skip_mass;
 };
 
 __global__ void reduce_density(ReduceArgs a) {
@@ -460,8 +460,8 @@ __global__ void reduce_density(ReduceArgs a) {
     if (a.part1)
         for (int p = 0; p < a.nparts; ++p) s1 += static_cast<double>(a.part1[p * a.rows_pad + j]);
     const bool skipped_mass =
-        a.skip_tiles && fabs(a.ca) * s0 + fabs(a.cb * s1) <
-                            static_cast<double>(a.skip_tiles[j / kTileRows]) * a.skip_flag_mass;
+        a.skip_mass && fabs(a.ca) * s0 + fabs(a.cb * s1) <
+                           0x1p24 * static_cast<double>(a.skip_mass[j / kTileRows]);
     if (a.flag_rows && (s0 < kDensityFlagMass || (a.risk && a.risk[j]) || skipped_mass)) {
         a.flag_rows[atomicAdd(a.flag_count, 1u)] = static_cast<unsigned int>(j);
         return;

@@ -283,6 +283,11 @@ __global__ void __launch_bounds__(128) tile_summary(const double* __restrict__ x
 //     check pass (pred 1, skip 1 until the check clears it);
 //   * otherwise computed (pred 0, skip 0).
 // skip_count (optional, zeroed by the caller): += skipped tiles per row tile.
+// skip_mass (optional, zeroed by the caller; density passes): += per row tile the
+// bound on what one row loses to the skipped tiles, sum over them of tile_w *
+// phi_max * (1 (Gaussian) | 1 + d/2 + ln2 |log2 phi_max| (Laplace-fused, lap_d = d)),
+// phi_max = 2^-(r^2/2 lower bound - 0.5): reduce_density recomputes the rows whose
+// mass does not dominate it.
 // Block = 128 row tiles (one per thread) x kPredWords mask words (32 column tiles
 // each): the column tiles' summaries are staged once in shared memory, so each
 // summary is read from global memory once per 128 row tiles (a thread per (row
@@ -296,7 +301,9 @@ __global__ void __launch_bounds__(128) tile_predict(const float* __restrict__ ce
                                                     int words, float thresh, float proven_half_r2,
                                                     uint32_t* __restrict__ pred,
                                                     uint32_t* __restrict__ skip,
-                                                    unsigned int* __restrict__ skip_count) {
+                                                    unsigned int* __restrict__ skip_count,
+                                                    float* __restrict__ skip_mass = nullptr,
+                                                    int lap_d = -1, float tile_w = 128.f) {
     pdl_launch_dependents();
     pdl_wait();
     __shared__ float colsum[kPredWords * 32][kSumFloats];
@@ -317,6 +324,7 @@ __global__ void __launch_bounds__(128) tile_predict(const float* __restrict__ ce
 #pragma unroll
     for (int c = 0; c < kBoxFloats; ++c) ab[c] = boxA[(size_t)rt * kBoxFloats + c];
     unsigned int nskip = 0;
+    float mass = 0.f;
     for (int wi = 0; wi < kPredWords && w0 + wi < words; ++wi) {
         uint32_t pbits = 0, sbits = 0;
         for (int b = 0; b < 32; ++b) {
@@ -340,6 +348,10 @@ __global__ void __launch_bounds__(128) tile_predict(const float* __restrict__ ce
             }
             if (0.5f * fmaxf(lower, lbp) > proven_half_r2) {
                 sbits |= 1u << b;
+                if (skip_mass) {
+                    const float x = 0.5f * fmaxf(lower, lbp) - 0.5f;   // -log2 phi_max
+                    mass += exp2f(-x) * (lap_d >= 0 ? 1.f + 0.5f * lap_d + 0.6931472f * x : 1.f);
+                }
                 continue;
             }
             float dd = 0.f;
@@ -359,6 +371,7 @@ __global__ void __launch_bounds__(128) tile_predict(const float* __restrict__ ce
         nskip += __popc(sbits);
     }
     if (skip_count && nskip) atomicAdd(skip_count + rt, nskip);
+    if (skip_mass && mass > 0.f) atomicAdd(skip_mass + rt, mass * tile_w * 1.001f);
 }
 
 }  // namespace fkde_b200

@@ -64,8 +64,31 @@ def run(ctx, kind, n, m, reps=5, seed=0):
           f"exp/s={exps / ms * 1e3:.3e} ({exps / ms * 1e3 / MUFU_PEAK * 100:.1f}% of MUFU@1.965GHz) "
           f"phases prep={tm[0]:.3f} score={tm[1]:.3f} fin={tm[2]:.3f} gath={tm[3]:.3f} "
           f"query={tm[4]:.3f} red={tm[5]:.3f}", flush=True)
+    st = ctx.skip_stats()
+    print(f"        direct rows: score {st['direct_rows']} density {st['density']['direct_rows']}; "
+          f"tiles skipped score {st['tiles_skipped']}/{st['tiles_total']} "
+          f"density {st['density']['tiles_skipped']}/{st['density']['tiles_total']}", flush=True)
     v = dO.cpu().numpy()
     assert np.isfinite(v).all()
+
+
+def run_bench(ctx, n, m, reps=1):
+    from paper_2602_10378_b200 import fixtures as F
+    X, Y = F.runtime_sweep_inputs(n, m, seed=0)
+    h = F.sdkde_bandwidth(X)
+    dX = torch.from_numpy(X).cuda()
+    dY = torch.from_numpy(Y).cuda()
+    dO = torch.empty(m, dtype=torch.float64, device="cuda")
+    lib = N.load()
+    ctx.set_option(N.OPT_TIMING, 1)
+    for _ in range(reps + 1):
+        rc = lib.fkde_gpu_sdkde_device(ctx.handle, dX.data_ptr(), n, dY.data_ptr(), m, 16, h, h, dO.data_ptr())
+        assert rc == 0, ctx.last_error()
+    tm = ctx.last_timing()
+    st = ctx.skip_stats()
+    print(f"bench   n={n:8d} m={m:7d}: {tm[N.T_TOTAL]:9.3f} ms phases prep={tm[0]:.3f} score={tm[1]:.3f} "
+          f"fin={tm[2]:.3f} gath={tm[3]:.3f} query={tm[4]:.3f} red={tm[5]:.3f} | direct rows score "
+          f"{st['direct_rows']} density {st['density']['direct_rows']}", flush=True)
 
 
 def main():
@@ -73,6 +96,8 @@ def main():
     which = sys.argv[1:] or ["small", "big"]
     if "sd1m" in which:
         run(ctx, "sdkde", 1 << 20, 1 << 17, reps=0)
+    if "bench1m" in which:   # the bench.py workload (reference mixture, SD-KDE rate bandwidth)
+        run_bench(ctx, 1 << 20, 1 << 17)
     if "sd256k" in which:
         run(ctx, "sdkde", 1 << 18, 1 << 14, reps=0)
     if "sd32k" in which:
