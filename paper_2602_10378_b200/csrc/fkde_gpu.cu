@@ -330,6 +330,7 @@ Status launch_pairwise(Device& D, const Options& o, const PairArgs& a, size_t n_
             attr_done_dev[D.dev & 63] |= 1 << MODE;
         }
         const int units = a.n_row_tiles * a.splits;
+        if (units == 0) return {};   // (an empty shard)
         int grid = std::min(units, D.num_sms);
         if (o.max_ctas > 0) grid = std::min(grid, o.max_ctas);
         PairArgs b = a;

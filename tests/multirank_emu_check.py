@@ -3,7 +3,10 @@ in-process NCCL emulator before the engine first loads NCCL).  Runs the engine's
 multi-rank C++ path -- single-process multi-device contexts and one context per
 rank driven from threads -- on ONE GPU and prints max differences against the
 single-device engine at a fixed column-split count (results are expected to be
-bitwise identical: every row / query sees the same per-unit reduction order)."""
+bitwise identical: every row / query sees the same per-unit reduction order).
+Optional 5th argument 1: every context runs on the spatial order with tile
+skipping (FKDE_OPT_SPATIAL = 1, the default for n >= 32768), so the sorted-order
+row shards, the sorted x^SD gather and the un-permutation run multi-rank too."""
 import ctypes
 import json
 import os
@@ -33,18 +36,24 @@ def run_all(ctx, X, Y, h):
 
 def main():
     n, m, world, splits = (int(a) for a in sys.argv[1:5])
+    spatial = int(sys.argv[5]) if len(sys.argv) > 5 else 0
+
+    def setup(c):
+        c.set_option(N.OPT_SPLITS, splits)
+        if spatial:
+            c.set_option(N.OPT_SPATIAL, 1)
     rng = np.random.default_rng(7)
     X = rng.normal(size=(n, 16)) * 1.5 + rng.integers(0, 3, size=(n, 1))
     Y = rng.normal(size=(m, 16)) * 1.5
     h = 1.3
     one = fk.Context([0])
-    one.set_option(N.OPT_SPLITS, splits)
+    setup(one)
     ref = run_all(one, X, Y, h)
     one.close()
 
     out = {}
     multi = fk.Context([0] * world)           # single process, world "devices"
-    multi.set_option(N.OPT_SPLITS, splits)
+    setup(multi)
     got = run_all(multi, X, Y, h)
     multi.close()
     out["multi_device"] = {k: float(np.max(np.abs(got[k] - ref[k]))) for k in ref}
@@ -60,7 +69,7 @@ def main():
     def rank_dev(r):
         try:
             c = fk.Context(rank=r, world=world, device=0, nccl_id=uid_d)
-            c.set_option(N.OPT_SPLITS, splits)
+            setup(c)
             dO = torch.zeros(m, dtype=torch.float64, device="cuda")
             for _ in range(2):
                 rc = lib.fkde_gpu_sdkde_device(c.handle, dX.data_ptr(), n, dY.data_ptr(), m, 16, h, h,
@@ -89,7 +98,7 @@ def main():
     def rank_main(r):
         try:
             c = fk.Context(rank=r, world=world, device=0, nccl_id=uid)
-            c.set_option(N.OPT_SPLITS, splits)
+            setup(c)
             res[r] = run_all(c, X, Y, h)
             c.close()
         except Exception as e:  # noqa: BLE001
@@ -105,6 +114,7 @@ def main():
     else:
         out["per_rank"] = [{k: float(np.max(np.abs(res[r][k] - ref[k]))) for k in ref}
                            for r in range(world)]
+    out["scale"] = {k: float(np.max(np.abs(ref[k]))) for k in ref}
     print(json.dumps(out))
 
 

@@ -47,3 +47,26 @@ def test_multirank_path_is_bitwise_single_device(emu_lib, n, m, world, splits):
     for form in [res["multi_device"]] + res["per_rank"]:
         for k, v in form.items():
             assert v == 0.0, (k, v, res)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,m,world,splits", [(5000, 1000, 2, 2), (9000, 777, 3, 3)])
+def test_multirank_spatial_order(emu_lib, n, m, world, splits):
+    # the spatial order with tile skipping, multi-rank: the score pass's row shards
+    # start on tile boundaries of the same sorted order, so scores and debiased
+    # samples are bitwise the single-device ones; query shards are not tile
+    # aligned, so the density pass's skip decisions (per query tile) differ from
+    # the single-device run by at most the 2^-24 relative skip guarantee
+    env = dict(os.environ, FKDE_NCCL_LIB=emu_lib)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "multirank_emu_check.py"),
+                        str(n), str(m), str(world), str(splits), "1"],
+                       capture_output=True, text=True, env=env, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    print(res)
+    assert "per_rank_error" not in res and "device_api_error" not in res, res
+    for form in [res["multi_device"]] + res["per_rank"]:
+        assert form["score"] == 0.0 and form["debiased"] == 0.0, form
+        for k in ("sdkde", "kde", "laplace"):
+            assert form[k] <= 1e-6 * res["scale"][k], (k, form, res)
+    assert all(v <= 1e-6 * res["scale"]["sdkde"] for v in res["device_api"]), res
