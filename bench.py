@@ -45,6 +45,15 @@ DIM = 16
 METRIC = "SD-KDE wall s & queries/sec, n=1M d=16, 131k queries, at 1/2/4/8 B200 vs CPU ref"
 PAPER_WALL_S = 2.3  # PAPER.md:30, 592 (RTX A6000), BASELINE.md section 1
 MUFU_EX2_PER_CLK_SM = 16
+# BASELINE.json configs: --workload K (default 5, the headline the metric names;
+# the others give per-config lines under the same timing contract)
+WORKLOADS = {
+    1: ("sdkde", 4096, 4096, "SD-KDE n=4096 m=4096 d=16 (BASELINE config 1)"),
+    2: ("sdkde", 32768, 32768, "SD-KDE n=32768 m=32768 d=16 (BASELINE config 2)"),
+    3: ("kde", 32768, 32768, "Gaussian KDE n=32768 m=32768 d=16 (BASELINE config 3)"),
+    4: ("laplace", 262144, 65536, "Laplace-corrected fused KDE n=262144 m=65536 d=16 (BASELINE config 4)"),
+    5: ("sdkde", N_TRAIN, N_QUERY, "SD-KDE n=1048576 m=131072 d=16 (BASELINE config 5)"),
+}
 
 
 def env_rank():
@@ -113,14 +122,15 @@ class ClockSampler:
 
 
 # ---- inputs -------------------------------------------------------------------------
-def make_inputs(n, m):
+def make_inputs(n, m, kind="sdkde"):
     from paper_2602_10378_b200 import fixtures as F
     X, Y = F.runtime_sweep_inputs(n, m, seed=0)
-    h = F.sdkde_bandwidth(X)  # BandwidthPolicy Auto for SD-KDE (sweep.cpp:31-61)
+    # BandwidthPolicy Auto (sweep.cpp:31-61): SD-KDE rate for SD-KDE, Silverman otherwise
+    h = F.sdkde_bandwidth(X) if kind == "sdkde" else F.silverman_bandwidth(X)
     return X, Y, h
 
 
-def make_inputs_oracle(n, m, orc):
+def make_inputs_oracle(n, m, orc, kind="sdkde"):
     """The same inputs from the oracle library alone (reference arm: the product
     package is never imported).  Bitwise equal to make_inputs (tests/test_bench.py)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -129,15 +139,25 @@ def make_inputs_oracle(n, m, orc):
     cs = orc.mix64(0 ^ orc.mix64(n))             # sweep.cpp:67-69 cell_data_seed
     X = orc.sample_mixture(w, mu, s, n, cs)
     Y = orc.sample_mixture(w, mu, s, m, orc.mix64(cs ^ 0x71))
-    h = orc.sdkde_bandwidth(X, orc.silverman_prefactor(X.shape[1]))
+    h = (orc.sdkde_bandwidth(X, orc.silverman_prefactor(X.shape[1])) if kind == "sdkde"
+         else orc.silverman_bandwidth(X))
     return X, Y, h
 
 
-def workload_config(n, m, d, h):
+def workload_config(n, m, d, h, wl=5):
     """Identical in both arms (the driver compares them)."""
-    return {"workload": f"SD-KDE n={n} m={m} d={d} (BASELINE config 5)", "h": h,
-            "n_train": n, "n_query": m, "d": d,
-            "l2": "inputs larger than L2 (X fp64 128 MiB; B-operand tiles 128 MiB)"}
+    big = n * d * 8 > (126 << 20)
+    return {"workload": WORKLOADS[wl][3], "h": h, "n_train": n, "n_query": m, "d": d,
+            "l2": (f"inputs larger than L2 (X fp64 {n * d * 8 >> 20} MiB)" if big else
+                   f"L2 flushed before every timed step (256 MiB write; X fp64 "
+                   f"{n * d * 8 >> 20} MiB fits the 126 MiB L2)")}
+
+
+def metric_of(wl):
+    if wl == 5:
+        return METRIC
+    kind, n, m, name = WORKLOADS[wl]
+    return f"{name}: wall s & queries/sec on B200 vs CPU ref"
 
 
 # ---- CPU baseline (the reference oracle, bounded sample) ------------------------------
@@ -151,21 +171,30 @@ def oracle_handle():
     return kind, O.get(kind)
 
 
-def cpu_oracle_sample(orc, kind, X, Y, h, rows_score=ROWS_SCORE, rows_query=ROWS_QUERY):
+def cpu_oracle_sample(orc, kind, X, Y, h, rows_score=ROWS_SCORE, rows_query=ROWS_QUERY,
+                      job="sdkde"):
     """Times the reference's naive oracle on a row sample; returns (sample wall s,
     extrapolated full-workload s, details).  Cost is exactly linear in evaluated rows."""
     threads = os.cpu_count() or 1
     n, m = X.shape[0], Y.shape[0]
-    rs = np.linspace(0, n - 1, rows_score).astype(np.int64)
+    rows_score = 0 if job != "sdkde" else min(rows_score, n)
+    rows_query = min(rows_query * (4 if job != "sdkde" else 1), m)
+    rs = np.linspace(0, n - 1, max(rows_score, 1)).astype(np.int64)
     t0 = time.perf_counter()
-    orc.score_naive(X, X[rs], h, threads=threads)
+    if rows_score:
+        orc.score_naive(X, X[rs], h, threads=threads)
     t1 = time.perf_counter()
     qs = np.linspace(0, m - 1, rows_query).astype(np.int64)
-    orc.kde_naive(X, Y[qs], h, threads=threads)  # same cost as against the debiased set
+    if job == "laplace":
+        orc.laplace_naive(X, Y[qs], h, threads=threads)
+    else:
+        orc.kde_naive(X, Y[qs], h, threads=threads)  # same cost as against the debiased set
     t2 = time.perf_counter()
-    full = (t1 - t0) * n / rows_score + (t2 - t1) * m / rows_query
-    sample = (f"score_naive on {rows_score} of {n} rows + kde_naive on {rows_query} of {m} "
-              f"queries (x {n} train), {threads} threads, extrapolated linearly in rows")
+    full = (t1 - t0) * n / max(rows_score, 1) + (t2 - t1) * m / rows_query
+    fn = "laplace_naive" if job == "laplace" else "kde_naive"
+    sample = ((f"score_naive on {rows_score} of {n} rows + " if rows_score else "") +
+              f"{fn} on {rows_query} of {m} queries (x {n} train), {threads} threads, "
+              "extrapolated linearly in rows")
     return t2 - t0, full, {"kind": kind, "cores": threads, "sample": sample,
                            "sample_s": t2 - t0, "extrapolated": True,
                            "sample_rows": {"score": rows_score, "query": rows_query}}
@@ -181,19 +210,20 @@ def run_reference(args):
     if rank != 0:
         return 0
     kind, orc = oracle_handle()
-    X, Y, h = make_inputs_oracle(N_TRAIN, N_QUERY, orc)
+    job, n_tr, n_q, _ = WORKLOADS[args.workload]
+    X, Y, h = make_inputs_oracle(n_tr, n_q, orc, job)
     for _ in range(args.warmup):
-        cpu_oracle_sample(orc, kind, X, Y, h, 16, 16)
+        cpu_oracle_sample(orc, kind, X, Y, h, 16, 16, job=job)
     samples, fulls = [], []
     info = None
     for _ in range(args.steps):
-        smp, full, info = cpu_oracle_sample(orc, kind, X, Y, h)
+        smp, full, info = cpu_oracle_sample(orc, kind, X, Y, h, job=job)
         samples.append(smp)
         fulls.append(full)
     wall = float(np.median(fulls))
-    qps = N_QUERY / wall
+    qps = n_q / wall
     line = {
-        "impl": "reference", "metric": METRIC, "value": qps, "unit": "queries/s",
+        "impl": "reference", "metric": metric_of(args.workload), "value": qps, "unit": "queries/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         # ms_per_step is what one timed step actually took (the bounded sample);
         # value is the full workload's rate extrapolated from it
@@ -201,7 +231,7 @@ def run_reference(args):
         "extrapolated": True, "full_workload_wall_s": wall,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: reference 16-D Gaussian mixture, runtime-sweep seeds",
-        "config": workload_config(N_TRAIN, N_QUERY, DIM, h),
+        "config": workload_config(n_tr, n_q, DIM, h, args.workload),
         "parallelism": f"{info['cores']} host threads on rank 0 (CPU only; no GPU used)",
         "reference_path": f"oracle/_ref ({'reference sources compiled' if kind == 'reference' else 'C port'})",
         "reference_flash_engine": REF_FLASH_NOTE,
@@ -237,17 +267,22 @@ def run_ours(args):
     lib = N.load()
     dev = torch.device("cuda", local)
 
-    X, Y, h = make_inputs(N_TRAIN, N_QUERY)
+    job, n_tr, n_q, _ = WORKLOADS[args.workload]
+    X, Y, h = make_inputs(n_tr, n_q, job)
     n, m, d = X.shape[0], Y.shape[0], X.shape[1]
+    kern = N.KERNEL_LAPLACE_CORRECTED if job == "laplace" else N.KERNEL_GAUSSIAN
     dX = torch.from_numpy(X).to(dev)
     dY = torch.from_numpy(Y).to(dev)
     dO = torch.empty(m, dtype=torch.float64, device=dev)
     stream = torch.cuda.ExternalStream(ctx.stream(), device=dev)
-    ctx.set_option(N.OPT_TIMING, 1)
 
     def step():
-        rc = lib.fkde_gpu_sdkde_device(ctx.handle, dX.data_ptr(), n, dY.data_ptr(), m, d, h, h,
-                                       dO.data_ptr())
+        if job == "sdkde":
+            rc = lib.fkde_gpu_sdkde_device(ctx.handle, dX.data_ptr(), n, dY.data_ptr(), m, d, h, h,
+                                           dO.data_ptr())
+        else:   # configs 3 / 4: density pass only (Laplace: fused, as BASELINE names it)
+            rc = lib.fkde_gpu_kde_device(ctx.handle, dX.data_ptr(), n, dY.data_ptr(), m, d, h, kern,
+                                         1, dO.data_ptr())
         if rc != 0:
             raise RuntimeError(ctx.last_error())
 
@@ -267,18 +302,40 @@ def run_ours(args):
     barrier()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    score_ms, query_ms, launches = [], [], 0
-    ev0.record(stream)
-    for _ in range(args.steps):
+    launches = 0
+    if n * d * 8 > (126 << 20):   # inputs larger than L2: steps back to back, no host sync
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+            launches += ctx.last_launch_count()
+        ev1.record(stream)
+        barrier()
+        dev_ms = ev0.elapsed_time(ev1)
+    else:   # L2-resident working set: L2 flushed (256 MiB write) before every timed step
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        with torch.cuda.stream(stream):
+            for a, b in evs:
+                flush.fill_(1)
+                a.record(stream)
+                step()
+                b.record(stream)
+                launches += ctx.last_launch_count()
+        barrier()
+        dev_ms = sum(a.elapsed_time(b) for a, b in evs)
+    clocks = sampler.stop()
+    # per-phase CUDA-event times (score / density pass): separate, untimed steps with
+    # the engine's phase events on (they make the call run eagerly: single-rank
+    # device calls are otherwise replayed from a captured CUDA graph)
+    ctx.set_option(N.OPT_TIMING, 1)
+    score_ms, query_ms = [], []
+    for _ in range(2):
         step()
         t = ctx.last_timing()  # syncs on this step's last event
         score_ms.append(t[N.T_SCORE])
         query_ms.append(t[N.T_QUERY])
-        launches += ctx.last_launch_count()
-    ev1.record(stream)
-    barrier()
-    dev_ms = ev0.elapsed_time(ev1)
-    clocks = sampler.stop()
+    ctx.set_option(N.OPT_TIMING, 0)
     skip = ctx.skip_stats()   # tile skipping of the last score pass (this rank)
 
     # e2e through the host C ABI: H2D of this step's inputs and D2H of its results
@@ -295,8 +352,12 @@ def run_ours(args):
 
     def host_step(bufs):
         x, y, o, db = bufs
-        rc = lib.fkde_gpu_sdkde(ctx.handle, ctypes.cast(x, dp), n, ctypes.cast(y, dp), m, d, h, h,
-                                ctypes.cast(o, dp), ctypes.cast(db, dp), ctypes.byref(idx))
+        if job == "sdkde":
+            rc = lib.fkde_gpu_sdkde(ctx.handle, ctypes.cast(x, dp), n, ctypes.cast(y, dp), m, d, h,
+                                    h, ctypes.cast(o, dp), ctypes.cast(db, dp), ctypes.byref(idx))
+        else:
+            rc = lib.fkde_gpu_kde(ctx.handle, ctypes.cast(x, dp), n, ctypes.cast(y, dp), m, d, h,
+                                  kern, 1, ctypes.cast(o, dp))
         if rc != 0:
             raise RuntimeError(ctx.last_error())
 
@@ -313,7 +374,9 @@ def run_ours(args):
     pinned = (pX.data_ptr(), pY.data_ptr(), pO.data_ptr(), pD.data_ptr())
     pageable = (gX.ctypes.data, gY.ctypes.data, gO.ctypes.data, gD.ctypes.data)
     e2e_s = e2e_time(pinned)
-    out_ok = bool(np.isfinite(pO.numpy()).all() and (pO.numpy() > 0).all())
+    # densities: finite; Gaussian ones also positive (the Laplace-corrected kernel
+    # takes negative values by construction)
+    out_ok = bool(np.isfinite(pO.numpy()).all() and (job == "laplace" or (pO.numpy() > 0).all()))
     e2e_pg_s = e2e_time(pageable)
     out_ok = out_ok and bool(np.array_equal(gO, pO.numpy()))
 
@@ -334,37 +397,48 @@ def run_ours(args):
         peaks, src = measured_peaks()
         sm_mhz = clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
         max_mhz = peaks.get("sm_max_mhz", 1965.0)
-        # dominant kernel: the score pass (check + score kernels, the T_SCORE phase).
-        # Algorithmic work = every (row, column) pair of this rank's rows; executed
-        # work = the pairs of the tiles the pass did not prove / check to be exact
-        # zeros (128 x 96 per tile), plus the check pass's GEMM1 on checked tiles.
-        rows_rank = -(-n // world)
+        # dominant kernel.  SD-KDE: the score pass (check + score kernels, the
+        # T_SCORE phase); KDE / Laplace: the density pass (T_QUERY).  Algorithmic
+        # work = every (row, column) pair of this rank's rows; executed work = the
+        # pairs of the tiles the pass did not prove / check to be exact zeros
+        # (128 x 96 per score tile, 128 x 128 per density tile).
+        sd = job == "sdkde"
+        if sd:
+            rows_rank, st, tile_pairs, phase_ms = -(-n // world), skip, 128 * 96, score_avg
+            kname = "score phase: pairwise_tc_kernel<Check> + <Score>"
+        else:
+            rows_rank, st, tile_pairs, phase_ms = -(-m // world), skip["density"], 128 * 128, query_avg
+            kname = f"density pass: pairwise_tc_kernel<{'Laplace' if job == 'laplace' else 'Gauss'}>"
         exps = rows_rank * n
-        tile_pairs = 128 * 96
-        exec_tiles = max(skip["tiles_total"] - skip["tiles_skipped"], 0) if skip["spatial_order"] \
-            else skip["tiles_total"] or -(-rows_rank // 128) * -(-n // 96)
+        exec_tiles = max(st["tiles_total"] - st["tiles_skipped"], 0) if st["spatial_order"] \
+            else st["tiles_total"] or -(-rows_rank // 128) * -(-n // (tile_pairs // 128))
         exec_exps = exec_tiles * tile_pairs
-        achieved = exec_exps / (score_avg / 1e3) / 1e9      # Gexp/s executed (MUFU)
-        algorithmic = exps / (score_avg / 1e3) / 1e9        # Gpairs/s of the pass's result
+        achieved = exec_exps / (phase_ms / 1e3) / 1e9      # Gexp/s executed (MUFU)
+        algorithmic = exps / (phase_ms / 1e3) / 1e9        # Gpairs/s of the pass's result
         peak = 148 * MUFU_EX2_PER_CLK_SM * max_mhz * 1e6 / 1e9
-        tflops = 4 * d * exps / (score_avg / 1e3) / 1e12    # 2 GEMMs x 2d flop per pair
-        prof = os.path.join(ROOT, "profiles", "ncu_score_pass.json")
+        # score: 2 GEMMs x 2d flop per pair; density: 1 GEMM
+        tflops = (4 if sd else 2) * d * exps / (phase_ms / 1e3) / 1e12
+        prof = os.path.join(ROOT, "profiles", "ncu_score_pass.json" if args.workload == 5
+                            else f"ncu_workload{args.workload}.json")
         traffic = None
         if os.path.exists(prof):
             with open(prof) as f:
                 traffic = json.load(f).get("dram_bytes_per_launch")
+        d2h = m * 8 + (n * d * 8 if sd else 0)
         line = {
-            "metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": world,
+            "metric": metric_of(args.workload), "value": qps, "unit": "queries/s", "n_gpus": world,
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_step,
             "wall_s": wall, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": qps / (N_QUERY / PAPER_WALL_S),
-            "vs_baseline_note": "paper's 2.3 s on one RTX A6000 (PAPER.md:30), same workload",
+            "vs_baseline": qps / (N_QUERY / PAPER_WALL_S) if args.workload == 5 else None,
+            "vs_baseline_note": ("paper's 2.3 s on one RTX A6000 (PAPER.md:30), same workload"
+                                 if args.workload == 5 else "no published number for this config"),
             "dtype": "f32 (fp16 hi/lo split tensor-core operands, f32 accumulate, f64 finalize)",
             "data": "synthetic: reference 16-D Gaussian mixture (configs/mixture-16d-default.json),"
-                    " reference RNG + runtime-sweep seeds, SD-KDE rate bandwidth",
-            "config": workload_config(n, m, d, h),
-            "parallelism": f"dp{world}: score rows sharded, 1 NCCL allgather of debiased samples, "
-                           f"queries sharded",
+                    " reference RNG + runtime-sweep seeds, "
+                    + ("SD-KDE rate bandwidth" if sd else "Silverman bandwidth"),
+            "config": workload_config(n, m, d, h, args.workload),
+            "parallelism": (f"dp{world}: score rows sharded, 1 NCCL allgather of debiased samples, "
+                            f"queries sharded" if sd else f"dp{world}: queries sharded, samples replicated"),
             "phases_ms": {"score_pass": score_avg, "density_pass": query_avg},
             # the reference's own performance model of this run:
             # paper-model pipeline FLOPs (4d+12+d/4+3/2) k^2 (perfmodel.cpp:62-67) and
@@ -380,26 +454,27 @@ def run_ours(args):
             "e2e": {"value": m / e2e_s, "unit": "queries/s", "wall_s": e2e_s,
                     "host_buffers": "pinned",
                     "h2d_bytes_per_step": (n + m) * d * 8,
-                    "d2h_bytes_per_step": m * 8 + n * d * 8, "outputs_finite": out_ok},
+                    "d2h_bytes_per_step": d2h, "outputs_finite": out_ok},
             "e2e_pageable": {"value": m / e2e_pg_s, "unit": "queries/s", "wall_s": e2e_pg_s,
                              "host_buffers": "pageable (numpy)",
                              "h2d_bytes_per_step": (n + m) * d * 8,
-                             "d2h_bytes_per_step": m * 8 + n * d * 8},
+                             "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
             "roofline": {"bound": "mufu",
-                         "kernel": "score phase: pairwise_tc_kernel<Check> + <Score>",
+                         "kernel": kname,
                          "achieved": achieved, "peak": peak, "unit": "Gexp/s (executed)",
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_source": f"nominal 16 ex2/clk/SM x 148 SMs x sm_max_mhz "
                                         f"{max_mhz:.0f} ({src} MEASURED_PEAKS)",
-                         "frac_at_observed_clock": exec_exps / (score_avg / 1e3) /
+                         "frac_at_observed_clock": exec_exps / (phase_ms / 1e3) /
                          (148 * MUFU_EX2_PER_CLK_SM * sm_mhz * 1e6),
                          "algorithmic": {
                              "pairs_per_s_G": algorithmic, "pairs": exps,
                              "vs_full_mufu_roof": algorithmic / peak,
                              "note": "every (row, column) pair of the result per second of the "
-                                     "score phase; above 1 because tile pairs whose every pair "
-                                     "contributes exactly zero in the fp16 P representation "
+                                     "dominant phase; above 1 because tile pairs whose every pair "
+                                     "contributes exactly zero (score: fp16 P representation; "
+                                     "density: below 2^-24 of the row's mass, else recomputed) "
                                      "are proven (box bound) or checked (GEMM1 max) and skipped"},
                          "tile_skipping": skip,
                          "tensor": {"achieved_tflops": tflops,
@@ -409,8 +484,8 @@ def run_ours(args):
         }
         if world == 1 and not args.no_cpu_baseline:
             kind, orc = oracle_handle()
-            smp, full, info = cpu_oracle_sample(orc, kind, X, Y, h)
-            line["cpu_baseline"] = dict(info, value=N_QUERY / full, unit="queries/s",
+            smp, full, info = cpu_oracle_sample(orc, kind, X, Y, h, job=job)
+            line["cpu_baseline"] = dict(info, value=m / full, unit="queries/s",
                                         wall_s=full, reference_flash_engine=REF_FLASH_NOTE)
         print(json.dumps(line), flush=True)
     ctx.close()
@@ -433,7 +508,7 @@ def run_dry(args, rank, world):
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     if rank == 0:
-        print(json.dumps({"metric": METRIC, "dry_run": True, "n_gpus": world,
+        print(json.dumps({"metric": metric_of(args.workload), "dry_run": True, "n_gpus": world,
                           "max_over_ranks": float(t.item()), "steps": args.steps,
                           "warmup": args.warmup}), flush=True)
     if dist:
@@ -463,6 +538,8 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", type=int, default=5, choices=sorted(WORKLOADS),
+                    help="BASELINE.json config (default 5, the headline)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dry-run", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()

@@ -869,7 +869,7 @@ Status query_program(Device& D, const Options& o, const Job& J, const double* dC
     STATUS_TRY(pack2(D, o.pdl, pa, pb));
     record(D, o, FKDE_T_QUERY);
     const uint32_t* dmask = nullptr;
-    int dwords = 0;
+    int dwords = 0, mass_parts = 0;
     const size_t q_rt = rows_pad / kTileRows, q_ct = cols_pad / kTileRows;
     D.dtiles_total = static_cast<uint64_t>(q_rt) * q_ct;
     if (skipping) {
@@ -881,9 +881,9 @@ Status query_program(Device& D, const Options& o, const Job& J, const double* dC
         STATUS_TRY(ensure(D.pmask, q_rt * dwords * sizeof(uint32_t)));
         STATUS_TRY(ensure(D.smask, q_rt * dwords * sizeof(uint32_t)));
         STATUS_TRY(ensure(D.qskip, q_rt * sizeof(unsigned int)));
-        STATUS_TRY(ensure(D.qmass, q_rt * sizeof(float)));
+        mass_parts = (dwords + kPredWords - 1) / kPredWords;   // tile_predict's gridDim.y
+        STATUS_TRY(ensure(D.qmass, q_rt * mass_parts * sizeof(float)));
         CUDA_TRY(cudaMemsetAsync(D.qskip.p, 0, q_rt * sizeof(unsigned int), D.stream));
-        CUDA_TRY(cudaMemsetAsync(D.qmass.p, 0, q_rt * sizeof(float), D.stream));
         if (sh.rows)
             tile_summary<<<static_cast<unsigned>(q_rt), 128, 0, D.stream>>>(
                 dQ + sh.begin * d, sh.rows, d, sc_q, D.ordsc.as<OrderScalars>(), kh, kTileRows, 0,
@@ -927,6 +927,8 @@ Status query_program(Device& D, const Options& o, const Job& J, const double* dC
         r.flag_rows = flag_count + 1;
         r.risk = D.risk.as<uint8_t>();
         r.skip_mass = dmask ? D.qmass.as<float>() : nullptr;
+        r.mass_parts = mass_parts;
+        r.mass_stride = q_rt;
         if (sh.rows) CUDA_TRY(launch_chain(o.pdl, reduce_density, dim3(grid1(sh.rows, 256)), dim3(256), 0, D.stream, r));
         ++D.launches;
     } else if (fused) {
@@ -943,6 +945,8 @@ Status query_program(Device& D, const Options& o, const Job& J, const double* dC
         r.flag_rows = flag_count + 1;
         r.risk = D.risk.as<uint8_t>();
         r.skip_mass = dmask ? D.qmass.as<float>() : nullptr;
+        r.mass_parts = mass_parts;
+        r.mass_stride = q_rt;
         if (sh.rows) CUDA_TRY(launch_chain(o.pdl, reduce_density, dim3(grid1(sh.rows, 256)), dim3(256), 0, D.stream, r));
         ++D.launches;
     } else {

@@ -948,9 +948,14 @@ pairwise_tc_kernel(PairArgs args) {
                 }
             }
             if constexpr (!kScore && !kCheck) {
-                // the kNP phases hold disjoint column subsets of this unit
+                // the kNP phases hold disjoint column subsets of this unit.  The slot
+                // is the phase RELATIVE to the unit (visited tiles k = first_own mod
+                // NP), not the warp's phase: which warp takes a unit's first tile
+                // depends on the tiles the CTA visited before it, i.e. on the dynamic
+                // schedule, and the fixed-order fp64 sum over slots in reduce_density
+                // is then bitwise reproducible from run to run
                 const size_t row = static_cast<size_t>(rt) * kTileRows + r;
-                const size_t idx = static_cast<size_t>(sp * NP + par) * args.rows_pad + row;
+                const size_t idx = static_cast<size_t>(sp * NP + first_own) * args.rows_pad + row;
                 args.part0[idx] = (acc2[0].x + acc2[0].y) + (acc2[1].x + acc2[1].y);
                 if constexpr (MODE == kModeLaplace)
                     args.part1[idx] = (accl2[0].x + accl2[0].y) + (accl2[1].x + accl2[1].y);

@@ -448,6 +448,8 @@ struct ReduceArgs {
     // mass |ca| s0 + |cb| |s1| (the scale of the fp32 sums' own rounding of the row)
     // is below 2^24 times that bound is flagged
     const float* skip_mass;
+    int mass_parts;          // skip_mass holds [mass_parts][mass_stride] partials
+    size_t mass_stride;
 };
 
 __global__ void reduce_density(ReduceArgs a) {
@@ -459,9 +461,12 @@ __global__ void reduce_density(ReduceArgs a) {
     for (int p = 0; p < a.nparts; ++p) s0 += static_cast<double>(a.part0[p * a.rows_pad + j]);
     if (a.part1)
         for (int p = 0; p < a.nparts; ++p) s1 += static_cast<double>(a.part1[p * a.rows_pad + j]);
-    const bool skipped_mass =
-        a.skip_mass && fabs(a.ca) * s0 + fabs(a.cb * s1) <
-                           0x1p24 * static_cast<double>(a.skip_mass[j / kTileRows]);
+    bool skipped_mass = false;
+    if (a.skip_mass) {   // (all lanes of a warp read the same row tile's partials: broadcast)
+        float mass = 0.f;
+        for (int p = 0; p < a.mass_parts; ++p) mass += a.skip_mass[p * a.mass_stride + j / kTileRows];
+        skipped_mass = fabs(a.ca) * s0 + fabs(a.cb * s1) < 0x1p24 * static_cast<double>(mass);
+    }
     if (a.flag_rows && (s0 < kDensityFlagMass || (a.risk && a.risk[j]) || skipped_mass)) {
         a.flag_rows[atomicAdd(a.flag_count, 1u)] = static_cast<unsigned int>(j);
         return;

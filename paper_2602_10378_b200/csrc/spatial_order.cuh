@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(128) tile_predict(const float* __restrict__ ce
                                                     uint32_t* __restrict__ pred,
                                                     uint32_t* __restrict__ skip,
                                                     unsigned int* __restrict__ skip_count,
-                                                    float* __restrict__ skip_mass = nullptr,
+                                                    float* __restrict__ skip_mass = nullptr,   // [gridDim.y][row_tiles]
                                                     int lap_d = -1, float tile_w = 128.f) {
     pdl_launch_dependents();
     pdl_wait();
@@ -371,7 +371,10 @@ __global__ void __launch_bounds__(128) tile_predict(const float* __restrict__ ce
         nskip += __popc(sbits);
     }
     if (skip_count && nskip) atomicAdd(skip_count + rt, nskip);
-    if (skip_mass && mass > 0.f) atomicAdd(skip_mass + rt, mass * tile_w * 1.001f);
+    // one partial per (column-word block, row tile), summed in a fixed order by the
+    // consumer (reduce_density): a float atomicAdd here made the bound -- and with
+    // it which rows are recomputed -- depend on the blocks' arrival order
+    if (skip_mass) skip_mass[(size_t)blockIdx.y * row_tiles + rt] = mass * tile_w * 1.001f;
 }
 
 }  // namespace fkde_b200

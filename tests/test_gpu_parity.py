@@ -802,3 +802,26 @@ def test_score_device_api_matches_host_api(ctx, port):
         assert rc == 0, ctx.last_error()
         stream.synchronize()
         assert np.array_equal(dS.cpu().numpy(), host)
+
+
+@pytest.mark.parametrize("kind", ["sdkde", "laplace"])
+def test_repeat_calls_are_bitwise_under_dynamic_scheduling(ctx, port, kind):
+    # Many units per CTA: the dynamic unit scheduler hands a unit to whichever CTA
+    # is free, so the CTA (and the epilogue warp taking a unit's first tile) varies
+    # from call to call.  The per-phase density partials (pairwise_tc.cuh: the
+    # unit-relative slot) and the skipped-mass bound (tile_predict: per-block
+    # partials summed in order) must not depend on it: repeated calls -- eager and
+    # graph-replayed, host and device buffers -- agree bit for bit.
+    n, m = 131072, 65536
+    tr, q = _mixture_inputs(port, n, m)
+    h = port.silverman_bandwidth(tr)
+    outs = []
+    for _ in range(3):
+        if kind == "sdkde":
+            r = fk.sdkde_flash(tr, q, fk.Bandwidth.uniform(h), ctx=ctx)
+            outs.append((r.values, r.debiased_samples.values))
+        else:
+            outs.append((fk.kde_flash(tr, q, h, fk.KernelKind.LaplaceCorrected, True, ctx=ctx).values,))
+    for o in outs[1:]:
+        for a, b in zip(outs[0], o):
+            assert np.array_equal(a, b), float(np.max(np.abs(a - b)))

@@ -86,7 +86,7 @@ def fnum(x):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("reps", nargs="+")
-    ap.add_argument("--launches")
+    ap.add_argument("--launches", action="append", default=[])
     ap.add_argument("--out", default="profiles/round1")
     a = ap.parse_args()
     os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
@@ -127,21 +127,30 @@ def main():
                 for s, ins in top:
                     md.append(f"- {100.0 * s / tot:5.1f}%  `{ins}`")
                 md.append("")
-            if "pairwise_tc_kernel<0>" in norm(name) and "1m" in os.path.basename(rep):
+            wl = re.match(r"prof_w(\d)", os.path.basename(rep))
+            if ("pairwise_tc_kernel<0>" in norm(name) and "1m" in os.path.basename(rep)) or \
+                    (wl and "pairwise_tc_kernel" in norm(name)):
                 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
                 rd = fnum(k.get("dram__bytes_read.sum"))
                 wr = fnum(k.get("dram__bytes_write.sum"))
                 if rd is not None and wr is not None:
                     rd *= scale.get(k["_units"].get("dram__bytes_read.sum", "byte"), 1)
                     wr *= scale.get(k["_units"].get("dram__bytes_write.sum", "byte"), 1)
-                    score_json = {"kernel": name, "report": os.path.basename(rep),
-                                  "dram_bytes_per_launch": rd + wr,
-                                  "duration": k.get("gpu__time_duration.sum"),
-                                  "duration_unit": k["_units"].get("gpu__time_duration.sum")}
-    if a.launches and os.path.exists(a.launches):
-        shutil.copy(a.launches, a.out + "_launches.csv")
+                    js = {"kernel": name, "report": os.path.basename(rep),
+                          "dram_bytes_per_launch": rd + wr,
+                          "duration": k.get("gpu__time_duration.sum"),
+                          "duration_unit": k["_units"].get("gpu__time_duration.sum")}
+                    if wl:   # bench.py --workload K reads profiles/ncu_workloadK.json
+                        with open(os.path.join(os.path.dirname(a.out), f"ncu_workload{wl.group(1)}.json"),
+                                  "w") as f:
+                            json.dump(js, f, indent=1)
+                    else:
+                        score_json = js
+    for li, lf in enumerate(x for x in a.launches if os.path.exists(x)):
+        suffix = "" if len(a.launches) == 1 else "_" + os.path.splitext(os.path.basename(lf))[0]
+        shutil.copy(lf, a.out + suffix + "_launches.csv")
         # launch-time shares per kernel name
-        rows = list(csv.reader(open(a.launches)))
+        rows = list(csv.reader(open(lf)))
         hdr_i = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
         hdr = rows[hdr_i]
         ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
@@ -153,7 +162,7 @@ def main():
                     nm = r[ki].split("(")[0]
                     agg[nm] = agg.get(nm, 0.0) + v
         tot = sum(agg.values()) or 1
-        md.append("## Launch list share (bench.py --steps 2, gpu__time_duration)")
+        md.append(f"## Launch list share ({os.path.basename(lf)}: bench.py --steps 2, gpu__time_duration)")
         md.append("")
         md.append("| kernel | total | share |")
         md.append("|---|---|---|")
