@@ -535,10 +535,11 @@ bool use_spatial(const Options& o, size_t n) {
 // Spatial order of the training points (spatial_order.cuh): D.Xs = X[perm],
 // D.perm = perm.  Identical on every rank (deterministic from the same input).
 Status spatial_order(Device& D, const double* dX, size_t n, int d, const PassScalars* sc) {
-    const int nparts = static_cast<int>(std::min<size_t>(296, std::max<size_t>(1, n / 256)));
+    const size_t ns = cov_sample_count(n);
+    const int nparts = static_cast<int>(std::min<size_t>(296, std::max<size_t>(1, ns / 256)));
     STATUS_TRY(ensure(D.colpart, static_cast<size_t>(nparts) * 256 * sizeof(double)));
     STATUS_TRY(ensure(D.ordsc, sizeof(OrderScalars)));
-    cov_stage1<<<nparts, 256, 0, D.stream>>>(dX, n, d, sc, D.colpart.as<double>());
+    cov_stage1<<<nparts, 256, 0, D.stream>>>(dX, n, ns, d, sc, D.colpart.as<double>());
     order_axes<<<1, 256, 0, D.stream>>>(D.colpart.as<double>(), nparts, d, D.ordsc.as<OrderScalars>());
     STATUS_TRY(ensure(D.keys, 2 * n * sizeof(uint32_t)));        // keys in | keys out
     STATUS_TRY(ensure(D.perm, 2 * n * sizeof(uint32_t)));        // idx in | perm
@@ -546,7 +547,7 @@ Status spatial_order(Device& D, const double* dX, size_t n, int d, const PassSca
     uint32_t* kout = kin + n;
     uint32_t* iin = D.perm.as<uint32_t>() + n;
     uint32_t* perm = D.perm.as<uint32_t>();
-    morton_keys<<<grid1(n, 256), 256, 0, D.stream>>>(dX, n, d, std::sqrt(static_cast<double>(n)), sc,
+    morton_keys<<<grid1(n, 256), 256, 0, D.stream>>>(dX, n, d, std::sqrt(static_cast<double>(ns)), sc,
                                                       D.ordsc.as<OrderScalars>(), kin, iin);
     size_t tmp = 0;
     CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin, kout, iin, perm, static_cast<int>(n),
@@ -582,7 +583,8 @@ Status order_queries(Device& D, const double* dQ, size_t m, int d, size_t n_cov,
     uint32_t* kout = kin + m;
     uint32_t* iin = D.qperm.as<uint32_t>() + m;
     uint32_t* perm = D.qperm.as<uint32_t>();
-    morton_keys<<<grid1(m, 256), 256, 0, D.stream>>>(dQ, m, d, std::sqrt(static_cast<double>(n_cov)), sc,
+    morton_keys<<<grid1(m, 256), 256, 0, D.stream>>>(dQ, m, d,
+                                                      std::sqrt(static_cast<double>(cov_sample_count(n_cov))), sc,
                                                       D.ordsc.as<OrderScalars>(), kin, iin);
     size_t tmp = 0;
     CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin, kout, iin, perm, static_cast<int>(m), 0,
@@ -701,11 +703,11 @@ Status score_program(Device& D, const Options& o, const Job& J, const double* dX
         // proven-zero threshold on the lower bound of r^2/2 (log2 units): every pair
         // then has log2 phi' = 15 - r^2/2 < kSkipLog2 - 0.5 (float boxes' margin)
         const float proven = 15.0f - kSkipLog2 + 0.5f;
-        tile_predict<<<dim3(grid1(rt, 128), static_cast<unsigned>((words + kPredWords - 1) / kPredWords)),
-                       128, 0, D.stream>>>(
+        const PredShape ps = pred_shape(rt, words, D.num_sms);
+        tile_predict<<<dim3(ps.gx, ps.gy), ps.rows, 0, D.stream>>>(
             D.cenA.as<float>(), D.boxA.as<float>(), static_cast<int>(rt), D.cenB.as<float>(),
             D.boxB.as<float>(), static_cast<int>(ct), words, pred, proven, D.pmask.as<uint32_t>(),
-            D.smask.as<uint32_t>(), nullptr);
+            D.smask.as<uint32_t>(), nullptr, nullptr, -1, 128.f, static_cast<int>(ps.wpb));
         D.launches += 1;
         CUDA_TRY(cudaGetLastError());
         PairArgs c = a;
@@ -881,7 +883,8 @@ Status query_program(Device& D, const Options& o, const Job& J, const double* dC
         STATUS_TRY(ensure(D.pmask, q_rt * dwords * sizeof(uint32_t)));
         STATUS_TRY(ensure(D.smask, q_rt * dwords * sizeof(uint32_t)));
         STATUS_TRY(ensure(D.qskip, q_rt * sizeof(unsigned int)));
-        mass_parts = (dwords + kPredWords - 1) / kPredWords;   // tile_predict's gridDim.y
+        const PredShape ps = pred_shape(q_rt, dwords, D.num_sms);
+        mass_parts = static_cast<int>(ps.gy);   // tile_predict's gridDim.y
         STATUS_TRY(ensure(D.qmass, q_rt * mass_parts * sizeof(float)));
         CUDA_TRY(cudaMemsetAsync(D.qskip.p, 0, q_rt * sizeof(unsigned int), D.stream));
         if (sh.rows)
@@ -892,12 +895,11 @@ Status query_program(Device& D, const Options& o, const Job& J, const double* dC
             dCols, n, d, sc_q, D.ordsc.as<OrderScalars>(), kh, kTileRows, cols_centred ? 1 : 0,
             D.cenB.as<float>(), D.boxB.as<float>());
         // (no predicted pairs: thresh = inf; only the proven bound skips)
-        tile_predict<<<dim3(grid1(q_rt, 128), static_cast<unsigned>((dwords + kPredWords - 1) / kPredWords)),
-                       128, 0, D.stream>>>(
+        tile_predict<<<dim3(ps.gx, ps.gy), ps.rows, 0, D.stream>>>(
             D.cenA.as<float>(), D.boxA.as<float>(), static_cast<int>(q_rt), D.cenB.as<float>(),
             D.boxB.as<float>(), static_cast<int>(q_ct), dwords, INFINITY, kDensitySkipHalfR2,
             D.pmask.as<uint32_t>(), D.smask.as<uint32_t>(), D.qskip.as<unsigned int>(), D.qmass.as<float>(),
-            kernel == FKDE_KERNEL_GAUSSIAN ? -1 : d, static_cast<float>(kTileRows));
+            kernel == FKDE_KERNEL_GAUSSIAN ? -1 : d, static_cast<float>(kTileRows), static_cast<int>(ps.wpb));
         D.launches += 3;
         CUDA_TRY(cudaGetLastError());
         dmask = D.smask.as<uint32_t>();

@@ -77,14 +77,30 @@ __global__ void __launch_bounds__(256) prep_stats(PrepArgs a) {
     if (!s_last) return;
     __threadfence();
     __shared__ double bound[16];
+    // the partials reduced by all 256 threads: thread (g, c) folds blocks g, g + 16, ...
+    // in order, then thread c folds the 16 group sums in order -- a fixed association,
+    // so the mean stays deterministic; a single thread per column walking every block's
+    // partial serially was a chain of L2 round trips (~40 us at 256 blocks)
+    {
+        double s = 0.0, l = INFINITY, h = -INFINITY;
+        for (unsigned b = g; b < gridDim.x; b += 16) {
+            const double* q = a.part + static_cast<size_t>(b) * 48;
+            s += __ldcg(q + c);
+            l = fmin(l, __ldcg(q + 16 + c));
+            h = fmax(h, __ldcg(q + 32 + c));
+        }
+        sm[g][c] = s;
+        mn[g][c] = l;
+        mx[g][c] = h;
+    }
+    __syncthreads();
     if (threadIdx.x < 16) {
         const int cc = threadIdx.x;
         double s = 0.0, l = INFINITY, h = -INFINITY;
-        for (unsigned b = 0; b < gridDim.x; ++b) {   // block order: deterministic
-            const double* q = a.part + static_cast<size_t>(b) * 48;
-            s += __ldcg(q + cc);
-            l = fmin(l, __ldcg(q + 16 + cc));
-            h = fmax(h, __ldcg(q + 32 + cc));
+        for (int k = 0; k < 16; ++k) {
+            s += sm[k][cc];
+            l = fmin(l, mn[k][cc]);
+            h = fmax(h, mx[k][cc]);
         }
         const double mu = (cc < a.d) ? s / static_cast<double>(a.n) : 0.0;
         a.sc->mu[cc] = mu;
@@ -163,10 +179,20 @@ __global__ void __launch_bounds__(256) scale_two(ScaleArgs a) {
         s_last = atomicAdd(a.done, 1u) == gridDim.x - 1;
     }
     __syncthreads();
-    if (!s_last || threadIdx.x != 0) return;
+    if (!s_last) return;
     __threadfence();
+    // every thread of the last block folds a strided slice of the block maxima (a
+    // max: any order gives the same bits), then a warp + block max
     float m = 0.f;
-    for (unsigned b = 0; b < gridDim.x; ++b) m = fmaxf(m, __uint_as_float(__ldcg(a.block_max + b)));
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x)
+        m = fmaxf(m, __uint_as_float(__ldcg(a.block_max + b)));
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    m = 0.f;
+    for (int w = 0; w < 8; ++w) m = fmaxf(m, wmax[w]);
     for (int c = 0; c < kMaxDim; ++c) a.sc->mu[c] = a.mu_src->mu[c];
     a.sc->max_half_norm_bits = __float_as_uint(m);
     int e = 0;
@@ -394,6 +420,7 @@ __global__ void finalize_score(FinalizeArgs a) {
     // S' and T' exclude the self pair (phi_ii = exp(0) = 1, engine.cpp:43-50
     // snaps r_ii^2 to 0): S = 1 + S', and T - x_i S = T' - x_i S'.
     double Sp = 0.0;
+#pragma unroll 4
     for (int s = 0; s < a.splits; ++s) Sp += a.part_s[s * a.rows_pad + i];
     Sp = ldexp(Sp, -kPScaleExp);  // the tc/simt score sums carry phi * 2^15
     // too little neighbour mass for fp16 P, or too much spread for the expansion
@@ -411,6 +438,7 @@ __global__ void finalize_score(FinalizeArgs a) {
     }
     const double inv = 1.0 / (a.h_score * a.h_score * S);
     double Tp = 0.0;
+#pragma unroll 4
     for (int s = 0; s < a.splits; ++s) Tp += a.part_t[(s * a.rows_pad + i) * kMaxDim + c];
     const double tc = ldexp(Tp, -kPScaleExp) / ys;  // sum_{j != i} phi_ij xc_j
     const double x = a.x[g * a.d + c];

@@ -35,20 +35,27 @@ struct OrderScalars {
     double inv_scale[kOrderAxes];       // 1 / (4 sqrt(lambda_k)): projections -> ~[-1, 1]
 };
 
-// ---- covariance partials: block b sums (x - mu)(x - mu)^T over its row range ------------
-__global__ void __launch_bounds__(256) cov_stage1(const double* __restrict__ x, size_t n, int d,
-                                                  const PassScalars* __restrict__ sc,
+// ---- covariance partials: block b sums (x - mu)(x - mu)^T over its sample range ---------
+// The axes only choose the ordering (any basis orders correctly; the results'
+// arithmetic never depends on it), so the covariance is taken over a fixed strided
+// sample of ns <= kCovSample points -- point (k n) / ns for k < ns, deterministic --
+// rather than all n (at n = 2^20 the full sum was ~0.2 ms per call).
+constexpr size_t kCovSample = 65536;
+inline size_t cov_sample_count(size_t n) { return n < kCovSample ? n : kCovSample; }
+__global__ void __launch_bounds__(256) cov_stage1(const double* __restrict__ x, size_t n, size_t ns,
+                                                  int d, const PassScalars* __restrict__ sc,
                                                   double* __restrict__ part /* [grid][256] */) {
     __shared__ double rows[64][kMaxDim];
     const int a = threadIdx.x >> 4, b = threadIdx.x & 15;
-    const size_t r0 = n * blockIdx.x / gridDim.x, r1 = n * (blockIdx.x + 1) / gridDim.x;
+    const size_t r0 = ns * blockIdx.x / gridDim.x, r1 = ns * (blockIdx.x + 1) / gridDim.x;
     double acc = 0.0;
     for (size_t base = r0; base < r1; base += 64) {
         const int nr = static_cast<int>(r1 - base < 64 ? r1 - base : 64);
         __syncthreads();
         for (int e = threadIdx.x; e < 64 * kMaxDim; e += 256) {
             const int r = e / kMaxDim, c = e % kMaxDim;
-            rows[r][c] = (r < nr && c < d) ? x[(base + r) * d + c] - sc->mu[c] : 0.0;
+            const size_t row = (base + r) * n / ns;   // (== base + r when ns == n)
+            rows[r][c] = (r < nr && c < d) ? x[row * d + c] - sc->mu[c] : 0.0;
         }
         __syncthreads();
         for (int r = 0; r < nr; ++r) acc = fma(rows[r][a], rows[r][b], acc);
@@ -292,7 +299,28 @@ __global__ void __launch_bounds__(128) tile_summary(const double* __restrict__ x
 // each): the column tiles' summaries are staged once in shared memory, so each
 // summary is read from global memory once per 128 row tiles (a thread per (row
 // tile, word) re-reading its 32 column summaries moved ~14 GB at n = 2^20).
-constexpr int kPredWords = 4;
+constexpr int kPredWords = 4;   // mask words per block at most (wpb <= kPredWords)
+
+// tile_predict's launch shape: blocks of `rows` row tiles (one per thread) x `wpb`
+// mask words.  Large problems use 128 x kPredWords (each column summary read from
+// global memory once per 128 row tiles); small ones (a few hundred tiles a side)
+// halve both until the grid covers the GPU twice, instead of leaving a handful of
+// blocks to walk 128 column tiles per thread.
+struct PredShape {
+    unsigned rows, wpb, gx, gy;
+};
+inline PredShape pred_shape(size_t row_tiles, int words, int sms) {
+    PredShape p{128u, static_cast<unsigned>(kPredWords), 0u, 0u};
+    for (;;) {
+        p.gx = static_cast<unsigned>((row_tiles + p.rows - 1) / p.rows);
+        p.gy = static_cast<unsigned>((words + p.wpb - 1) / p.wpb);
+        if (static_cast<size_t>(p.gx) * p.gy >= 2u * static_cast<unsigned>(sms)) break;
+        if (p.wpb > 1) p.wpb >>= 1;
+        else if (p.rows > 32) p.rows >>= 1;
+        else break;
+    }
+    return p;
+}
 constexpr int kSumFloats = kMaxDim + kBoxFloats;   // centroid + boxes
 __global__ void __launch_bounds__(128) tile_predict(const float* __restrict__ cenA,
                                                     const float* __restrict__ boxA, int row_tiles,
@@ -303,13 +331,14 @@ __global__ void __launch_bounds__(128) tile_predict(const float* __restrict__ ce
                                                     uint32_t* __restrict__ skip,
                                                     unsigned int* __restrict__ skip_count,
                                                     float* __restrict__ skip_mass = nullptr,   // [gridDim.y][row_tiles]
-                                                    int lap_d = -1, float tile_w = 128.f) {
+                                                    int lap_d = -1, float tile_w = 128.f,
+                                                    int wpb = kPredWords) {
     pdl_launch_dependents();
     pdl_wait();
     __shared__ float colsum[kPredWords * 32][kSumFloats];
-    const int w0 = blockIdx.y * kPredWords;
+    const int w0 = blockIdx.y * wpb;
     const int ct0 = w0 * 32;
-    const int nct = min(kPredWords * 32, col_tiles - ct0);
+    const int nct = min(wpb * 32, col_tiles - ct0);
     for (int e = threadIdx.x; e < nct * kSumFloats; e += blockDim.x) {
         const int j = e / kSumFloats, v = e % kSumFloats;
         colsum[j][v] = v < kMaxDim ? cenB[(size_t)(ct0 + j) * kMaxDim + v]
@@ -325,7 +354,7 @@ __global__ void __launch_bounds__(128) tile_predict(const float* __restrict__ ce
     for (int c = 0; c < kBoxFloats; ++c) ab[c] = boxA[(size_t)rt * kBoxFloats + c];
     unsigned int nskip = 0;
     float mass = 0.f;
-    for (int wi = 0; wi < kPredWords && w0 + wi < words; ++wi) {
+    for (int wi = 0; wi < wpb && w0 + wi < words; ++wi) {
         uint32_t pbits = 0, sbits = 0;
         for (int b = 0; b < 32; ++b) {
             const int j = wi * 32 + b;
