@@ -551,10 +551,10 @@ Status spatial_order(Device& D, const double* dX, size_t n, int d, const PassSca
                                                       D.ordsc.as<OrderScalars>(), kin, iin);
     size_t tmp = 0;
     CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin, kout, iin, perm, static_cast<int>(n),
-                                             0, kOrderAxes * kMortonBits, D.stream));
+                                             0, kSortBits, D.stream));
     STATUS_TRY(ensure(D.cubtmp, tmp));
     CUDA_TRY(cub::DeviceRadixSort::SortPairs(D.cubtmp.p, tmp, kin, kout, iin, perm, static_cast<int>(n),
-                                             0, kOrderAxes * kMortonBits, D.stream));
+                                             0, kSortBits, D.stream));
     STATUS_TRY(ensure(D.Xs, n * d * sizeof(double)));
     gather_rows<<<grid1(n * d, 256), 256, 0, D.stream>>>(dX, perm, n, d, D.Xs.as<double>());
     D.launches += 4;   // (+ CUB's own sort kernels)
@@ -588,10 +588,10 @@ Status order_queries(Device& D, const double* dQ, size_t m, int d, size_t n_cov,
                                                       D.ordsc.as<OrderScalars>(), kin, iin);
     size_t tmp = 0;
     CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin, kout, iin, perm, static_cast<int>(m), 0,
-                                             kOrderAxes * kMortonBits, D.stream));
+                                             kSortBits, D.stream));
     STATUS_TRY(ensure(D.qcubtmp, tmp));
     CUDA_TRY(cub::DeviceRadixSort::SortPairs(D.qcubtmp.p, tmp, kin, kout, iin, perm, static_cast<int>(m),
-                                             0, kOrderAxes * kMortonBits, D.stream));
+                                             0, kSortBits, D.stream));
     STATUS_TRY(ensure(D.Qs, m * d * sizeof(double)));
     gather_rows<<<grid1(m * d, 256), 256, 0, D.stream>>>(dQ, perm, m, d, D.Qs.as<double>());
     D.launches += 2;

@@ -29,6 +29,15 @@ namespace fkde_b200 {
 
 constexpr int kOrderAxes = 3;
 constexpr int kMortonBits = 10;     // per axis -> 30-bit keys
+// bits of the key the sort orders by: the top FKDE_MORTON_SORT_BITS of the 30-bit
+// Morton key (the top 8 bits of each axis at 24: a cell is 1/256 of +-4 sigma per
+// axis, far finer than a 128-point tile) -- CUB's onesweep sort then runs 3
+// passes of 8 bits instead of 4
+#ifndef FKDE_MORTON_SORT_BITS
+#define FKDE_MORTON_SORT_BITS 24
+#endif
+constexpr int kSortBits = FKDE_MORTON_SORT_BITS;
+static_assert(kSortBits <= kOrderAxes * kMortonBits, "sort bits within the key");
 
 struct OrderScalars {
     double axis[kOrderAxes][kMaxDim];   // unit principal axes
@@ -77,8 +86,18 @@ __global__ void __launch_bounds__(256) order_axes(const double* __restrict__ par
     __shared__ double C[kMaxDim][kMaxDim];
     const int t = threadIdx.x;
     {
+        // (unrolled: 8 independent L2 loads in flight instead of one round trip per
+        // partial; the association order is fixed, so C is deterministic)
         double s = 0.0;
-        for (int p = 0; p < nparts; ++p) s += part[p * 256 + t];
+        int p = 0;
+        for (; p + 8 <= nparts; p += 8) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = part[(p + u) * 256 + t];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) s += v[u];
+        }
+        for (; p < nparts; ++p) s += part[p * 256 + t];
         C[t >> 4][t & 15] = s;
     }
     __syncthreads();
@@ -94,10 +113,13 @@ __global__ void __launch_bounds__(256) order_axes(const double* __restrict__ par
         double z[kOrderAxes];
 #pragma unroll
         for (int k = 0; k < kOrderAxes; ++k) {   // z = C q (row r)
-            double acc = 0.0;
+            double acc0 = 0.0, acc1 = 0.0;   // two chains: half the dependent-FMA latency
 #pragma unroll
-            for (int c = 0; c < kMaxDim; ++c) acc = fma(crow[c], __shfl_sync(0xffffffffu, q[k], c), acc);
-            z[k] = acc;
+            for (int c = 0; c < kMaxDim; c += 2) {
+                acc0 = fma(crow[c], __shfl_sync(0xffffffffu, q[k], c), acc0);
+                acc1 = fma(crow[c + 1], __shfl_sync(0xffffffffu, q[k], c + 1), acc1);
+            }
+            z[k] = acc0 + acc1;
         }
 #pragma unroll
         for (int k = 0; k < kOrderAxes; ++k) {   // modified Gram-Schmidt
@@ -177,7 +199,7 @@ __global__ void morton_keys(const double* __restrict__ x, size_t n, int d, doubl
         if (!(u == u)) u = 0.0;
         key |= spread3(static_cast<uint32_t>(u)) << (kOrderAxes - 1 - k);
     }
-    keys[i] = key;
+    keys[i] = key >> (kOrderAxes * kMortonBits - kSortBits);
     idx[i] = static_cast<uint32_t>(i);
 }
 
@@ -215,58 +237,53 @@ __global__ void __launch_bounds__(128) tile_summary(const double* __restrict__ x
                                                     const OrderScalars* __restrict__ os, double k,
                                                     int tile_w, int centred, float* __restrict__ cen,
                                                     float* __restrict__ box) {
-    __shared__ float red[4][3][kMaxDim + kOrderAxes];   // per warp: sum, min, max
+    constexpr int V = kMaxDim + kOrderAxes;
+    // the 128 points' 19 values go through shared memory and are reduced by 76
+    // threads (value v, interleaved quarter p of the rows), not by 19 x 3 five-level
+    // shuffle trees per warp (~1100 SHFL per tile)
+    constexpr int kStride = V + 1;
+    __shared__ float vals[128 * kStride];
+    __shared__ unsigned char ok[128];
     const size_t r0 = static_cast<size_t>(blockIdx.x) * tile_w;
     const size_t r1 = r0 + tile_w < n ? r0 + tile_w : n;
     const size_t r = r0 + threadIdx.x;
     const bool valid = threadIdx.x < tile_w && r < r1;
-    constexpr int V = kMaxDim + kOrderAxes;
-    float sum[V], lo[V], hi[V];
     {
         double y[kMaxDim];
 #pragma unroll
         for (int c = 0; c < kMaxDim; ++c)
             y[c] = (valid && c < d) ? (x[r * d + c] - (centred ? 0.0 : sc->mu[c])) * k : 0.0;
+        float* row = vals + threadIdx.x * kStride;
 #pragma unroll
-        for (int c = 0; c < kMaxDim; ++c) sum[c] = static_cast<float>(y[c]);
+        for (int c = 0; c < kMaxDim; ++c) row[c] = static_cast<float>(y[c]);
 #pragma unroll
         for (int a = 0; a < kOrderAxes; ++a) {
             double p = 0.0;
 #pragma unroll
             for (int c = 0; c < kMaxDim; ++c) p = fma(y[c], os->axis[a][c], p);
-            sum[kMaxDim + a] = static_cast<float>(p);
+            row[kMaxDim + a] = static_cast<float>(p);
         }
-#pragma unroll
-        for (int v = 0; v < V; ++v) {
-            lo[v] = valid ? sum[v] : INFINITY;
-            hi[v] = valid ? sum[v] : -INFINITY;
-            if (!valid) sum[v] = 0.f;
-        }
+        ok[threadIdx.x] = valid ? 1 : 0;
     }
-#pragma unroll
-    for (int v = 0; v < V; ++v)
-        for (int o = 16; o > 0; o >>= 1) {
-            sum[v] += __shfl_xor_sync(0xffffffffu, sum[v], o);
-            lo[v] = fminf(lo[v], __shfl_xor_sync(0xffffffffu, lo[v], o));
-            hi[v] = fmaxf(hi[v], __shfl_xor_sync(0xffffffffu, hi[v], o));
-        }
-    const int w = threadIdx.x >> 5;
-    if ((threadIdx.x & 31) == 0)
-#pragma unroll
-        for (int v = 0; v < V; ++v) {
-            red[w][0][v] = sum[v];
-            red[w][1][v] = lo[v];
-            red[w][2][v] = hi[v];
-        }
     __syncthreads();
-    if (threadIdx.x < V) {
-        const int v = threadIdx.x;
-        float s = 0.f, l = INFINITY, h = -INFINITY;
-        for (int q = 0; q < 4; ++q) {
-            s += red[q][0][v];
-            l = fminf(l, red[q][1][v]);
-            h = fmaxf(h, red[q][2][v]);
+    const int t = threadIdx.x;
+    if (t >= 96) return;   // warps 0-2 (whole warps: the shuffles below): t = 4v + p, v < V work
+    const int v = t >> 2, p = t & 3;
+    float s = 0.f, l = INFINITY, h = -INFINITY;
+    if (v < V)
+        for (int i = p; i < 128; i += 4) {   // fixed order per quarter: deterministic
+            if (!ok[i]) continue;
+            const float x = vals[i * kStride + v];
+            s += x;
+            l = fminf(l, x);
+            h = fmaxf(h, x);
         }
+    for (int o = 1; o < 4; o <<= 1) {   // the four quarters (lanes 4v .. 4v+3)
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+        l = fminf(l, __shfl_xor_sync(0xffffffffu, l, o));
+        h = fmaxf(h, __shfl_xor_sync(0xffffffffu, h, o));
+    }
+    if (p == 0 && v < V) {
         const float cnt = r1 > r0 ? static_cast<float>(r1 - r0) : 1.f;
         if (v < kMaxDim) {
             cen[static_cast<size_t>(blockIdx.x) * kMaxDim + v] = r1 > r0 ? s / cnt : 1e18f;
