@@ -115,17 +115,30 @@ constexpr int kB2GroupLog2 = 2;
 #endif
 
 // Column tiles of one unit that a pass visits: [.., end) filtered by a mask row
-// (bit == want).  Every warp of the CTA walks the same sequence.  The walk keeps
-// the current mask word in a register, so a step costs a few integer ops and a
-// load only every 32 tiles (a load per step put an L1 round trip on every tile
-// of every warp's critical path).
-struct TileWalk {
+// (bit == want).  Every warp of the CTA walks the same sequence, warp-uniformly
+// (first / next / count are called by whole converged warps), keeping the current
+// word's remaining bits in a register.  kWindow (the check pass, whose predicted
+// set is ~2 % dense): a window of the next 32 mask words is held one per lane,
+// loaded together, and the next non-empty word is found by a ballot -- one L2
+// round trip per 32 words instead of one per word, which was one per visited tile
+// on such a sparse mask.  The score / density masks are ~30 % dense (a load per ~9
+// visited tiles), where the window's registers cost more (spills in the control
+// warps) than the loads it saves.
+template <bool kWindow>
+struct TileWalkT {
     const uint32_t* row;   // nullptr: every tile
     int end;
     uint32_t want;         // 0u: visit clear bits, ~0u: visit set bits
     int w = 0;             // current word
     uint32_t bits = 0;     // visited tiles of word w not yet returned
+    int base = 0;          // kWindow: lane l holds word base + l (0 past the range)
+    uint32_t cache = 0;
     __device__ __forceinline__ uint32_t word(int i) const { return ~(row[i] ^ want); }
+    __device__ __forceinline__ void load(int b) {
+        base = b;
+        const int i = b + static_cast<int>(threadIdx.x & 31u);
+        cache = (i << 5) < end ? word(i) : 0u;
+    }
     __device__ __forceinline__ int first(int from) {   // first visited tile >= from, or end
         if (!row) {
             w = from;
@@ -133,7 +146,12 @@ struct TileWalk {
         }
         if (from >= end) return end;
         w = from >> 5;
-        bits = word(w) & (0xFFFFFFFFu << (from & 31));
+        if constexpr (kWindow) {
+            load(w);
+            bits = __shfl_sync(0xffffffffu, cache, 0) & (0xFFFFFFFFu << (from & 31));
+        } else {
+            bits = word(w) & (0xFFFFFFFFu << (from & 31));
+        }
         return next();
     }
     __device__ __forceinline__ int next() {   // the following visited tile, or end
@@ -142,25 +160,47 @@ struct TileWalk {
             return w < end ? w : end;
         }
         while (!bits) {
-            if (((w + 1) << 5) >= end) return end;
-            bits = word(++w);
+            if constexpr (kWindow) {
+                const int lane = static_cast<int>(threadIdx.x & 31u);
+                const unsigned ahead = __ballot_sync(0xffffffffu, cache != 0u && base + lane > w);
+                if (ahead) {
+                    const int l = __ffs(ahead) - 1;
+                    w = base + l;
+                    bits = __shfl_sync(0xffffffffu, cache, l);
+                } else {
+                    if (((base + 32) << 5) >= end) return end;
+                    load(base + 32);
+                    w = base - 1;
+                }
+            } else {
+                if (((w + 1) << 5) >= end) return end;
+                bits = word(++w);
+            }
         }
         const int c = (w << 5) + __ffs(bits) - 1;
         bits &= bits - 1u;
         return c < end ? c : end;
     }
-    __device__ __forceinline__ int count(int from) const {   // visited tiles in [from, end)
+    // visited tiles in [from, end).  Called by whole converged warps (every role
+    // walks its units warp-uniformly): the lanes load the range's mask words in
+    // parallel and the popcounts are reduced across the warp.  (One lane walking the
+    // ~50 words of a unit's column range serially put ~50 dependent L2 round trips
+    // at the start of every unit in every warp: 24 % of the check kernel's stall
+    // samples, ncu source view.)
+    __device__ __forceinline__ int count(int from) const {
         if (!row) return end > from ? end - from : 0;
+        if (from >= end) return 0;
+        const int lane = static_cast<int>(threadIdx.x & 31u);
+        const int w0 = from >> 5, w1 = (end - 1) >> 5;
         int n = 0;
-        while (from < end) {
-            const int i = from >> 5;
-            uint32_t b = word(i) & (0xFFFFFFFFu << (from & 31));
+        for (int i = w0 + lane; i <= w1; i += 32) {
+            uint32_t b = word(i);
+            if (i == w0) b &= 0xFFFFFFFFu << (from & 31);
             const int top = end - (i << 5);
             if (top < 32) b &= (1u << top) - 1u;
             n += __popc(b);
-            from = (i + 1) << 5;
         }
-        return n;
+        return static_cast<int>(__reduce_add_sync(0xffffffffu, static_cast<unsigned>(n)));
     }
 };
 
@@ -382,7 +422,7 @@ pairwise_tc_kernel(PairArgs args) {
     };
     // the column tiles a unit visits (score: clear skip bits; check: set pred bits)
     auto walk_of = [&](int rt, int ct1) {
-        TileWalk w;
+        TileWalkT<kCheck> w;
         const uint32_t* m = kCheck ? args.pred_mask : args.skip_mask;
         w.row = m ? m + (size_t)rt * args.mask_words : nullptr;
         w.end = ct1;
@@ -410,7 +450,7 @@ pairwise_tc_kernel(PairArgs args) {
             const int sp = u / args.n_row_tiles, rt = u % args.n_row_tiles;
             const int ct0 = static_cast<int>((long long)sp * args.n_col_tiles / args.splits);
             const int ct1 = static_cast<int>((long long)(sp + 1) * args.n_col_tiles / args.splits);
-            TileWalk wk = walk_of(rt, ct1);
+            auto wk = walk_of(rt, ct1);
             int ct = wk.first(ct0);
             if (ct >= ct1) continue;   // nothing to visit: no A tile either
             const int ab = it_a & 1;
@@ -485,7 +525,7 @@ pairwise_tc_kernel(PairArgs args) {
             const int ct0 = static_cast<int>((long long)sp * args.n_col_tiles / args.splits);
             const int ct1 = static_cast<int>((long long)(sp + 1) * args.n_col_tiles / args.splits);
             // (GEMM1 only needs how many tiles the unit visits, not which)
-            TileWalk wk2 = walk_of(rt, ct1);
+            auto wk2 = walk_of(rt, ct1);
             const int len = wk2.count(ct0);
             if (len == 0) continue;
             int sub_cnt = 0;
@@ -618,7 +658,7 @@ pairwise_tc_kernel(PairArgs args) {
                 const int sp = u / args.n_row_tiles, rt = u % args.n_row_tiles;
                 const int ct0 = static_cast<int>((long long)sp * args.n_col_tiles / args.splits);
                 const int ct1 = static_cast<int>((long long)(sp + 1) * args.n_col_tiles / args.splits);
-                TileWalk wk = walk_of(rt, ct1);
+                auto wk = walk_of(rt, ct1);
                 const int len = wk.count(ct0);
 #if FKDE_DRAIN_F64
                 double acc[kMaxDim + 1];
@@ -773,7 +813,7 @@ pairwise_tc_kernel(PairArgs args) {
             const int sp = u / args.n_row_tiles, rt = u % args.n_row_tiles;
             const int ct0 = static_cast<int>((long long)sp * args.n_col_tiles / args.splits);
             const int ct1 = static_cast<int>((long long)(sp + 1) * args.n_col_tiles / args.splits);
-            TileWalk wk = walk_of(rt, ct1);
+            auto wk = walk_of(rt, ct1);
             float2 acc2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
             float2 accl2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
             // score: global index of this lane's row minus the unit's first
@@ -805,7 +845,7 @@ pairwise_tc_kernel(PairArgs args) {
                 auto vidx = [&](int rel) {
                     const int c = ct0 + rel;
                     if (rel < 0 || c >= ct1 || !((wk.word(c >> 5) >> (c & 31)) & 1u)) return -1;
-                    TileWalk w2 = wk;
+                    auto w2 = wk;
                     w2.end = c;
                     return w2.count(ct0);
                 };
