@@ -48,6 +48,13 @@ constexpr int kDirTargetItems = 4 * 148;
 constexpr int kDirMaxSplits = 256;
 constexpr int kDirPart = 20;         // doubles per (row, split) partial: m, S, L, T[16], pad
 constexpr int kDirFewRows = 64;      // up to this many flagged rows: one row per block
+// The running maximum m of the exponents (log2 units) is raised only when a new
+// exponent exceeds it by more than kDirLazy: terms are then 2^(t - m) <= 2^8, far
+// inside the fp32 / fp64 ranges, and the sums keep their relative precision, but
+// the rescale (an fp64 exp2 and 18 multiplies, divergent across the warp's rows)
+// runs a few times per row instead of at every new record (~20 % of the kernel's
+// stall samples on isolated points, ncu source view).
+constexpr float kDirLazy = 8.0f;
 
 struct DirectArgs {
     int mode;                    // kExactScore / kExactGauss / kExactLaplace
@@ -94,7 +101,7 @@ __device__ __forceinline__ float dir_ex2(float x) {
 
 // finalize one row from merged (M, S, L, T) in the scaled form sum_j 2^(t_ij - M)
 __device__ __forceinline__ void direct_finish_row(const DirectArgs& a, size_t i, float M, double S, double L,
-                                  const double* T) {
+                                  const double* T, int tstride = 1) {
     const double em = M == -INFINITY ? 0.0 : exp2(static_cast<double>(M));
     if (a.mode == kExactScore) {
         const size_t g = a.row0 + i;
@@ -103,7 +110,7 @@ __device__ __forceinline__ void direct_finish_row(const DirectArgs& a, size_t i,
         if (a.phi_sum) a.phi_sum[g] = Stot;
         const double inv = 1.0 / (a.h * a.h * Stot);
         for (int c = 0; c < a.d; ++c) {
-            const double num = em * T[c];      // sum_j phi_ij (x_j - x_i)
+            const double num = em * T[c * tstride];   // sum_j phi_ij (x_j - x_i)
             const double s = num * inv;
             const double xi = a.rowpts[i * a.d + c];
             if (a.score) a.score[g * a.d + c] = s;
@@ -187,7 +194,7 @@ __device__ __forceinline__ void direct_few_rows(const DirectArgs& a, unsigned in
             }
             if (j == self) continue;   // phi_ii = 1 is added back in fp64
             const float t = -r2 * k2;
-            if (t > m) {
+            if (t > m + kDirLazy) {   // lazy running maximum (see kDirLazy)
                 const double f64 = exp2(static_cast<double>(m) - static_cast<double>(t));
                 S64 *= f64;
                 L64 *= f64;
@@ -307,7 +314,12 @@ __global__ void __launch_bounds__(kDirRows) direct_rows_kernel(DirectArgs a) {
             float s32 = 0.f, l32 = 0.f, t32[kMaxDim];
 #pragma unroll
             for (int c = 0; c < kMaxDim; ++c) t32[c] = 0.f;
+            // the self pair (score): its exponent is pushed to -1e30 (phi = 0 exactly;
+            // phi_ii = 1 is added back in fp64) -- an int compare against one index
+            // per tile instead of a 64-bit compare and a divergent branch per pair
+            const int jself = (self >= jt && self < jt + static_cast<size_t>(nt)) ? static_cast<int>(self - jt) : -1;
             if (active) {
+#pragma unroll 2
                 for (int jj = 0; jj < nt; ++jj) {
                     float df[kMaxDim];
                     float r2 = 0.f;
@@ -319,13 +331,21 @@ __global__ void __launch_bounds__(kDirRows) direct_rows_kernel(DirectArgs a) {
                         df[4 * q + 2] = cv.z - u[4 * q + 2];
                         df[4 * q + 3] = cv.w - u[4 * q + 3];
                     }
+                    // four partial sums: a 16-deep dependent FFMA chain per pair was the
+                    // latency that bound this loop at 4 warps per sub-partition
+                    float r2p[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-                    for (int c = 0; c < kMaxDim; ++c) r2 = fmaf(df[c], df[c], r2);
-                    if (jt + jj == self) continue;   // phi_ii = 1 is added back in fp64
-                    const float t = -r2 * k2;
-                    if (t > m) {   // new running maximum: rescale everything so far
+                    for (int c = 0; c < kMaxDim; ++c) r2p[c & 3] = fmaf(df[c], df[c], r2p[c & 3]);
+                    r2 = (r2p[0] + r2p[1]) + (r2p[2] + r2p[3]);
+                    const float t = jj == jself ? -1e30f : -r2 * k2;
+                    if (t > m + kDirLazy) {   // new running maximum (lazy): rescale the sums
+                        // (one fp32 ex2 for both: a software fp64 exp2 here, executed by the
+                        // whole warp whenever any of its rows rescaled, was 11 % of the
+                        // kernel's instructions; the factor's 2^-22 relative error is far
+                        // inside the tolerance, and it underflows to 0 exactly when the old
+                        // terms are below 2^-126 of the new maximum)
                         const float f = dir_ex2(m - t);
-                        const double f64 = exp2(static_cast<double>(m) - static_cast<double>(t));
+                        const double f64 = static_cast<double>(f);
                         s32 *= f;
                         l32 *= f;
 #pragma unroll

@@ -132,7 +132,7 @@ struct TileWalkT {
     int w = 0;             // current word
     uint32_t bits = 0;     // visited tiles of word w not yet returned
     int base = 0;          // kWindow: lane l holds word base + l (0 past the range)
-    uint32_t cache = 0;
+    uint32_t cache = 0;    // !kWindow: word w + 1 (prefetched)
     __device__ __forceinline__ uint32_t word(int i) const { return ~(row[i] ^ want); }
     __device__ __forceinline__ void load(int b) {
         base = b;
@@ -151,6 +151,7 @@ struct TileWalkT {
             bits = __shfl_sync(0xffffffffu, cache, 0) & (0xFFFFFFFFu << (from & 31));
         } else {
             bits = word(w) & (0xFFFFFFFFu << (from & 31));
+            cache = ((w + 1) << 5) < end ? word(w + 1) : 0u;   // the next word, in flight
         }
         return next();
     }
@@ -173,8 +174,13 @@ struct TileWalkT {
                     w = base - 1;
                 }
             } else {
+                // the next word was loaded one word ahead, so its L2 round trip
+                // overlaps the visited tiles of this one (the GEMM2 issuer's walk
+                // sits on the S/P ring's critical path)
                 if (((w + 1) << 5) >= end) return end;
-                bits = word(++w);
+                bits = cache;
+                ++w;
+                cache = ((w + 1) << 5) < end ? word(w + 1) : 0u;
             }
         }
         const int c = (w << 5) + __ffs(bits) - 1;
