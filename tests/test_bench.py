@@ -57,3 +57,23 @@ def test_reference_arm_never_loads_the_product():
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr[-2000:]
     assert "CLEAN" in r.stdout and "NOPKG" in r.stdout, r.stdout
+
+
+def test_reference_arm_every_workload_config():
+    # --workload K (BASELINE.json config K) through the reference arm, CPU only:
+    # the same metric / config keys as the product arm, the reference's own oracle
+    # timed (config 1 and 3: score + density, density only; bounded samples)
+    sys.path.insert(0, ROOT)
+    import bench
+    for wl in (1, 3):
+        env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+        r = subprocess.run([sys.executable, BENCH, "--impl", "reference", "--workload", str(wl),
+                            "--steps", "1", "--warmup", "0"], capture_output=True, text=True,
+                           timeout=600, env=env)
+        assert r.returncode == 0, r.stderr[-2000:]
+        line = _last_json(r.stdout)
+        job, n, m, name = bench.WORKLOADS[wl]
+        assert line["impl"] == "reference" and line["config"]["workload"] == name
+        assert line["config"]["n_train"] == n and line["config"]["n_query"] == m
+        assert line["metric"] == bench.metric_of(wl) and line["value"] > 0
+        assert ("score_naive" in line["cpu_baseline"]["sample"]) == (job == "sdkde")
