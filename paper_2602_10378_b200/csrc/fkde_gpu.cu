@@ -526,7 +526,7 @@ constexpr size_t kSpatialMinN = 32768;
 constexpr float kSkipPredict = 40.0f;
 // score pass on the spatial order: O is drained at every change of the B2 tile group
 // (kB2GroupLog2 column tiles, pairwise_tc.cuh) or after kCentredFlush visited tiles
-constexpr int kCentredFlush = 4;
+constexpr int kCentredFlush = 1 << kB2GroupLog2;   // a whole B2 group
 
 bool use_spatial(const Options& o, size_t n) {
     return o.spatial == 1 || o.spatial == 3 || (o.spatial == 0 && n >= kSpatialMinN);

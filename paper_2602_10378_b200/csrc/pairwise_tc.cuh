@@ -99,8 +99,12 @@ struct PairArgs {
 // log2 phi' (S * dscale, with the 2^15 offset) below which both fp16 halves of
 // phi' are exactly zero (phi' < 2^-25 rounds to zero; one unit of margin for ex2.approx)
 constexpr float kSkipLog2 = -26.0f;
-// score pass on the spatial order: column tiles per B2 group (ones columns 16..19)
-constexpr int kB2GroupLog2 = 2;
+// score pass on the spatial order: column tiles per B2 group (ones columns 16 .. 16 + 2^glog - 1)
+#ifndef FKDE_B2_GROUP_LOG2
+#define FKDE_B2_GROUP_LOG2 3
+#endif
+constexpr int kB2GroupLog2 = FKDE_B2_GROUP_LOG2;
+static_assert(kB2GroupLog2 >= 2 && kB2GroupLog2 <= 4, "ones columns 16 .. 16 + 2^glog - 1 within the block");
 
 #ifdef FKDE_ENABLE_TRACE
 #define FKDE_TRACE(slot, tile)                                                               \
@@ -687,13 +691,14 @@ pairwise_tc_kernel(PairArgs args) {
                     const uint32_t g = it_u++;
                     pend = 0;
                     const uint32_t to = lane_addr + Cfg::kTmemO + (g & 1) * 64;
-                    uint32_t od[16], ol[16], os4[4];
+                    constexpr int kSlots = 1 << kB2GroupLog2;
+                    uint32_t od[16], ol[16], os4[kSlots];
                     FKDE_TRACE(4, g);
                     ptx::mbar_wait(&o_full[g & 1], (g >> 1) & 1);
                     FKDE_TRACE(5, g);
                     ptx::tc_fence_after();
                     ptx::tmem_ld16(to, od);
-                    ptx::tmem_ld4(to + 16, os4);   // S_J per ring slot (non-centred: 16-18 = S)
+                    ptx::tmem_ldn(to + 16, os4);   // S_J per ring slot (non-centred: 16 = S)
                     ptx::tmem_ld16(to + 32, ol);
                     ptx::tmem_ld_wait();
                     ptx::tc_fence_before();

@@ -283,9 +283,10 @@ __device__ __forceinline__ void pack_row_centred(const PackArgs& a, size_t i) {
                 ch[c][w] = pack_h2(vh[k0], vh[k0 + 1]);
                 ch[4 + c][w] = pack_h2(vl[k0], vl[k0 + 1]);
             }
-        // the ones (S_J) in column 16 + (J mod group): chunk-2 word slot/2, half slot%2
+        // the ones (S_J) in column 16 + (J mod group): chunk 2 + slot/8, word (slot/2) mod 4,
+        // half slot%2 (groups of up to 16 tiles: columns 16..31)
         const int slot = static_cast<int>(i / a.cen_tile) & a.ones_mask;
-        ch[2][slot >> 1] = (slot & 1) ? pack_h2(__float2half(0.f), __float2half(1.f))
+        ch[2 + (slot >> 3)][(slot >> 1) & 3] = (slot & 1) ? pack_h2(__float2half(0.f), __float2half(1.f))
                                       : pack_h2(__float2half(1.f), __float2half(0.f));
     }
     const size_t tile = i / kTileRows;
