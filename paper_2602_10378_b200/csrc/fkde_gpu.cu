@@ -196,6 +196,9 @@ struct Device {
     // spatial order of the score pass (spatial_order.cuh): sorted points, permutation,
     // keys, CUB scratch, axes, tile centroids, skip statistics, un-permuted outputs
     DevBuf Xs, perm, keys, cubtmp, ordsc, cenA, cenB, boxA, boxB, skipstats, unperm0, unperm1, pmask, smask;
+    // the density pass's tile masks: its own buffers, so that the score pass's skip mask
+    // (read back by fkde_gpu_last_skip_stats) is not overwritten by the density pass
+    DevBuf dpmask, dsmask;
     size_t mask_bytes = 0;       // skip mask of the last score pass (0: none)
     uint64_t tiles_total = 0;    // tile pairs of the last score pass
     bool ordered = false;        // last score pass ran on the spatial order
@@ -221,7 +224,7 @@ struct Device {
                 &aux0,  &aux1,  &colpart, &scal, &err,  &flags, &risk,      &dpart,   &ddone,
                 &pdone, &sched, &qmax,  &Xs,   &perm,   &keys,  &cubtmp, &ordsc,    &cenA,    &cenB,
                 &boxA,  &boxB,  &skipstats, &unperm0, &unperm1, &pmask, &smask, &Qs, &qperm,
-                &qkeys, &qcubtmp, &qskip, &qmass, &qout};
+                &qkeys, &qcubtmp, &qskip, &qmass, &qout, &dpmask, &dsmask};
     }
 };
 
@@ -570,8 +573,17 @@ Status spatial_order(Device& D, const double* dX, size_t n, int d, const PassSca
 // whose term mass (|ca| s0 + |cb| |s1|: the scale of the fp32 sums' own rounding of
 // that row) is not at least 2^24 times that bound is recomputed by direct
 // differences (reduce_density flags it).  The skip therefore changes no row by more
-// than 2^-24 of its term mass.
-constexpr float kDensitySkipHalfR2 = 45.0f;
+// than 2^-24 of its term mass.  41.5 (phi < 2^-41, the score pass's level): at config
+// 5 it skips 1.6 % more tile pairs than 45 (0.55 ms of the density pass) and sends 4
+// rows instead of 1 to the recompute (tools/density_skip_probe.sh).
+constexpr float kDensitySkipHalfR2 = 41.5f;
+float density_skip_half_r2() {   // (FKDE_DENSITY_SKIP: debug override for A/B runs)
+    static const float v = [] {
+        const char* e = std::getenv("FKDE_DENSITY_SKIP");
+        return e && *e ? static_cast<float>(std::atof(e)) : kDensitySkipHalfR2;
+    }();
+    return v;
+}
 
 // Queries sorted on the training order's axes (D.ordsc; sc: the training mean,
 // n_cov: the count the covariance was summed over): D.Qs = Q[qperm]
@@ -880,8 +892,8 @@ Status query_program(Device& D, const Options& o, const Job& J, const double* dC
         STATUS_TRY(ensure(D.cenB, q_ct * kMaxDim * sizeof(float)));
         STATUS_TRY(ensure(D.boxA, q_rt * kBoxFloats * sizeof(float)));
         STATUS_TRY(ensure(D.boxB, q_ct * kBoxFloats * sizeof(float)));
-        STATUS_TRY(ensure(D.pmask, q_rt * dwords * sizeof(uint32_t)));
-        STATUS_TRY(ensure(D.smask, q_rt * dwords * sizeof(uint32_t)));
+        STATUS_TRY(ensure(D.dpmask, q_rt * dwords * sizeof(uint32_t)));
+        STATUS_TRY(ensure(D.dsmask, q_rt * dwords * sizeof(uint32_t)));
         STATUS_TRY(ensure(D.qskip, q_rt * sizeof(unsigned int)));
         const PredShape ps = pred_shape(q_rt, dwords, D.num_sms);
         mass_parts = static_cast<int>(ps.gy);   // tile_predict's gridDim.y
@@ -897,12 +909,12 @@ Status query_program(Device& D, const Options& o, const Job& J, const double* dC
         // (no predicted pairs: thresh = inf; only the proven bound skips)
         tile_predict<<<dim3(ps.gx, ps.gy), ps.rows, 0, D.stream>>>(
             D.cenA.as<float>(), D.boxA.as<float>(), static_cast<int>(q_rt), D.cenB.as<float>(),
-            D.boxB.as<float>(), static_cast<int>(q_ct), dwords, INFINITY, kDensitySkipHalfR2,
-            D.pmask.as<uint32_t>(), D.smask.as<uint32_t>(), D.qskip.as<unsigned int>(), D.qmass.as<float>(),
+            D.boxB.as<float>(), static_cast<int>(q_ct), dwords, INFINITY, density_skip_half_r2(),
+            D.dpmask.as<uint32_t>(), D.dsmask.as<uint32_t>(), D.qskip.as<unsigned int>(), D.qmass.as<float>(),
             kernel == FKDE_KERNEL_GAUSSIAN ? -1 : d, static_cast<float>(kTileRows), static_cast<int>(ps.wpb));
         D.launches += 3;
         CUDA_TRY(cudaGetLastError());
-        dmask = D.smask.as<uint32_t>();
+        dmask = D.dsmask.as<uint32_t>();
         D.dtiles_rows = q_rt;
     }
 
