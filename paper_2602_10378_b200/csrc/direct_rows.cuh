@@ -183,16 +183,16 @@ __device__ __forceinline__ void direct_few_rows(const DirectArgs& a, unsigned in
         double S64 = 0.0, L64 = 0.0, T64[kMaxDim];
 #pragma unroll
         for (int c = 0; c < kMaxDim; ++c) T64[c] = 0.0;
-        for (size_t j = j0 + threadIdx.x; j < j1; j += kDirRows) {
+        // one column's contribution (coordinates already loaded into vv)
+        auto pair = [&](size_t j, const float (&vv)[kMaxDim]) {
             float df[kMaxDim];
             float r2 = 0.f;
 #pragma unroll
             for (int c = 0; c < kMaxDim; ++c) {
-                const float v = c < d ? static_cast<float>(a.cols[j * d + c] - (a.center_cols ? a.sc->mu[c] : 0.0)) : 0.f;
-                df[c] = v - u[c];
+                df[c] = vv[c] - u[c];
                 r2 = fmaf(df[c], df[c], r2);
             }
-            if (j == self) continue;   // phi_ii = 1 is added back in fp64
+            if (j == self) return;   // phi_ii = 1 is added back in fp64
             const float t = -r2 * k2;
             if (t > m + kDirLazy) {   // lazy running maximum (see kDirLazy)
                 const double f64 = exp2(static_cast<double>(m) - static_cast<double>(t));
@@ -209,6 +209,22 @@ __device__ __forceinline__ void direct_few_rows(const DirectArgs& a, unsigned in
 #pragma unroll
                 for (int c = 0; c < kMaxDim; ++c) T64[c] += static_cast<double>(p * df[c]);
             }
+        };
+        auto load = [&](size_t j, float (&vv)[kMaxDim]) {
+#pragma unroll
+            for (int c = 0; c < kMaxDim; ++c)
+                vv[c] = c < d ? static_cast<float>(a.cols[j * d + c] - (a.center_cols ? a.sc->mu[c] : 0.0)) : 0.f;
+        };
+        // two columns per step, both loaded before either is used: the loop is bound by
+        // the L2 round trip of its column loads (ncu: 83 % of the stall samples at config
+        // 4, issue slots 12 % busy), so two round trips overlap
+        for (size_t j = j0 + threadIdx.x; j < j1; j += 2 * kDirRows) {
+            const size_t j2 = j + kDirRows;
+            float va[kMaxDim], vb[kMaxDim];
+            load(j, va);
+            if (j2 < j1) load(j2, vb);
+            pair(j, va);
+            if (j2 < j1) pair(j2, vb);
         }
         // block reduction: maximum, then the sums rescaled to it
         double v[kMaxDim + 2];
@@ -260,7 +276,9 @@ __device__ __forceinline__ void direct_few_rows(const DirectArgs& a, unsigned in
     }
 }
 
-__global__ void __launch_bounds__(kDirRows) direct_rows_kernel(DirectArgs a) {
+// (<= 128 registers: four blocks per SM, the grid is one wave; the few-row loop's
+// two-column unroll would otherwise take the kernel to ~170)
+__global__ void __launch_bounds__(kDirRows, 4) direct_rows_kernel(DirectArgs a) {
     pdl_launch_dependents();
     pdl_wait();
     __shared__ float4 tile[kDirTileCols][kMaxDim / 4];

@@ -573,10 +573,11 @@ Status spatial_order(Device& D, const double* dX, size_t n, int d, const PassSca
 // whose term mass (|ca| s0 + |cb| |s1|: the scale of the fp32 sums' own rounding of
 // that row) is not at least 2^24 times that bound is recomputed by direct
 // differences (reduce_density flags it).  The skip therefore changes no row by more
-// than 2^-24 of its term mass.  41.5 (phi < 2^-41, the score pass's level): at config
-// 5 it skips 1.6 % more tile pairs than 45 (0.55 ms of the density pass) and sends 4
-// rows instead of 1 to the recompute (tools/density_skip_probe.sh).
-constexpr float kDensitySkipHalfR2 = 41.5f;
+// than 2^-24 of its term mass.  The threshold trades skipped tiles against rows sent
+// to the recompute: 45 / 43 / 41.5 give config 5's density pass 12.2 / 11.9 / 11.6 ms
+// but config 4 (Laplace-fused) 2.10 / 2.06 / 2.22 ms per call (1 / ~3 / 7 recomputed
+// rows there); 43 is the best of both (tools/density_skip_probe.sh).
+constexpr float kDensitySkipHalfR2 = 43.0f;
 float density_skip_half_r2() {   // (FKDE_DENSITY_SKIP: debug override for A/B runs)
     static const float v = [] {
         const char* e = std::getenv("FKDE_DENSITY_SKIP");

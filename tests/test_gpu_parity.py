@@ -691,7 +691,7 @@ def test_spatial_order_matches_input_order(port, n, d, h):
 def test_tile_skipping_is_exact(port, n):
     # score pass: skipped tile pairs contribute exact zeros (fp16 P), so the spatial
     # order with skipping (FKDE_OPT_SPATIAL=1) and without (3) give the same bits for
-    # the scores and x^SD.  Density pass: a skipped pair has phi < 2^-41 and a row
+    # the scores and x^SD.  Density pass: a skipped pair has phi < 2^-42.5 and a row
     # keeps its skip only if the skipped mass bound is 2^-24 of its own mass (else
     # it is recomputed directly), so densities agree to that bound plus the fp32
     # reassociation of the visited tiles' sums
