@@ -78,11 +78,14 @@ enum {
                                  the default (~256 columns)                      */
     FKDE_OPT_TRACE_PTR = 6,   /* debug: device pointer (32*8*256 int64) receiving
                                  clock64 stamps of the score kernel's block 0   */
-    FKDE_OPT_SPATIAL = 7,     /* score pass on a spatial (Morton / principal-axis)
-                                 order of the points with exact-zero tile skipping:
+    FKDE_OPT_SPATIAL = 7,     /* score and density passes on a spatial (Morton /
+                                 principal-axis) order of the points, skipping the
+                                 tile pairs proven / checked to contribute nothing
+                                 (score: exact zeros; density: < 2^-24 of a row's
+                                 mass, else the row is recomputed directly):
                                  0 = auto (n >= 32768), 1 = always, 2 = never,
                                  3 = the order without skipping (tests: skipping
-                                 must not change a bit)                          */
+                                 must not change a score bit)                    */
     FKDE_OPT_PDL = 8          /* 1 (default) = launch the kernel chain with
                                  programmatic dependent launch; 0 = plain launches */
 };
