@@ -299,6 +299,14 @@ int choose_splits(const Options& o, size_t row_tiles, size_t col_tiles, int ctas
 
 inline unsigned grid1(size_t n, unsigned bs) { return static_cast<unsigned>((n + bs - 1) / bs); }
 
+double risk_half_norm() {   // (FKDE_RISK_HALF_NORM: debug override for accuracy probes)
+    static const double v = [] {
+        const char* e = std::getenv("FKDE_RISK_HALF_NORM");
+        return e && *e ? std::atof(e) : kRiskHalfNorm;
+    }();
+    return v;
+}
+
 // Kernel-chain launch with programmatic dependent launch (layout.cuh: every chain
 // kernel waits on griddepcontrol before touching global memory), so each kernel's
 // launch and prologue (block scheduling, barrier init, TMEM allocation) overlap
@@ -418,7 +426,7 @@ Status pack_args(Device& D, const double* x, size_t rows, int d, int format, boo
     a.out = out.as<uint4>();
     a.a_offset = a_offset;
     a.risk = format == 0 ? D.risk.as<uint8_t>() : nullptr;   // row side: spread flags
-    a.risk_half_norm = kRiskHalfNorm;
+    a.risk_half_norm = risk_half_norm();
     *rows_padded = rp;
     return {};
 }
