@@ -829,3 +829,38 @@ def test_repeat_calls_are_bitwise_under_dynamic_scheduling(ctx, port, kind):
     for o in outs[1:]:
         for a, b in zip(outs[0], o):
             assert np.array_equal(a, b), float(np.max(np.abs(a - b)))
+
+
+@pytest.mark.parametrize("d,n,m,hs,seed", [(2, 33000, 3000, 0.35, 11), (5, 40961, 2049, 0.8, 12),
+                                           (9, 36000, 5000, 1.3, 13), (16, 65600, 777, 2.0, 14)])
+def test_spatial_path_other_dims(port, d, n, m, hs, seed):
+    # the spatial order + tile skipping (n >= 32768) on dimensions other than the
+    # BASELINE's 16, ragged sizes (not multiples of the 128 / 96-point tiles), a
+    # clustered input: SD-KDE, KDE and Laplace on row subsamples vs the oracle
+    rng = np.random.default_rng(seed)
+    centres = rng.normal(scale=4.0, size=(6, d))
+    tr = centres[rng.integers(0, 6, n)] + rng.normal(size=(n, d))
+    q = centres[rng.integers(0, 6, m)] + rng.normal(size=(m, d)) * 1.3
+    h = hs * np.sqrt(d / 2.0)
+    c = fk.Context([0])
+    r = fk.sdkde_flash(tr, q, fk.Bandwidth.uniform(h), ctx=c)
+    s = fk.score_flash(tr, h, ctx=c).values
+    st = c.skip_stats()
+    kde = fk.kde_flash(tr, q, h, ctx=c).values
+    lap = fk.kde_flash(tr, q, h, fk.KernelKind.LaplaceCorrected, True, ctx=c).values
+    c.close()
+    assert st["spatial_order"]
+    rows = np.linspace(0, n - 1, 256).astype(int)
+    qs = np.linspace(0, m - 1, 256).astype(int)
+    th = os.cpu_count()
+    ref_s = port.score_naive(tr, tr[rows], h, threads=th)
+    ref_deb = tr[rows] + 0.5 * h * h * ref_s
+    e = dict(score=max_rowwise_rel(s[rows], ref_s),
+             debiased=max_rowwise_rel(r.debiased_samples.values[rows], ref_deb),
+             kde=max_component_rel(kde[qs], port.kde_naive(tr, q[qs], h, threads=th)),
+             laplace=max_rel_vs_peak(lap[qs], port.laplace_naive(tr, q[qs], h, threads=th)),
+             sdkde=max_component_rel(r.values[qs],
+                                     port.kde_naive(r.debiased_samples.values, q[qs], h, threads=th)))
+    _report(f"spatial_d{d}", skipped=st["tiles_skipped"] / max(st["tiles_total"], 1), **e)
+    assert e["score"] < TOL_SCORE and e["debiased"] < TOL_DEB
+    assert e["kde"] < TOL_DENS and e["laplace"] < TOL_LAP and e["sdkde"] < TOL_DENS
