@@ -884,9 +884,11 @@ pairwise_tc_kernel(PairArgs args) {
                 const uint32_t ts = lane_addr + sb * Cfg::kNCol;
                 const float2 dsc2 = make_float2(dsc, dsc);
                 if constexpr (kScore) {
-                    const int jdiag = (rel >= drel_lo && rel <= drel_hi)
-                                          ? static_cast<int>(jd0 - (long long)rel * Cfg::kNCol)
-                                          : -1;   // this row's diagonal column (if in this tile)
+                    // the row tile's diagonal crosses this column tile (warp-uniform: a
+                    // plain branch per chunk, no vote); jdiag = this row's diagonal
+                    // column, masked below where it lies in the chunk
+                    const bool diag_tile = rel >= drel_lo && rel <= drel_hi;
+                    const int jdiag = diag_tile ? static_cast<int>(jd0 - (long long)rel * Cfg::kNCol) : -1;
                     const float2 neg1 = make_float2(-1.f, -1.f);
                     const float2 vk2 = make_float2(8193.f, 8193.f);   // 2^13 + 1
                     (void)vk2;
@@ -896,7 +898,7 @@ pairwise_tc_kernel(PairArgs args) {
                         ptx::tmem_ld32(ts + ch * 32, v);
                         ptx::tmem_ld_wait();
                         if (ch == 0) FKDE_TRACE(6, sidx);
-                        if (__any_sync(0xffffffffu, jdiag >= 0)) {
+                        if (diag_tile) {
 #pragma unroll
                             for (int c = 0; c < 32; ++c)    // -inf -> phi = 0
                                 v[c] = ptx::sel_eq(v[c], c + ch * 32, jdiag, 0xFF800000u);
