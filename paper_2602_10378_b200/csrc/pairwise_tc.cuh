@@ -99,6 +99,12 @@ struct PairArgs {
 // log2 phi' (S * dscale, with the 2^15 offset) below which both fp16 halves of
 // phi' are exactly zero (phi' < 2^-25 rounds to zero; one unit of margin for ex2.approx)
 constexpr float kSkipLog2 = -26.0f;
+// score epilogue: unroll factor of the per-tile loop over 32-column chunks (1: fully
+// unrolled, 3, made the score phase ~2 % slower in an interleaved A/B)
+#ifndef FKDE_SCORE_CH_UNROLL
+#define FKDE_SCORE_CH_UNROLL 1
+#endif
+constexpr int kScoreChUnroll = FKDE_SCORE_CH_UNROLL;
 // score pass on the spatial order: column tiles per B2 group (ones columns 16 .. 16 + 2^glog - 1)
 #ifndef FKDE_B2_GROUP_LOG2
 #define FKDE_B2_GROUP_LOG2 3
@@ -892,7 +898,7 @@ pairwise_tc_kernel(PairArgs args) {
                     const float2 neg1 = make_float2(-1.f, -1.f);
                     const float2 vk2 = make_float2(8193.f, 8193.f);   // 2^13 + 1
                     (void)vk2;
-#pragma unroll 1
+#pragma unroll kScoreChUnroll
                     for (int ch = 0; ch < Cfg::kNCol / 32; ++ch) {
                         uint32_t v[32];
                         ptx::tmem_ld32(ts + ch * 32, v);
