@@ -186,6 +186,7 @@ struct Device {
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;       // host copies that overlap the next pass
     cudaEvent_t ev_side_in = nullptr, ev_side_out = nullptr;
+    cudaEvent_t ev_y_in = nullptr, ev_y = nullptr;   // SD-KDE: query upload on the side stream
     ncclComm_t comm = nullptr;
     bool attrs_set = false;
     DevBuf X, Y, opA, opB, opB2, part0, part1, xsd, out, aux0, aux1, colpart, scal, err, flags;
@@ -1061,10 +1062,22 @@ Status run_job(Device& D, const Options& o, const Job& J) {
                                  D.stream));
         dX = D.X.as<double>();
     }
+    bool y_async = false;
     if (J.m && !dY) {
         STATUS_TRY(ensure(D.Y, J.m * d * sizeof(double)));
-        CUDA_TRY(cudaMemcpyAsync(D.Y.p, J.hY, J.m * d * sizeof(double), cudaMemcpyHostToDevice,
-                                 D.stream));
+        if (J.kind == Job::kSdkde) {
+            // the queries are first read by the density pass: their upload runs on the
+            // side stream once X's has finished, overlapping the score pass
+            CUDA_TRY(cudaEventRecord(D.ev_y_in, D.stream));
+            CUDA_TRY(cudaStreamWaitEvent(D.side, D.ev_y_in, 0));
+            CUDA_TRY(cudaMemcpyAsync(D.Y.p, J.hY, J.m * d * sizeof(double), cudaMemcpyHostToDevice,
+                                     D.side));
+            CUDA_TRY(cudaEventRecord(D.ev_y, D.side));
+            y_async = true;
+        } else {
+            CUDA_TRY(cudaMemcpyAsync(D.Y.p, J.hY, J.m * d * sizeof(double), cudaMemcpyHostToDevice,
+                                     D.stream));
+        }
         dY = D.Y.as<double>();
     }
     STATUS_TRY(ensure(D.scal, 2 * sizeof(PassScalars)));
@@ -1105,6 +1118,7 @@ Status run_job(Device& D, const Options& o, const Job& J) {
             }
             // sc_q: same centring mean (copied from sc_s by scale_two), fresh scale
             // (x_sd is already centred)
+            if (y_async) CUDA_TRY(cudaStreamWaitEvent(D.stream, D.ev_y, 0));
             STATUS_TRY(query_program(D, o, J, D.xsd.as<double>(), true, dY, sc_s, sc_q,
                                      FKDE_KERNEL_GAUSSIAN, 1));
             break;
@@ -1243,6 +1257,8 @@ Status init_device(Device& D, int dev, int rank, int world) {
     CUDA_TRY(cudaStreamCreateWithFlags(&D.side, cudaStreamNonBlocking));
     CUDA_TRY(cudaEventCreateWithFlags(&D.ev_side_in, cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&D.ev_side_out, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&D.ev_y_in, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&D.ev_y, cudaEventDisableTiming));
     return {};
 }
 
@@ -1368,6 +1384,8 @@ void fkde_gpu_destroy(fkde_gpu_ctx* ctx) {
         if (D.side) cudaStreamDestroy(D.side);
         if (D.ev_side_in) cudaEventDestroy(D.ev_side_in);
         if (D.ev_side_out) cudaEventDestroy(D.ev_side_out);
+        if (D.ev_y_in) cudaEventDestroy(D.ev_y_in);
+        if (D.ev_y) cudaEventDestroy(D.ev_y);
     }
     delete ctx;
 }
