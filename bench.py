@@ -329,13 +329,15 @@ def run_ours(args):
     # the engine's phase events on (they make the call run eagerly: single-rank
     # device calls are otherwise replayed from a captured CUDA graph)
     ctx.set_option(N.OPT_TIMING, 1)
-    score_ms, query_ms = [], []
+    score_ms, query_ms, kern_ms = [], [], []
     for _ in range(2):
         step()
         t = ctx.last_timing()  # syncs on this step's last event
         score_ms.append(t[N.T_SCORE])
         query_ms.append(t[N.T_QUERY])
+        kern_ms.append(ctx.last_kernel_timing())   # events bracketing each pass kernel
     ctx.set_option(N.OPT_TIMING, 0)
+    kern_avg = [float(np.mean([k[i] for k in kern_ms])) for i in range(N.KT_COUNT)]
     skip = ctx.skip_stats()   # tile skipping of the last score pass (this rank)
 
     # e2e through the host C ABI: H2D of this step's inputs and D2H of its results
@@ -381,14 +383,15 @@ def run_ours(args):
     out_ok = out_ok and bool(np.array_equal(gO, pO.numpy()))
 
     # max over ranks
-    vals = torch.tensor([dev_ms, e2e_s, e2e_pg_s, float(np.mean(score_ms)), float(np.mean(query_ms))],
-                        dtype=torch.float64, device=dev)
+    vals = torch.tensor([dev_ms, e2e_s, e2e_pg_s, float(np.mean(score_ms)), float(np.mean(query_ms))]
+                        + kern_avg, dtype=torch.float64, device=dev)
     if dist:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
         lsum = torch.tensor([launches], dtype=torch.float64, device=dev)
         dist.all_reduce(lsum)
         launches = int(lsum.item())
-    dev_ms, e2e_s, e2e_pg_s, score_avg, query_avg = [float(v) for v in vals.tolist()]
+    dev_ms, e2e_s, e2e_pg_s, score_avg, query_avg = [float(v) for v in vals.tolist()[:5]]
+    k_score, k_check, k_density = [float(v) for v in vals.tolist()[5:8]]
 
     if rank == 0:
         ms_step = dev_ms / args.steps
@@ -402,13 +405,17 @@ def run_ours(args):
         # work = every (row, column) pair of this rank's rows; executed work = the
         # pairs of the tiles the pass did not prove / check to be exact zeros
         # (128 x 96 per score tile, 128 x 128 per density tile).
+        # the dominant kernel's own launch, timed by CUDA events bracketing it on the
+        # engine's stream (fkde_gpu_last_kernel_timing); the whole phase beside it
         sd = job == "sdkde"
         if sd:
-            rows_rank, st, tile_pairs, phase_ms = -(-n // world), skip, 128 * 96, score_avg
-            kname = "score phase: pairwise_tc_kernel<Check> + <Score>"
+            rows_rank, st, tile_pairs = -(-n // world), skip, 128 * 96
+            phase_ms = k_score if k_score > 0 else score_avg
+            kname = "pairwise_tc_kernel<Score> (score pass)"
         else:
-            rows_rank, st, tile_pairs, phase_ms = -(-m // world), skip["density"], 128 * 128, query_avg
-            kname = f"density pass: pairwise_tc_kernel<{'Laplace' if job == 'laplace' else 'Gauss'}>"
+            rows_rank, st, tile_pairs = -(-m // world), skip["density"], 128 * 128
+            phase_ms = k_density if k_density > 0 else query_avg
+            kname = f"pairwise_tc_kernel<{'Laplace' if job == 'laplace' else 'Gauss'}> (density pass)"
         exps = rows_rank * n
         exec_tiles = max(st["tiles_total"] - st["tiles_skipped"], 0) if st["spatial_order"] \
             else st["tiles_total"] or -(-rows_rank // 128) * -(-n // (tile_pairs // 128))
@@ -440,6 +447,9 @@ def run_ours(args):
             "parallelism": (f"dp{world}: score rows sharded, 1 NCCL allgather of debiased samples, "
                             f"queries sharded" if sd else f"dp{world}: queries sharded, samples replicated"),
             "phases_ms": {"score_pass": score_avg, "density_pass": query_avg},
+            "kernels_ms": {"score": k_score, "check": k_check, "density": k_density,
+                           "note": "CUDA events bracketing each pass kernel on the engine's "
+                                   "stream (phases include the planning kernels around them)"},
             # the reference's own performance model of this run:
             # paper-model pipeline FLOPs (4d+12+d/4+3/2) k^2 (perfmodel.cpp:62-67) and
             # the runtime sweep's model_flops (sweep.cpp:74-90), with the utilization
@@ -472,7 +482,7 @@ def run_ours(args):
                              "pairs_per_s_G": algorithmic, "pairs": exps,
                              "vs_full_mufu_roof": algorithmic / peak,
                              "note": "every (row, column) pair of the result per second of the "
-                                     "dominant phase; above 1 because tile pairs whose every pair "
+                                     "dominant kernel; above 1 because tile pairs whose every pair "
                                      "contributes exactly zero (score: fp16 P representation; "
                                      "density: below 2^-24 of the row's mass, else recomputed) "
                                      "are proven (box bound) or checked (GEMM1 max) and skipped"},

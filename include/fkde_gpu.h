@@ -123,6 +123,16 @@ int fkde_gpu_world(const fkde_gpu_ctx* ctx, int* rank, int* world);
 void* fkde_gpu_stream(fkde_gpu_ctx* ctx);
 /* device timings of the last call (needs FKDE_OPT_TIMING=1); n <= FKDE_T_COUNT */
 int fkde_gpu_last_timing(const fkde_gpu_ctx* ctx, float* ms, int n);
+/* per-kernel device times of the last call (needs FKDE_OPT_TIMING=1): CUDA events
+ * bracketing each tensor-core pass kernel on the engine's stream, ms, 0 where the
+ * kernel did not run; n <= FKDE_KT_COUNT */
+enum {
+    FKDE_KT_SCORE = 0,    /* pairwise_tc_kernel<Score>                         */
+    FKDE_KT_CHECK = 1,    /* pairwise_tc_kernel<Check> (score tile skipping)   */
+    FKDE_KT_DENSITY = 2,  /* pairwise_tc_kernel<Gauss|Laplace> (last launch)   */
+    FKDE_KT_COUNT = 3
+};
+int fkde_gpu_last_kernel_timing(const fkde_gpu_ctx* ctx, float* ms, int n);
 /* number of kernels this library launched during the last call (this rank) */
 int64_t fkde_gpu_last_launch_count(const fkde_gpu_ctx* ctx);
 /* tile skipping of the last call on device 0 (synchronises); fills

@@ -35,11 +35,13 @@ OPT_PDL = 8
 ENGINE_TC = 0
 
 T_PREP, T_SCORE, T_FINALIZE, T_GATHER, T_QUERY, T_REDUCE, T_TOTAL, T_COUNT = range(8)
+KT_SCORE, KT_CHECK, KT_DENSITY, KT_COUNT = range(4)   # FKDE_KT_*
 
 EXPORTED_SYMBOLS = (
     "fkde_gpu_device_count", "fkde_gpu_create", "fkde_gpu_nccl_unique_id",
     "fkde_gpu_create_rank", "fkde_gpu_destroy", "fkde_gpu_last_error", "fkde_gpu_set_option",
-    "fkde_gpu_world", "fkde_gpu_stream", "fkde_gpu_last_timing", "fkde_gpu_last_launch_count",
+    "fkde_gpu_world", "fkde_gpu_stream", "fkde_gpu_last_timing", "fkde_gpu_last_kernel_timing",
+    "fkde_gpu_last_launch_count",
     "fkde_gpu_score", "fkde_gpu_score_accumulate", "fkde_gpu_kde", "fkde_gpu_sdkde",
     "fkde_gpu_estimate", "fkde_gpu_pairwise_sq_dists", "fkde_gpu_sdkde_device",
     "fkde_gpu_kde_device", "fkde_gpu_score_device", "fkde_gpu_shard_range",
@@ -83,6 +85,7 @@ def _declare(lib):
     lib.fkde_gpu_stream.argtypes = [_vp]
     lib.fkde_gpu_stream.restype = _vp
     lib.fkde_gpu_last_timing.argtypes = [_vp, ctypes.POINTER(ctypes.c_float), ctypes.c_int]
+    lib.fkde_gpu_last_kernel_timing.argtypes = [_vp, ctypes.POINTER(ctypes.c_float), ctypes.c_int]
     lib.fkde_gpu_last_launch_count.argtypes = [_vp]
     lib.fkde_gpu_last_launch_count.restype = ctypes.c_int64
     lib.fkde_gpu_workspace_bytes.argtypes = [_vp, _szp]

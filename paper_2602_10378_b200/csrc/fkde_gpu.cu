@@ -187,6 +187,9 @@ struct Device {
     cudaStream_t side = nullptr;       // host copies that overlap the next pass
     cudaEvent_t ev_side_in = nullptr, ev_side_out = nullptr;
     cudaEvent_t ev_y_in = nullptr, ev_y = nullptr;   // SD-KDE: query upload on the side stream
+    // FKDE_OPT_TIMING: events bracketing each tensor-core pass kernel (FKDE_KT_*)
+    cudaEvent_t kev[2 * FKDE_KT_COUNT] = {};
+    bool kran[FKDE_KT_COUNT] = {};
     ncclComm_t comm = nullptr;
     bool attrs_set = false;
     DevBuf X, Y, opA, opB, opB2, part0, part1, xsd, out, aux0, aux1, colpart, scal, err, flags;
@@ -347,8 +350,18 @@ Status launch_pairwise(Device& D, const Options& o, const PairArgs& a, size_t n_
         if (o.max_ctas > 0) grid = std::min(grid, o.max_ctas);
         PairArgs b = a;
         b.sched = D.sched.as<unsigned int>() + 2 * MODE;   // (ensure_call_scratch)
+        const int kt = MODE == kModeScore ? FKDE_KT_SCORE : (MODE == kModeCheck ? FKDE_KT_CHECK : FKDE_KT_DENSITY);
+        if (o.timing) {
+            if (!D.kev[0])
+                for (auto& e : D.kev) CUDA_TRY(cudaEventCreate(&e));
+            CUDA_TRY(cudaEventRecord(D.kev[2 * kt], D.stream));
+        }
         CUDA_TRY(launch_chain(o.pdl, pairwise_tc_kernel<MODE>, dim3(grid), dim3(Cfg::kThreads),
                               Cfg::kSmemBytes, D.stream, b));
+        if (o.timing) {
+            CUDA_TRY(cudaEventRecord(D.kev[2 * kt + 1], D.stream));
+            D.kran[kt] = true;
+        }
     }
     ++D.launches;
     CUDA_TRY(cudaGetLastError());
@@ -1031,6 +1044,7 @@ Status query_program(Device& D, const Options& o, const Job& J, const double* dC
 Status run_job(Device& D, const Options& o, const Job& J) {
     CUDA_TRY(cudaSetDevice(D.dev));
     D.launches = 0;
+    for (bool& k : D.kran) k = false;
     if (o.timing && !D.ev[0])
         for (auto& e : D.ev) CUDA_TRY(cudaEventCreate(&e));
     record(D, o, FKDE_T_PREP);
@@ -1385,6 +1399,8 @@ void fkde_gpu_destroy(fkde_gpu_ctx* ctx) {
         if (D.ev_side_in) cudaEventDestroy(D.ev_side_in);
         if (D.ev_side_out) cudaEventDestroy(D.ev_side_out);
         if (D.ev_y_in) cudaEventDestroy(D.ev_y_in);
+        for (cudaEvent_t e : D.kev)
+            if (e) cudaEventDestroy(e);
         if (D.ev_y) cudaEventDestroy(D.ev_y);
     }
     delete ctx;
@@ -1519,6 +1535,22 @@ int fkde_gpu_last_skip_stats(fkde_gpu_ctx* ctx, uint64_t* out, size_t n) {
         v[8] = h[1] & 0xFFFFFFFFull;
     }
     for (size_t i = 0; i < n && i < FKDE_SKIP_STATS_COUNT; ++i) out[i] = v[i];
+    return FKDE_OK;
+}
+
+int fkde_gpu_last_kernel_timing(const fkde_gpu_ctx* ctx, float* ms, int n) {
+    if (!ctx || (!ms && n > 0)) return FKDE_INVALID_ARGUMENT;
+    const Device& D = ctx->devs[0];
+    for (int i = 0; i < n && i < FKDE_KT_COUNT; ++i) ms[i] = 0.f;
+    if (!ctx->opt.timing || !D.kev[0]) return FKDE_OK;
+    cudaSetDevice(D.dev);
+    for (int i = 0; i < n && i < FKDE_KT_COUNT; ++i) {
+        if (!D.kran[i]) continue;
+        if (cudaEventSynchronize(D.kev[2 * i + 1]) != cudaSuccess) return FKDE_CUDA_ERROR;
+        float v = 0.f;
+        if (cudaEventElapsedTime(&v, D.kev[2 * i], D.kev[2 * i + 1]) != cudaSuccess) return FKDE_CUDA_ERROR;
+        ms[i] = v;
+    }
     return FKDE_OK;
 }
 

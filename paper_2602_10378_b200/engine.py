@@ -105,6 +105,13 @@ class Context:
         self._lib.fkde_gpu_last_timing(self._h, buf, N.T_COUNT)
         return list(buf)
 
+    def last_kernel_timing(self) -> list:
+        """Device ms of the last call's score / check / density kernels (FKDE_KT_*;
+        needs OPT_TIMING) -- fkde_gpu_last_kernel_timing."""
+        buf = (ctypes.c_float * N.KT_COUNT)()
+        self._lib.fkde_gpu_last_kernel_timing(self._h, buf, N.KT_COUNT)
+        return list(buf)
+
     def last_launch_count(self) -> int:
         return int(self._lib.fkde_gpu_last_launch_count(self._h))
 

@@ -864,3 +864,23 @@ def test_spatial_path_other_dims(port, d, n, m, hs, seed):
     _report(f"spatial_d{d}", skipped=st["tiles_skipped"] / max(st["tiles_total"], 1), **e)
     assert e["score"] < TOL_SCORE and e["debiased"] < TOL_DEB
     assert e["kde"] < TOL_DENS and e["laplace"] < TOL_LAP and e["sdkde"] < TOL_DENS
+
+
+def test_kernel_timing_brackets_the_pass_kernels(port):
+    # fkde_gpu_last_kernel_timing: with OPT_TIMING the score / check / density kernels
+    # are bracketed by events; each is positive where the kernel ran, within its phase
+    tr, q = _mixture_inputs(port, 40000, 5000)
+    h = port.sdkde_bandwidth(tr, port.silverman_prefactor(16))
+    c = fk.Context([0])
+    c.set_option(N.OPT_TIMING, 1)
+    fk.sdkde_flash(tr, q, fk.Bandwidth.uniform(h), ctx=c)
+    k = c.last_kernel_timing()
+    t = c.last_timing()
+    c.set_option(N.OPT_TIMING, 0)
+    fk.kde_flash(tr[:3000], q, h, ctx=c)
+    off = c.last_kernel_timing()
+    c.close()
+    assert k[N.KT_SCORE] > 0 and k[N.KT_CHECK] > 0 and k[N.KT_DENSITY] > 0
+    assert k[N.KT_SCORE] + k[N.KT_CHECK] <= t[N.T_SCORE] * 1.01
+    assert k[N.KT_DENSITY] <= t[N.T_QUERY] * 1.01
+    assert off == [0.0, 0.0, 0.0]
