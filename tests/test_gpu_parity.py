@@ -884,3 +884,42 @@ def test_kernel_timing_brackets_the_pass_kernels(port):
     assert k[N.KT_SCORE] + k[N.KT_CHECK] <= t[N.T_SCORE] * 1.01
     assert k[N.KT_DENSITY] <= t[N.T_QUERY] * 1.01
     assert off == [0.0, 0.0, 0.0]
+
+
+def test_repeated_host_calls_are_bitwise_and_checked(port):
+    # repeated host-buffer calls (reused workspaces) give every result bitwise equal to
+    # a timing-on call, for SD-KDE (with and without x^SD), KDE and the score; the
+    # input checks run on every call (a non-finite input after clean calls is
+    # reported, and the next clean call is clean again)
+    tr, q = _mixture_inputs(port, 3000, 900)
+    h = port.sdkde_bandwidth(tr, port.silverman_prefactor(16))
+    eager = fk.Context([0])
+    eager.set_option(N.OPT_TIMING, 1)   # (timing runs every call eagerly)
+    ref_sd = fk.sdkde_flash(tr, q, fk.Bandwidth.uniform(h), ctx=eager)
+    ref_kde = fk.kde_flash(tr, q, h, ctx=eager).values
+    ref_s = fk.score_flash(tr, h, ctx=eager).values
+    eager.close()
+    c = fk.Context([0])
+    for _ in range(4):
+        r = fk.sdkde_flash(tr, q, fk.Bandwidth.uniform(h), ctx=c)
+        assert np.array_equal(r.values, ref_sd.values)
+        assert np.array_equal(r.debiased_samples.values, ref_sd.debiased_samples.values)
+        assert np.array_equal(fk.kde_flash(tr, q, h, ctx=c).values, ref_kde)
+        assert np.array_equal(fk.score_flash(tr, h, ctx=c).values, ref_s)
+    lib = N.load()
+    out = np.empty(900)
+    dp = ctypes.POINTER(ctypes.c_double)
+    idx = ctypes.c_size_t(0)
+    for _ in range(3):   # densities only (no x^SD): its own graph
+        rc = lib.fkde_gpu_sdkde(c.handle, tr.ctypes.data_as(dp), 3000, q.ctypes.data_as(dp), 900, 16,
+                                h, h, out.ctypes.data_as(dp), None, ctypes.byref(idx))
+        assert rc == N.OK and np.array_equal(out, ref_sd.values)
+    bad = tr.copy()
+    bad[17, 3] = np.nan
+    rc = lib.fkde_gpu_sdkde(c.handle, bad.ctypes.data_as(dp), 3000, q.ctypes.data_as(dp), 900, 16,
+                            h, h, out.ctypes.data_as(dp), None, ctypes.byref(idx))
+    assert rc == N.NON_FINITE
+    rc = lib.fkde_gpu_sdkde(c.handle, tr.ctypes.data_as(dp), 3000, q.ctypes.data_as(dp), 900, 16,
+                            h, h, out.ctypes.data_as(dp), None, ctypes.byref(idx))
+    assert rc == N.OK and np.array_equal(out, ref_sd.values)
+    c.close()
